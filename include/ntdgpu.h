@@ -1,0 +1,146 @@
+/*
+ * ntdgpu.h -- C ABI of the B200-native NTD-PCG hot path (libntdgpu.so).
+ *
+ * Drop-in boundary for the reference package `ntdprecon`
+ * (/root/reference/pkg/src/ntdprecon).  Every entry point replaces one numba
+ * kernel family of the reference (cited per function) and is bound from
+ * Python with ctypes by paper_1909_09771_b200/_lib.py.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers (fp64 unless stated), batch-major:
+ *      banded operator / factor arrays  (B, 7, N)   system stride 7N, band stride N
+ *      vectors                          (B, N)      system stride N
+ *    with N = nx*ny*nz and row r = i + nx*j + nx*ny*k (i fastest), exactly the
+ *    reference layout (banded_core.py:36-62).  Band order of an operator:
+ *    -nxy,-nx,-1,0,+1,+nx,+nxy (banded_core.py:44).  Band order of an NTD
+ *    factor: l1,u1,l2,u2,l3,u3,m_recip (ntd_factor.py:461).
+ *  - `active` (int32[B], device, may be NULL = all active): systems with
+ *    active[s]==0 are skipped by the kernel (their outputs are untouched).
+ *  - `stream` is a cudaStream_t; every call only enqueues work on it (no host
+ *    synchronisation).  Results are bitwise run-to-run deterministic.
+ *  - Return value: 0 on success, NTD_EINVAL for bad arguments, NTD_ENOTSUP for
+ *    a grid the kernels were not instantiated for, NTD_ELAUNCH if the launch
+ *    failed (ntd_last_error() has the CUDA message).
+ *  - Factorisation failures are reported on the device in `status`
+ *    (int64[B][3] = code, plane, row); code 0 ok, 1 zero/non-finite pivot,
+ *    2 non-finite filter weight, 3 non-finite sandwich adjustment -- the
+ *    reference's FactorizationError cases (ntd_factor.py:91-109,133-134,
+ *    247-248,383-386,397-399; ilu0.py:80-83,153-155).
+ */
+#ifndef NTDGPU_H
+#define NTDGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NTD_OK 0
+#define NTD_EINVAL (-1)
+#define NTD_ENOTSUP (-2)
+#define NTD_ELAUNCH (-3)
+
+/* Library identification and the last CUDA error message (host string). */
+const char *ntd_version(void);
+const char *ntd_last_error(void);
+
+/* Largest nx the line kernels are instantiated for. */
+int64_t ntd_max_nx(void);
+
+/* y = A x, bitwise equal to the reference (banded_core.py:95-130, spmv /
+ * _spmv_kernel): same summation order, no FMA contraction. */
+int ntd_spmv(const double *a, const double *x, double *y, int64_t nx,
+             int64_t ny, int64_t nz, int64_t batch, const int32_t *active,
+             void *stream);
+
+/* t = r - A w (precond_pcg.py:58,62: `r - spmv(a, w)`), bitwise. If
+ * z_out != NULL the operand is w + v (formed on the fly, bitwise equal to
+ * numpy's `z = v; z += w`, precond_pcg.py:61) and is also stored to z_out. */
+int ntd_residual(const double *a, const double *r, const double *w,
+                 const double *v, double *z_out, double *t, int64_t nx,
+                 int64_t ny, int64_t nz, int64_t batch, const int32_t *active,
+                 void *stream);
+
+/* out[s] = x_s . y_s (banded_core.py:133-136 dot / 146-147 norm2 when x==y,
+ * fixed-order tree reduction).  work: >= ntd_dot_work_doubles(batch).  If
+ * sqrt_out != 0 the square root is stored (norm2). */
+int64_t ntd_dot_work_doubles(int64_t batch);
+int ntd_dot(const double *x, const double *y, double *out, int sqrt_out,
+            int64_t n, int64_t batch, double *work, const int32_t *active,
+            void *stream);
+
+/* -------- PCG building blocks (precond_pcg.py:68-122) ------------------
+ * Per-system scalar state lives on the device: state (double[B][NTD_ST_N])
+ * and flags (int32[B][NTD_FL_N]).  history: double[B][max_iters]. */
+enum { NTD_ST_RZ = 0, NTD_ST_PAP, NTD_ST_ALPHA, NTD_ST_BETA, NTD_ST_BNORM,
+       NTD_ST_RELRES, NTD_ST_TOL, NTD_ST_N = 8 };
+enum { NTD_FL_ACTIVE = 0, NTD_FL_STATUS, NTD_FL_ITERS, NTD_FL_N = 4 };
+/* NTD_FL_STATUS values */
+enum { NTD_PCG_RUNNING = 0, NTD_PCG_CONVERGED = 1, NTD_PCG_BREAKDOWN = 2,
+       NTD_PCG_NONFINITE = 3 };
+
+/* Initialise: x = 0, r = b, bnorm = ||b||; zero rhs => converged at 0
+ * iterations (precond_pcg.py:84-90).  active[s] mirrors flags[s][ACTIVE]. */
+int ntd_pcg_init(const double *b, double *x, double *r, double *state,
+                 int32_t *flags, int32_t *active, double tol, int64_t n,
+                 int64_t batch, double *work, void *stream);
+/* p = z, rz = r.z (precond_pcg.py:91-94) */
+int ntd_pcg_start(const double *r, const double *z, double *p, double *state,
+                  const int32_t *active, int64_t n, int64_t batch, double *work,
+                  void *stream);
+/* ap = A p; pap = p.ap; breakdown check; alpha = rz/pap (precond_pcg.py:98-102) */
+int ntd_pcg_spmv_alpha(const double *a, const double *p, double *ap,
+                       double *state, int32_t *flags, int32_t *active,
+                       int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+                       double *work, void *stream);
+/* x = alpha p + x; r = -alpha ap + r; relres = ||b - A x||/||b||; history;
+ * convergence / non-finite flags (precond_pcg.py:103-114).  xtmp: scratch
+ * (B,N) that receives the updated x before the true residual is formed. */
+int ntd_pcg_update_residual(const double *a, const double *b, double *x,
+                            double *r, const double *p, const double *ap,
+                            double *state, int32_t *flags, int32_t *active,
+                            double *history, int64_t max_iters, int64_t nx,
+                            int64_t ny, int64_t nz, int64_t batch, double *work,
+                            void *stream);
+/* rz_new = r.z; beta = rz_new/rz; p = beta p + z (precond_pcg.py:116-119) */
+int ntd_pcg_direction(const double *r, const double *z, double *p,
+                      double *state, const int32_t *active, int64_t n,
+                      int64_t batch, double *work, void *stream);
+
+/* -------- NTD preconditioner -------------------------------------------
+ * Setup: the nested twisted filtered factorisation, factor_level3
+ * (ntd_factor.py:351-458, incl. the sandwich diagonal shift :387-399).
+ * a: (B,7,N) operator; pre: (B,7,N) output; status: int64[B][3]. */
+int64_t ntd_factor_work_doubles(int64_t nx, int64_t ny, int64_t nz,
+                                int64_t batch);
+int ntd_factor(const double *a, double *pre, double *work, int64_t *status,
+               int64_t nx, int64_t ny, int64_t nz, int64_t batch, void *stream);
+
+/* Apply: x = B^{-1} b, ntd_apply (ntd_solve.py:188-322).  b is not modified.
+ * work: >= ntd_apply_work_doubles. */
+int64_t ntd_apply_work_doubles(int64_t nx, int64_t ny, int64_t nz,
+                               int64_t batch);
+int ntd_apply(const double *pre, const double *b, double *x, double *work,
+              int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+              const int32_t *active, void *stream);
+
+/* -------- Block ILU0 (ilu0.py) ------------------------------------------
+ * Factor of blkdiag(A[:split,:split], A[split:,split:]) on the 7-band
+ * pattern, build_block_ilu0 (ilu0.py:34-92,126-156); bitwise equal to the
+ * reference.  f: (B,7,N) output.  status: int64[B][3] (code 1, -1, min bad
+ * row).  Requires the structured-grid zero pattern of BandedMatrix
+ * (banded_core.py:39-42); the Python layer validates it. */
+int ntd_ilu0_factor(const double *a, double *f, int64_t split, int64_t *status,
+                    int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+                    void *stream);
+/* z = (LU)^{-1} r per half, ilu0_apply (ilu0.py:95-123,159-169); bitwise.
+ * If acc != NULL, acc += z is also formed (precond_pcg.py:64). */
+int ntd_ilu0_apply(const double *f, int64_t split, const double *r, double *z,
+                   double *acc, int64_t nx, int64_t ny, int64_t nz,
+                   int64_t batch, const int32_t *active, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NTDGPU_H */

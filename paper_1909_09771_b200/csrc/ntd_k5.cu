@@ -1,0 +1,3 @@
+// instantiation of the NTD kernels for K=5 cells per lane (see ntd.cu)
+#include "ntd_kernels.cuh"
+NTD_INSTANTIATE(5)

@@ -1,0 +1,761 @@
+#pragma once
+// ntd.cu -- NTD preconditioner setup (factor_level3) and apply (ntd_apply)
+// on sm_100a.
+//
+// Reference: /root/reference/pkg/src/ntdprecon/ntd_factor.py (setup) and
+// ntd_solve.py (apply).  Mapping (one CTA of 4 warps per system):
+//   level 3 (planes): the two twisted halves (ntd_solve.py:198-221 / :233-253,
+//     ntd_factor.py:436-446) are two warp pairs; the twist plane is handled by
+//     pair 0 between two __syncthreads.
+//   level 2 (lines of a plane, _plane_solve ntd_solve.py:140-185 and
+//     _factor_plane ntd_factor.py:147-219): the two halves are the two warps
+//     of a pair; they meet at the twist line through a named barrier and a
+//     shared-memory exchange of the neighbouring lines.
+//   level 1 (cells of a line): one warp, shuffle scans (ntd_line.cuh).
+// All level-2/3 couplings are diagonal (elementwise per cell), so a line's
+// right-hand side only needs lines that the same lane layout already holds.
+#include "common.cuh"
+#include "ntd_line.cuh"
+
+enum { M_LOWER3 = 0, M_UPPER3 = 1, M_SETUP = 2 };
+
+struct FactorPtrs {
+    const double *l1, *u1, *l2, *u2, *l3, *u3, *mr;
+};
+
+__device__ __forceinline__ FactorPtrs factor_ptrs(const double *pre, i64 n)
+{
+    FactorPtrs f;
+    f.l1 = pre;
+    f.u1 = pre + n;
+    f.l2 = pre + 2 * n;
+    f.u2 = pre + 3 * n;
+    f.l3 = pre + 4 * n;
+    f.u3 = pre + 5 * n;
+    f.mr = pre + 6 * n;
+    return f;
+}
+
+// What a plane solve reads as right-hand side and where it writes.
+struct PlaneIO {
+    // M_LOWER3: rhs = b - [hasM] l3*x[r-nxy] - [hasP] u3*x[r+nxy]; lower and
+    //           final values -> x.
+    // M_UPPER3: rhs = nbrUp ? u3*x[r+nxy] : l3*x[r-nxy]; lower -> xs;
+    //           final: x[r] -= value.
+    // M_SETUP:  rhs = useg[local]; lower -> ylow[local]; final -> out[local].
+    const double *b;
+    double *x, *xs;
+    bool hasM, hasP, nbrUp;
+    const double *useg;
+    double *ylow, *out;
+};
+
+template <int K, int MODE>
+__device__ __forceinline__ void rhs_lower(const FactorPtrs &F, const PlaneIO &io, const LineGeom<K> &g, i64 lb,
+                                          i64 llocal, i64 nxy, double (&rhs)[K], double &rhst)
+{
+#pragma unroll
+    for (int k = 0; k <= K; k++) {
+        bool tw = (k == K);
+        if (!tw && !g.valid(k)) {
+            rhs[k] = 0.0;
+            continue;
+        }
+        int c = tw ? g.t : g.cell(k);
+        i64 r = lb + c;
+        double v;
+        if (MODE == M_LOWER3) {
+            v = io.b[r];
+            if (io.hasM) v -= F.l3[r] * io.x[r - nxy];
+            if (io.hasP) v -= F.u3[r] * io.x[r + nxy];
+        } else if (MODE == M_UPPER3) {
+            v = io.nbrUp ? F.u3[r] * io.x[r + nxy] : F.l3[r] * io.x[r - nxy];
+        } else {
+            v = io.useg[llocal + c];
+        }
+        if (tw)
+            rhst = v;
+        else
+            rhs[k] = v;
+    }
+}
+
+template <int K, int MODE>
+__device__ __forceinline__ void load_lowerstore(const PlaneIO &io, const LineGeom<K> &g, i64 lb, i64 llocal,
+                                                double (&y)[K], double &yt)
+{
+    if (MODE == M_LOWER3)
+        load_slots(g, io.x, lb, y, yt);
+    else if (MODE == M_UPPER3)
+        load_slots(g, io.xs, lb, y, yt);
+    else
+        load_slots(g, io.ylow, llocal, y, yt);
+}
+
+template <int K, int MODE>
+__device__ __forceinline__ void store_lower(const PlaneIO &io, const LineGeom<K> &g, i64 lb, i64 llocal,
+                                            const double (&y)[K], double yt)
+{
+    if (MODE == M_LOWER3)
+        store_slots(g, io.x, lb, y, yt);
+    else if (MODE == M_UPPER3)
+        store_slots(g, io.xs, lb, y, yt);
+    else
+        store_slots(g, io.ylow, llocal, y, yt);
+}
+
+template <int K, int MODE>
+__device__ __forceinline__ void finalize(const PlaneIO &io, const LineGeom<K> &g, i64 lb, i64 llocal,
+                                         const double (&v)[K], double vt)
+{
+    if (MODE == M_LOWER3) {
+        store_slots(g, io.x, lb, v, vt);
+    } else if (MODE == M_UPPER3) {
+        double xo[K], xot;
+        load_slots(g, io.x, lb, xo, xot);
+        double nv[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) nv[k] = xo[k] - v[k];
+        store_slots(g, io.x, lb, nv, xot - vt);
+    } else {
+        store_slots(g, io.out, llocal, v, vt);
+    }
+}
+
+// Twisted solve of one factored plane (ntd_solve.py:140-185) by a warp pair.
+// w2: warp within the pair (0 = ascending lines, 1 = descending lines).
+// ex: this pair's shared exchange buffer [2 parity][2 warps][32K+1].
+template <int K, int MODE>
+__device__ void plane_solve(const FactorPtrs &F, const PlaneIO &io, i64 pb, int nx, int ny, int w2, int bar_id,
+                            double *ex, int &parity)
+{
+    const int lane = threadIdx.x & 31;
+    const LineGeom<K> g(nx, lane);
+    const i64 nxy = (i64)nx * ny;
+    const int t2 = (ny - 1) / 2;
+    double xprev[K], xprevt = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; k++) xprev[k] = 0.0;
+    // ---------------- level-2 lower sweep, ends inward (ntd_solve.py:147-171)
+    const int cnt = w2 == 0 ? t2 : (ny - 1 - t2);
+    const double *cplL = w2 == 0 ? F.l2 : F.u2;  // b -= l2*x[r-nx] | u2*x[r+nx]
+    for (int i = 0; i < cnt; i++) {
+        int q = w2 == 0 ? i : ny - 1 - i;
+        i64 lb = pb + (i64)q * nx, ll = (i64)q * nx;
+        double mr[K], oL[K], oU[K], mrt, l1t, u1t;
+        load_line_factors(g, F.mr, F.l1, F.u1, lb, mr, oL, oU, mrt, l1t, u1t);
+        double rhs[K], rhst;
+        rhs_lower<K, MODE>(F, io, g, lb, ll, nxy, rhs, rhst);
+        if (i > 0) {
+            double c[K], ct;
+            load_slots(g, cplL, lb, c, ct);
+#pragma unroll
+            for (int k = 0; k < K; k++) rhs[k] -= c[k] * xprev[k];
+            rhst -= ct * xprevt;
+        }
+        double x[K], xt;
+        line_solve(g, mr, oL, oU, rhs, rhst, mrt, l1t, u1t, x, xt);
+        store_lower<K, MODE>(io, g, lb, ll, x, xt);
+#pragma unroll
+        for (int k = 0; k < K; k++) xprev[k] = x[k];
+        xprevt = xt;
+    }
+    // ---------------- exchange the lines next to the twist
+    const int stride = 32 * K + 1;
+    double *mine = ex + (parity * 2 + w2) * stride;
+    double *other = ex + (parity * 2 + (1 - w2)) * stride;
+#pragma unroll
+    for (int k = 0; k < K; k++) mine[lane * K + k] = xprev[k];
+    if (lane == 0) mine[32 * K] = xprevt;
+    named_bar(bar_id, 64);
+    parity ^= 1;
+    double xo[K], xot = other[32 * K];
+#pragma unroll
+    for (int k = 0; k < K; k++) xo[k] = other[lane * K + k];
+    // x_{t2-1} lives in warp 0, x_{t2+1} in warp 1
+    double xa[K], xat, xd[K], xdt;
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        xa[k] = w2 == 0 ? xprev[k] : xo[k];
+        xd[k] = w2 == 0 ? xo[k] : xprev[k];
+    }
+    xat = w2 == 0 ? xprevt : xot;
+    xdt = w2 == 0 ? xot : xprevt;
+    // ---------------- twist line (ntd_solve.py:172-177), both warps
+    double xT[K], xTt;
+    {
+        const int q = t2;
+        i64 lb = pb + (i64)q * nx, ll = (i64)q * nx;
+        double mr[K], oL[K], oU[K], mrt, l1t, u1t;
+        load_line_factors(g, F.mr, F.l1, F.u1, lb, mr, oL, oU, mrt, l1t, u1t);
+        double rhs[K], rhst;
+        rhs_lower<K, MODE>(F, io, g, lb, ll, nxy, rhs, rhst);
+        if (t2 > 0) {
+            double c[K], ct;
+            load_slots(g, F.l2, lb, c, ct);
+#pragma unroll
+            for (int k = 0; k < K; k++) rhs[k] -= c[k] * xa[k];
+            rhst -= ct * xat;
+        }
+        if (t2 < ny - 1) {
+            double c[K], ct;
+            load_slots(g, F.u2, lb, c, ct);
+#pragma unroll
+            for (int k = 0; k < K; k++) rhs[k] -= c[k] * xd[k];
+            rhst -= ct * xdt;
+        }
+        line_solve(g, mr, oL, oU, rhs, rhst, mrt, l1t, u1t, xT, xTt);
+        if (w2 == 0) finalize<K, MODE>(io, g, lb, ll, xT, xTt);
+    }
+    // ---------------- level-2 upper sweep, twist outward (ntd_solve.py:178-185)
+    double xn[K], xnt = xTt;
+#pragma unroll
+    for (int k = 0; k < K; k++) xn[k] = xT[k];
+    const double *cplU = w2 == 0 ? F.u2 : F.l2;  // bs = u2*x[r+nx] | l2*x[r-nx]
+    for (int i = 0; i < cnt; i++) {
+        int q = w2 == 0 ? t2 - 1 - i : t2 + 1 + i;
+        i64 lb = pb + (i64)q * nx, ll = (i64)q * nx;
+        double mr[K], oL[K], oU[K], mrt, l1t, u1t;
+        load_line_factors(g, F.mr, F.l1, F.u1, lb, mr, oL, oU, mrt, l1t, u1t);
+        double c[K], ct, y[K], yt;
+        load_slots(g, cplU, lb, c, ct);
+        load_lowerstore<K, MODE>(io, g, lb, ll, y, yt);
+        double bs[K], bst = ct * xnt;
+#pragma unroll
+        for (int k = 0; k < K; k++) bs[k] = c[k] * xn[k];
+        double xs[K], xst;
+        line_solve(g, mr, oL, oU, bs, bst, mrt, l1t, u1t, xs, xst);
+#pragma unroll
+        for (int k = 0; k < K; k++) xn[k] = y[k] - xs[k];
+        xnt = yt - xst;
+        finalize<K, MODE>(io, g, lb, ll, xn, xnt);
+    }
+}
+
+// =============================================================== apply
+template <int K>
+__global__ void __launch_bounds__(128) k_ntd_apply(const double *__restrict__ pre, const double *__restrict__ b,
+                                                   double *x, double *work, int nx, int ny, int nz,
+                                                   const int32_t *__restrict__ active)
+{
+    __shared__ double ex[2][2 * 2 * (32 * K + 1)];
+    const i64 sys = blockIdx.x;
+    if (active && !active[sys]) return;
+    const i64 nxy = (i64)nx * ny, n = nxy * nz;
+    const FactorPtrs F = factor_ptrs(pre + sys * 7 * n, n);
+    const int warp = threadIdx.x >> 5, pair = warp >> 1, w2 = warp & 1, bar = 1 + pair;
+    double *myex = ex[pair];
+    int parity = 0;
+    PlaneIO io;
+    io.b = b + sys * n;
+    io.x = x + sys * n;
+    io.xs = work + sys * n;
+    io.useg = nullptr;
+    io.ylow = io.out = nullptr;
+    const int t3 = (nz - 1) / 2;
+    // level-3 lower sweep, both halves (ntd_solve.py:198-221)
+    io.nbrUp = false;
+    if (pair == 0) {
+        for (int p = 0; p < t3; p++) {
+            io.hasM = p > 0;
+            io.hasP = false;
+            plane_solve<K, M_LOWER3>(F, io, (i64)p * nxy, nx, ny, w2, bar, myex, parity);
+        }
+    } else {
+        for (int p = nz - 1; p > t3; p--) {
+            io.hasM = false;
+            io.hasP = p < nz - 1;
+            plane_solve<K, M_LOWER3>(F, io, (i64)p * nxy, nx, ny, w2, bar, myex, parity);
+        }
+    }
+    __syncthreads();
+    // twist plane (ntd_solve.py:222-232)
+    if (pair == 0) {
+        io.hasM = t3 > 0;
+        io.hasP = t3 < nz - 1;
+        plane_solve<K, M_LOWER3>(F, io, (i64)t3 * nxy, nx, ny, w2, bar, myex, parity);
+    }
+    __syncthreads();
+    // level-3 upper sweep (ntd_solve.py:233-253)
+    if (pair == 0) {
+        io.nbrUp = true;
+        for (int p = t3 - 1; p >= 0; p--)
+            plane_solve<K, M_UPPER3>(F, io, (i64)p * nxy, nx, ny, w2, bar, myex, parity);
+    } else {
+        io.nbrUp = false;
+        for (int p = t3 + 1; p < nz; p++)
+            plane_solve<K, M_UPPER3>(F, io, (i64)p * nxy, nx, ny, w2, bar, myex, parity);
+    }
+}
+
+// =============================================================== factor
+// Per-pair global scratch (plane-local, nxy each).
+enum { S_PC0 = 0, S_PC1 = 5, S_W = 10, S_YL, S_BETA, S_QD, S_TDW, S_XW, S_BW, S_PER_PAIR };
+
+struct PairScratch {
+    double *base;
+    i64 nxy;
+    __device__ double *at(int k) const { return base + k * nxy; }
+};
+
+// status codes (ntdgpu.h)
+struct ErrState {
+    int code;
+    i64 plane, row;
+};
+
+__device__ __forceinline__ void set_err(volatile int *ecode, i64 *eplane, i64 *erow, int code, i64 plane, i64 row)
+{
+    if (*ecode == 0) {
+        *eplane = plane;
+        *erow = row;
+        __threadfence_block();
+        *ecode = code;
+    }
+}
+
+// _line_factor (ntd_factor.py:80-110) on one line: exact, sequential pivots.
+// td/tl/tu are global (plane-local) arrays; mr output global.  smem per warp:
+// sd[nx] diag, sc[nx] products, sm[nx] reciprocals.  Returns -1 or bad cell.
+static __device__ int line_factor_warp(const double *__restrict__ td, const double *__restrict__ tl,
+                                const double *__restrict__ tu, double *__restrict__ mr, int nx, double *sd,
+                                double *sc, double *sm)
+{
+    const int lane = threadIdx.x & 31;
+    const int t = (nx - 1) / 2;
+    for (int c = lane; c < nx; c += 32) {
+        sd[c] = td[c];
+        double p = 0.0;
+        if (c < t && c > 0) p = mul_rn(tl[c], tu[c - 1]);
+        if (c > t && c < nx - 1) p = mul_rn(tu[c], tl[c + 1]);
+        sc[c] = p;
+    }
+    __syncwarp();
+    int bad = -1;
+    if (lane == 0) {
+        double m = 0.0;
+        for (int i = 0; i < t; i++) {
+            double piv = (i == 0) ? sd[0] : sub_rn(sd[i], mul_rn(sc[i], m));
+            if (piv == 0.0 || !isfinite(piv)) {
+                bad = i;
+                break;
+            }
+            m = 1.0 / piv;
+            sm[i] = m;
+        }
+    } else if (lane == 16) {
+        double m = 0.0;
+        for (int i = nx - 1; i > t; i--) {
+            double piv = (i == nx - 1) ? sd[i] : sub_rn(sd[i], mul_rn(sc[i], m));
+            if (piv == 0.0 || !isfinite(piv)) {
+                bad = i;
+                break;
+            }
+            m = 1.0 / piv;
+            sm[i] = m;
+        }
+    }
+    int bad_a = __shfl_sync(FULL_MASK, bad, 0);
+    int bad_d = __shfl_sync(FULL_MASK, bad, 16);
+    __syncwarp();
+    if (bad_a >= 0) return bad_a;
+    if (bad_d >= 0) return bad_d;
+    int badt = -1;
+    if (lane == 0) {
+        double piv = sd[t];
+        if (t > 0) piv = sub_rn(piv, mul_rn(mul_rn(tl[t], tu[t - 1]), sm[t - 1]));
+        if (t < nx - 1) piv = sub_rn(piv, mul_rn(mul_rn(tu[t], tl[t + 1]), sm[t + 1]));
+        if (piv == 0.0 || !isfinite(piv))
+            badt = t;
+        else
+            sm[t] = 1.0 / piv;
+    }
+    badt = __shfl_sync(FULL_MASK, badt, 0);
+    __syncwarp();
+    if (badt >= 0) return badt;
+    for (int c = lane; c < nx; c += 32) mr[c] = sm[c];
+    __syncwarp();
+    return -1;
+}
+
+// _correct_line (ntd_factor.py:113-144): line q corrected through factored
+// line m.  P* are the plane's corrected bands (plane-local), L1G/U1G/MRG the
+// plane's factor outputs, TDW/XW/BW scratch.  Returns -1 or bad plane-local row.
+template <int K>
+__device__ i64 correct_line_warp(int q, int m, const double *P_l2, const double *P_u2, double *TDW, double *L1G,
+                                 double *U1G, const double *MRG, double *XW, double *BW, int nx)
+{
+    const int lane = threadIdx.x & 31;
+    const LineGeom<K> g(nx, lane);
+    const i64 sq = (i64)q * nx, sm = (i64)m * nx;
+    const double *src = m < q ? P_u2 : P_l2;
+    for (int c = lane; c < nx; c += 32) BW[sm + c] = src[sm + c];
+    __syncwarp();
+    double mr[K], oL[K], oU[K], mrt, l1t, u1t, rhs[K], rhst, xw[K], xwt;
+    load_line_factors(g, MRG, L1G, U1G, sm, mr, oL, oU, mrt, l1t, u1t);
+    load_slots(g, BW, sm, rhs, rhst);
+    line_solve(g, mr, oL, oU, rhs, rhst, mrt, l1t, u1t, xw, xwt);
+    store_slots(g, XW, sm, xw, xwt);
+    __syncwarp();
+    // beta = w/u where u != 0 (first non-finite -> error)
+    int badk = 0x7fffffff;
+    for (int c = lane; c < nx; c += 32) {
+        double u = BW[sm + c];
+        double bet = u != 0.0 ? XW[sm + c] / u : 0.0;
+        if (!isfinite(bet) && c < badk) badk = c;
+        XW[sm + c] = bet;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) badk = min(badk, __shfl_xor_sync(FULL_MASK, badk, o));
+    __syncwarp();
+    if (badk != 0x7fffffff) return sm + badk;
+    for (int c = lane; c < nx; c += 32) {
+        double rs = m < q ? P_l2[sq + c] : P_u2[sq + c];
+        double bet = XW[sm + c];
+        double inner = sub_rn(mul_rn(2.0, bet), mul_rn(mul_rn(bet, TDW[sm + c]), bet));
+        TDW[sq + c] = sub_rn(TDW[sq + c], mul_rn(mul_rn(rs, inner), BW[sm + c]));
+        if (c >= 1)
+            L1G[sq + c] = add_rn(L1G[sq + c], mul_rn(mul_rn(mul_rn(mul_rn(rs, bet), L1G[sm + c]), XW[sm + c - 1]),
+                                                     BW[sm + c - 1]));
+        if (c + 1 < nx)
+            U1G[sq + c] = add_rn(U1G[sq + c], mul_rn(mul_rn(mul_rn(mul_rn(rs, bet), U1G[sm + c]), XW[sm + c + 1]),
+                                                     BW[sm + c + 1]));
+    }
+    __syncwarp();
+    return -1;
+}
+
+struct FactorCtx {
+    const double *a;  // (7,N) of this system: -nxy,-nx,-1,0,+1,+nx,+nxy
+    double *pre;      // (7,N) output l1,u1,l2,u2,l3,u3,mr
+    i64 n, nxy;
+    int nx, ny, nz;
+};
+
+// _factor_plane (ntd_factor.py:147-219) by a warp pair on the corrected plane
+// bands P (plane-local, 5 arrays).  Returns via err* (pair-shared).
+template <int K>
+__device__ void factor_plane_pair(const FactorCtx &c, i64 pb, const double *P[5], const PairScratch &S, int w2,
+                                  int bar_id, volatile int *ecode, i64 *eplane, i64 *erow, int plane,
+                                  double *lsm, volatile i64 *wbad)
+{
+    const int lane = threadIdx.x & 31;
+    const int nx = c.nx, ny = c.ny, t2 = (ny - 1) / 2;
+    double *L1G = c.pre + pb, *U1G = c.pre + c.n + pb, *MRG = c.pre + 6 * c.n + pb;
+    double *TDW = S.at(S_TDW), *XW = S.at(S_XW), *BW = S.at(S_BW);
+    double *sd = lsm, *sc = lsm + nx, *sm = lsm + 2 * nx;
+    auto init_line = [&](int q) {
+        i64 sq = (i64)q * nx;
+        for (int cc = lane; cc < nx; cc += 32) {
+            TDW[sq + cc] = P[0][sq + cc];
+            L1G[sq + cc] = P[1][sq + cc];
+            U1G[sq + cc] = P[2][sq + cc];
+        }
+        __syncwarp();
+    };
+    // each warp: (code, cell-row) of its first failure
+    int mcode = 0;
+    i64 mrow = -1;
+    const int cnt = w2 == 0 ? t2 : (ny - 1 - t2);
+    for (int i = 0; i < cnt && !mcode; i++) {
+        int q = w2 == 0 ? i : ny - 1 - i;
+        init_line(q);
+        if (i > 0) {
+            i64 st = correct_line_warp<K>(q, w2 == 0 ? q - 1 : q + 1, P[3], P[4], TDW, L1G, U1G, MRG, XW, BW, nx);
+            if (st >= 0) {
+                mcode = 2;
+                mrow = st;
+                break;
+            }
+        }
+        int st = line_factor_warp(TDW + (i64)q * nx, L1G + (i64)q * nx, U1G + (i64)q * nx, MRG + (i64)q * nx, nx,
+                                  sd, sc, sm);
+        if (st >= 0) {
+            mcode = 1;
+            mrow = (i64)q * nx + st;
+        }
+    }
+    if (lane == 0) {
+        wbad[w2] = mcode;
+        wbad[2 + w2] = mrow;
+    }
+    named_bar(bar_id, 64);
+    int c0 = (int)wbad[0], c1 = (int)wbad[1];
+    if (c0 || c1) {
+        if (w2 == 0 && lane == 0) {
+            int cc = c0 ? c0 : c1;
+            i64 rr = wbad[2 + (c0 ? 0 : 1)];
+            set_err(ecode, eplane, erow, cc, plane, pb + rr);
+        }
+        named_bar(bar_id, 64);
+        return;
+    }
+    if (w2 == 0) {
+        const int q = t2;
+        init_line(q);
+        i64 st = -1;
+        int code = 0;
+        if (t2 > 0) {
+            st = correct_line_warp<K>(q, q - 1, P[3], P[4], TDW, L1G, U1G, MRG, XW, BW, nx);
+            if (st >= 0) code = 2;
+        }
+        if (!code && t2 < ny - 1) {
+            st = correct_line_warp<K>(q, q + 1, P[3], P[4], TDW, L1G, U1G, MRG, XW, BW, nx);
+            if (st >= 0) code = 2;
+        }
+        if (!code) {
+            int s2 = line_factor_warp(TDW + (i64)q * nx, L1G + (i64)q * nx, U1G + (i64)q * nx, MRG + (i64)q * nx, nx,
+                                      sd, sc, sm);
+            if (s2 >= 0) {
+                code = 1;
+                st = (i64)q * nx + s2;
+            }
+        }
+        if (code && lane == 0) set_err(ecode, eplane, erow, code, plane, pb + st);
+    }
+    named_bar(bar_id, 64);
+}
+
+// correct_from (ntd_factor.py:378-404) for plane p through factored neighbour
+// m, whose corrected (pre-factor) bands are Q.  Updates P in place.
+template <int K>
+__device__ void correct_from_pair(const FactorCtx &c, int p, int m, double *P[5], const double *Q[5],
+                                  const PairScratch &S, int w2, int bar_id, double *ex, int &parity,
+                                  volatile int *ecode, i64 *eplane, i64 *erow, volatile int *flag)
+{
+    const i64 nxy = c.nxy, n = c.n;
+    const int nx = c.nx;
+    const int tid = threadIdx.x & 63;
+    const FactorPtrs F = factor_ptrs(c.pre, n);
+    const double *useg = (m < p ? c.a + 6 * n : c.a) + (i64)m * nxy;  // u3 | l3 = copies of A's +-nxy
+    const double *rowscale = (m < p ? c.a : c.a + 6 * n) + (i64)p * nxy;
+    double *W = S.at(S_W), *BETA = S.at(S_BETA), *QD = S.at(S_QD);
+    PlaneIO io;
+    io.b = nullptr;
+    io.x = io.xs = nullptr;
+    io.hasM = io.hasP = io.nbrUp = false;
+    io.useg = useg;
+    io.ylow = S.at(S_YL);
+    io.out = W;
+    plane_solve<K, M_SETUP>(F, io, (i64)m * nxy, c.nx, c.ny, w2, bar_id, ex, parity);
+    named_bar(bar_id, 64);
+    // beta (_beta_from :242-249), qw (_plane_band_action :266-274), qd shift (:393-399)
+    int fb = 0, fq = 0;
+    for (i64 k = tid; k < nxy; k += 64) {
+        double u = useg[k], w = W[k];
+        double bet = u != 0.0 ? w / u : 0.0;
+        if (!isfinite(bet)) fb = 1;
+        BETA[k] = bet;
+        double qw = mul_rn(Q[0][k], w);
+        if (k >= 1) qw = add_rn(qw, mul_rn(Q[1][k], W[k - 1]));
+        if (k + 1 < nxy) qw = add_rn(qw, mul_rn(Q[2][k], W[k + 1]));
+        if (k >= nx) qw = add_rn(qw, mul_rn(Q[3][k], W[k - nx]));
+        if (k + nx < nxy) qw = add_rn(qw, mul_rn(Q[4][k], W[k + nx]));
+        double qd = Q[0][k];
+        if (w != 0.0) qd = add_rn(qd, sub_rn(u, qw) / w);
+        if (!isfinite(qd)) fq = 1;
+        QD[k] = qd;
+    }
+    if (fb) flag[0] = 1;
+    if (fq) flag[1] = 1;
+    named_bar(bar_id, 64);
+    if (flag[0] || flag[1]) {
+        if (tid == 0) set_err(ecode, eplane, erow, flag[0] ? 2 : 3, p, -1);
+        named_bar(bar_id, 64);
+        return;
+    }
+    // _plane_correction (ntd_factor.py:222-239)
+    for (i64 k = tid; k < nxy; k += 64) {
+        double rs = rowscale[k], bet = BETA[k];
+        double inner = sub_rn(mul_rn(2.0, bet), mul_rn(mul_rn(bet, QD[k]), bet));
+        P[0][k] = sub_rn(P[0][k], mul_rn(mul_rn(rs, inner), useg[k]));
+        double rb = mul_rn(rs, bet);
+        if (k >= 1) P[1][k] = add_rn(P[1][k], mul_rn(mul_rn(mul_rn(rb, Q[1][k]), BETA[k - 1]), useg[k - 1]));
+        if (k + 1 < nxy) P[2][k] = add_rn(P[2][k], mul_rn(mul_rn(mul_rn(rb, Q[2][k]), BETA[k + 1]), useg[k + 1]));
+        if (k >= nx) P[3][k] = add_rn(P[3][k], mul_rn(mul_rn(mul_rn(rb, Q[3][k]), BETA[k - nx]), useg[k - nx]));
+        if (k + nx < nxy)
+            P[4][k] = add_rn(P[4][k], mul_rn(mul_rn(mul_rn(rb, Q[4][k]), BETA[k + nx]), useg[k + nx]));
+    }
+    named_bar(bar_id, 64);
+}
+
+// plane_bands_of (ntd_factor.py:372-376): d, -1, +1, -nx, +nx of plane p
+static __device__ void load_plane_bands(const FactorCtx &c, int p, double *P[5], int bar_id)
+{
+    const int tid = threadIdx.x & 63;
+    const i64 pb = (i64)p * c.nxy, n = c.n;
+    for (i64 k = tid; k < c.nxy; k += 64) {
+        P[0][k] = c.a[3 * n + pb + k];
+        P[1][k] = c.a[2 * n + pb + k];
+        P[2][k] = c.a[4 * n + pb + k];
+        P[3][k] = c.a[1 * n + pb + k];
+        P[4][k] = c.a[5 * n + pb + k];
+    }
+    named_bar(bar_id, 64);
+}
+
+// factor_one (ntd_factor.py:406-419)
+template <int K>
+__device__ void factor_one_pair(const FactorCtx &c, int p, double *P[5], const PairScratch &S, int w2, int bar_id,
+                                volatile int *ecode, i64 *eplane, i64 *erow, double *lsm, volatile i64 *wbad)
+{
+    const int tid = threadIdx.x & 63;
+    const i64 pb = (i64)p * c.nxy, n = c.n;
+    for (i64 k = tid; k < c.nxy; k += 64) {
+        c.pre[2 * n + pb + k] = P[3][k];
+        c.pre[3 * n + pb + k] = P[4][k];
+    }
+    named_bar(bar_id, 64);
+    const double *Pc[5] = {P[0], P[1], P[2], P[3], P[4]};
+    factor_plane_pair<K>(c, pb, Pc, S, w2, bar_id, ecode, eplane, erow, p, lsm, wbad);
+}
+
+template <int K>
+__global__ void __launch_bounds__(128) k_ntd_factor(const double *__restrict__ a, double *pre, double *work,
+                                                    int64_t *status, int nx, int ny, int nz)
+{
+    extern __shared__ double lsm_all[];  // 4 warps x 3 x nx
+    __shared__ double ex[2][2 * 2 * (32 * K + 1)];
+    __shared__ int ecode_s[2];
+    __shared__ i64 eplane_s[2], erow_s[2];
+    __shared__ i64 wbad_s[2][4];
+    __shared__ int flag_s[2][2];
+    __shared__ int last_p[2];
+    const i64 sys = blockIdx.x;
+    const i64 nxy = (i64)nx * ny, n = nxy * nz;
+    FactorCtx c;
+    c.a = a + sys * 7 * n;
+    c.pre = pre + sys * 7 * n;
+    c.n = n;
+    c.nxy = nxy;
+    c.nx = nx;
+    c.ny = ny;
+    c.nz = nz;
+    const int warp = threadIdx.x >> 5, pair = warp >> 1, w2 = warp & 1, bar = 1 + pair;
+    double *lsm = lsm_all + warp * 3 * nx;
+    if (threadIdx.x < 2) {
+        ecode_s[threadIdx.x] = 0;
+        eplane_s[threadIdx.x] = -1;
+        erow_s[threadIdx.x] = -1;
+        last_p[threadIdx.x] = -1;
+        flag_s[threadIdx.x][0] = flag_s[threadIdx.x][1] = 0;
+    }
+    // zero the factor (factor_level3 :365-369) and copy l3/u3 (:363-364)
+    for (i64 k = threadIdx.x; k < n; k += blockDim.x) {
+        c.pre[k] = 0.0;
+        c.pre[n + k] = 0.0;
+        c.pre[2 * n + k] = 0.0;
+        c.pre[3 * n + k] = 0.0;
+        c.pre[4 * n + k] = c.a[k];
+        c.pre[5 * n + k] = c.a[6 * n + k];
+        c.pre[6 * n + k] = 0.0;
+    }
+    __syncthreads();
+    PairScratch S[2];
+    for (int h = 0; h < 2; h++) {
+        S[h].base = work + (sys * 2 + h) * S_PER_PAIR * nxy;
+        S[h].nxy = nxy;
+    }
+    const PairScratch &MS = S[pair];
+    volatile int *ecode = &ecode_s[pair];
+    double *bufA[5], *bufB[5];
+    for (int b = 0; b < 5; b++) {
+        bufA[b] = MS.at(S_PC0 + b);
+        bufB[b] = MS.at(S_PC1 + b);
+    }
+    double **Pcur = bufA, **Pprev = bufB;
+    int parity = 0;
+    const int t3 = (nz - 1) / 2;
+    // run_half (ntd_factor.py:425-434)
+    {
+        int cntp = pair == 0 ? t3 : (nz - 1 - t3);
+        int prev_p = -1;
+        for (int i = 0; i < cntp; i++) {
+            int p = pair == 0 ? i : nz - 1 - i;
+            load_plane_bands(c, p, Pcur, bar);
+            if (prev_p >= 0) {
+                if ((threadIdx.x & 63) == 0) flag_s[pair][0] = flag_s[pair][1] = 0;
+                named_bar(bar, 64);
+                const double *Q[5] = {Pprev[0], Pprev[1], Pprev[2], Pprev[3], Pprev[4]};
+                correct_from_pair<K>(c, p, prev_p, Pcur, Q, MS, w2, bar, ex[pair], parity, ecode, &eplane_s[pair],
+                                     &erow_s[pair], flag_s[pair]);
+                if (*ecode) break;
+            }
+            factor_one_pair<K>(c, p, Pcur, MS, w2, bar, ecode, &eplane_s[pair], &erow_s[pair], lsm, wbad_s[pair]);
+            if (*ecode) break;
+            double **tmp = Pcur;
+            Pcur = Pprev;
+            Pprev = tmp;
+            prev_p = p;
+        }
+        if ((threadIdx.x & 63) == 0) last_p[pair] = prev_p;
+    }
+    __syncthreads();
+    // twist plane, corrected from both sides (ntd_factor.py:448-453)
+    if (pair == 0 && !ecode_s[0] && !ecode_s[1]) {
+        double *Pt[5];
+        for (int b = 0; b < 5; b++) Pt[b] = Pcur[b];  // pair 0's free buffer
+        load_plane_bands(c, t3, Pt, bar);
+        int pa = last_p[0], pd = last_p[1];
+        if (pa >= 0) {
+            if ((threadIdx.x & 63) == 0) flag_s[0][0] = flag_s[0][1] = 0;
+            named_bar(bar, 64);
+            const double *Q[5] = {Pprev[0], Pprev[1], Pprev[2], Pprev[3], Pprev[4]};
+            correct_from_pair<K>(c, t3, pa, Pt, Q, MS, w2, bar, ex[0], parity, ecode, &eplane_s[0], &erow_s[0],
+                                 flag_s[0]);
+        }
+        if (!*ecode && pd >= 0) {
+            // pair 1's last corrected bands: its "Pprev" after the final swap
+            int cnt1 = nz - 1 - t3;
+            double *Q1[5];
+            for (int b = 0; b < 5; b++) Q1[b] = S[1].at(((cnt1 & 1) ? S_PC0 : S_PC1) + b);
+            if ((threadIdx.x & 63) == 0) flag_s[0][0] = flag_s[0][1] = 0;
+            named_bar(bar, 64);
+            const double *Q[5] = {Q1[0], Q1[1], Q1[2], Q1[3], Q1[4]};
+            correct_from_pair<K>(c, t3, pd, Pt, Q, MS, w2, bar, ex[0], parity, ecode, &eplane_s[0], &erow_s[0],
+                                 flag_s[0]);
+        }
+        if (!*ecode)
+            factor_one_pair<K>(c, t3, Pt, MS, w2, bar, ecode, &eplane_s[0], &erow_s[0], lsm, wbad_s[0]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // the ascending half's error is reported first (fut_a.result(), :442)
+        int h = ecode_s[0] ? 0 : (ecode_s[1] ? 1 : -1);
+        status[sys * 3 + 0] = h >= 0 ? ecode_s[h] : 0;
+        status[sys * 3 + 1] = h >= 0 ? eplane_s[h] : -1;
+        status[sys * 3 + 2] = h >= 0 ? erow_s[h] : -1;
+    }
+}
+
+
+// ---- per-K launchers (instantiated in ntd_k<K>.cu)
+template <int K>
+int launch_apply_k(const double *pre, const double *b, double *x, double *work, int nx, int ny, int nz, i64 batch,
+                   const int32_t *active, cudaStream_t st);
+template <int K>
+int launch_factor_k(const double *a, double *pre, double *work, int64_t *status, int nx, int ny, int nz, i64 batch,
+                    cudaStream_t st);
+
+#define NTD_INSTANTIATE(K)                                                                                        \
+    template <>                                                                                                    \
+    int launch_apply_k<K>(const double *pre, const double *b, double *x, double *work, int nx, int ny, int nz,     \
+                          i64 batch, const int32_t *active, cudaStream_t st)                                       \
+    {                                                                                                              \
+        k_ntd_apply<K><<<(unsigned)batch, 128, 0, st>>>(pre, b, x, work, nx, ny, nz, active);                      \
+        return ntd::check_launch("ntd_apply");                                                                     \
+    }                                                                                                              \
+    template <>                                                                                                    \
+    int launch_factor_k<K>(const double *a, double *pre, double *work, int64_t *status, int nx, int ny, int nz,    \
+                           i64 batch, cudaStream_t st)                                                             \
+    {                                                                                                              \
+        size_t smem = sizeof(double) * 4 * 3 * (size_t)nx;                                                        \
+        cudaError_t e = cudaFuncSetAttribute(k_ntd_factor<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                                             (int)(smem > 48 * 1024 ? smem : 48 * 1024));                          \
+        if (e != cudaSuccess) {                                                                                    \
+            ntd::set_error("ntd_factor smem", e);                                                                  \
+            return NTD_ELAUNCH;                                                                                    \
+        }                                                                                                          \
+        k_ntd_factor<K><<<(unsigned)batch, 128, smem, st>>>(a, pre, work, status, nx, ny, nz);                     \
+        return ntd::check_launch("ntd_factor");                                                                    \
+    }

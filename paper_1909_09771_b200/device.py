@@ -1,0 +1,204 @@
+"""Batched device-side building blocks (B independent systems per launch).
+
+Everything here works on CUDA tensors laid out batch-major -- operators and
+factors (B, 7, N), vectors (B, N) -- and calls libntdgpu.so through the C ABI
+(include/ntdgpu.h).  The reference-compatible single-system API
+(banded_core / ntd_factor / ntd_solve / ilu0 / precond_pcg) and the batched
+solver both sit on top of these functions.
+"""
+
+import torch
+
+from . import _lib
+
+FACTOR_MESSAGES = {1: "zero or non-finite pivot", 2: "non-finite filter weight",
+                   3: "non-finite sandwich adjustment"}
+
+
+def _dev():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def ntd_factor_message(code, plane, row):
+    """Reference FactorizationError texts (ntd_factor.py:383-386,397-399,414-419)."""
+    if code == 1:
+        return f"zero or non-finite pivot at row {row} (plane {plane})"
+    if code == 2 and row >= 0:
+        return f"non-finite filter weight at row {row} (plane {plane})"
+    if code == 2:
+        return f"plane {plane}: non-finite filter weights"
+    return f"plane {plane}: non-finite sandwich adjustment"
+
+
+def ntd_factor(a_dev, nx, ny, nz, batch):
+    """factor_level3 on B systems.  Returns (pre (B,7,N), status (B,3) host)."""
+    lib = _lib.load()
+    n = nx * ny * nz
+    pre = torch.empty((batch, 7, n), dtype=torch.float64, device=_dev())
+    work = torch.empty(lib.ntd_factor_work_doubles(nx, ny, nz, batch), dtype=torch.float64, device=_dev())
+    status = torch.zeros((batch, 3), dtype=torch.int64, device=_dev())
+    _lib.call("ntd_factor", _lib.ptr(a_dev), _lib.ptr(pre), _lib.ptr(work), _lib.ptr(status), nx, ny, nz,
+              batch, _lib.stream())
+    return pre, status.cpu()
+
+
+def ntd_apply(pre_dev, b_dev, nx, ny, nz, batch, x=None, work=None, active=None):
+    lib = _lib.load()
+    if x is None:
+        x = torch.empty_like(b_dev)
+    if work is None:
+        work = torch.empty(lib.ntd_apply_work_doubles(nx, ny, nz, batch), dtype=torch.float64, device=_dev())
+    _lib.call("ntd_apply", _lib.ptr(pre_dev), _lib.ptr(b_dev), _lib.ptr(x), _lib.ptr(work), nx, ny, nz, batch,
+              _lib.ptr(active), _lib.stream())
+    return x
+
+
+def check_grid_pattern(a_dev, nx, ny, nz):
+    """True when no band couples across a line or plane boundary
+    (BandedMatrix invariant, banded_core.py:39-42); required by the ILU0
+    wavefront kernels."""
+    d = a_dev.reshape(-1, 7, nz, ny, nx)
+    bad = (d[:, 2, :, :, 0] != 0).any() | (d[:, 4, :, :, nx - 1] != 0).any()
+    bad = bad | (d[:, 1, :, 0, :] != 0).any() | (d[:, 5, :, ny - 1, :] != 0).any()
+    return not bool(bad.item())
+
+
+def ilu0_factor(a_dev, nx, ny, nz, batch, split):
+    n = nx * ny * nz
+    f = torch.empty((batch, 7, n), dtype=torch.float64, device=_dev())
+    status = torch.zeros((batch, 3), dtype=torch.int64, device=_dev())
+    _lib.call("ntd_ilu0_factor", _lib.ptr(a_dev), _lib.ptr(f), split, _lib.ptr(status), nx, ny, nz, batch,
+              _lib.stream())
+    return f, status.cpu()
+
+
+def ilu0_apply(f_dev, split, r_dev, nx, ny, nz, batch, z=None, acc=None, active=None):
+    if z is None:
+        z = torch.empty_like(r_dev)
+    _lib.call("ntd_ilu0_apply", _lib.ptr(f_dev), split, _lib.ptr(r_dev), _lib.ptr(z), _lib.ptr(acc), nx, ny,
+              nz, batch, _lib.ptr(active), _lib.stream())
+    return z
+
+
+def residual(a_dev, r_dev, w_dev, nx, ny, nz, batch, t=None, v=None, z_out=None, active=None):
+    """t = r - A w, or (v given) z_out = v + w and t = r - A z_out."""
+    if t is None:
+        t = torch.empty_like(r_dev)
+    _lib.call("ntd_residual", _lib.ptr(a_dev), _lib.ptr(r_dev), _lib.ptr(w_dev), _lib.ptr(v), _lib.ptr(z_out),
+              _lib.ptr(t), nx, ny, nz, batch, _lib.ptr(active), _lib.stream())
+    return t
+
+
+class CombinedDevice:
+    """Symmetric ILU0 -> NTD -> ILU0 preconditioner on B systems
+    (precond_pcg.py:28-65), all buffers preallocated on the device."""
+
+    def __init__(self, a_dev, nx, ny, nz, batch, pre=None, ilu=None, split=None):
+        self.a, self.nx, self.ny, self.nz, self.batch = a_dev, nx, ny, nz, batch
+        n = nx * ny * nz
+        self.n = n
+        self.pre = pre
+        self.ilu = ilu
+        self.split = n // 2 if split is None else split
+        shape = (batch, n)
+        self.w = torch.empty(shape, dtype=torch.float64, device=_dev())
+        self.t = torch.empty(shape, dtype=torch.float64, device=_dev())
+        self.xn = torch.empty(shape, dtype=torch.float64, device=_dev())
+        self.work = torch.empty(_lib.load().ntd_apply_work_doubles(nx, ny, nz, batch), dtype=torch.float64,
+                                device=_dev())
+
+    def apply(self, r, z, active=None):
+        """z = M^{-1} r:  w = ilu(r); t = r - A w; z = ntd(t) + w;
+        t = r - A z; z += ilu(t)   (precond_pcg.py:57-65)."""
+        g = (self.nx, self.ny, self.nz, self.batch)
+        ilu0_apply(self.ilu, self.split, r, *g, z=self.w, active=active)
+        residual(self.a, r, self.w, *g, t=self.t, active=active)
+        ntd_apply(self.pre, self.t, *g, x=self.xn, work=self.work, active=active)
+        residual(self.a, r, self.w, *g, t=self.t, v=self.xn, z_out=z, active=active)
+        ilu0_apply(self.ilu, self.split, self.t, *g, z=self.xn, acc=z, active=active)
+        return z
+
+
+class PcgDevice:
+    """Device-resident PCG over B systems (precond_pcg.py:68-122).
+
+    Per-system scalars (rz, alpha, beta, relres, convergence) live on the
+    device; one small device->host read of the flags per iteration decides
+    whether to continue.  Converged systems are masked out of every kernel."""
+
+    def __init__(self, a_dev, nx, ny, nz, batch, max_iters):
+        lib = _lib.load()
+        self.a, self.nx, self.ny, self.nz, self.batch = a_dev, nx, ny, nz, batch
+        n = nx * ny * nz
+        self.n = n
+        self.max_iters = max_iters
+        dev = _dev()
+        shape = (batch, n)
+        self.x = torch.empty(shape, dtype=torch.float64, device=dev)
+        self.r = torch.empty(shape, dtype=torch.float64, device=dev)
+        self.z = torch.empty(shape, dtype=torch.float64, device=dev)
+        self.p = torch.empty(shape, dtype=torch.float64, device=dev)
+        self.ap = torch.empty(shape, dtype=torch.float64, device=dev)
+        self.state = torch.zeros((batch, _lib.NTD_ST["N"]), dtype=torch.float64, device=dev)
+        self.flags = torch.zeros((batch, _lib.NTD_FL["N"]), dtype=torch.int32, device=dev)
+        self.active = torch.zeros(batch, dtype=torch.int32, device=dev)
+        self.history = torch.zeros((batch, max(1, max_iters)), dtype=torch.float64, device=dev)
+        self.work = torch.empty(lib.ntd_dot_work_doubles(batch), dtype=torch.float64, device=dev)
+        self.host_flags = torch.zeros((batch, _lib.NTD_FL["N"]), dtype=torch.int32).pin_memory()
+        self.host_state = torch.zeros((batch, _lib.NTD_ST["N"]), dtype=torch.float64).pin_memory()
+
+    def _g(self):
+        return self.nx, self.ny, self.nz, self.batch
+
+    def init(self, b, tol):
+        self.b = b
+        _lib.call("ntd_pcg_init", _lib.ptr(b), _lib.ptr(self.x), _lib.ptr(self.r), _lib.ptr(self.state),
+                  _lib.ptr(self.flags), _lib.ptr(self.active), float(tol), self.n, self.batch,
+                  _lib.ptr(self.work), _lib.stream())
+
+    def start(self, z):
+        _lib.call("ntd_pcg_start", _lib.ptr(self.r), _lib.ptr(z), _lib.ptr(self.p), _lib.ptr(self.state),
+                  _lib.ptr(self.active), self.n, self.batch, _lib.ptr(self.work), _lib.stream())
+
+    def step_update(self):
+        """ap = A p; alpha; x, r update; true residual; convergence flags."""
+        _lib.call("ntd_pcg_spmv_alpha", _lib.ptr(self.a), _lib.ptr(self.p), _lib.ptr(self.ap),
+                  _lib.ptr(self.state), _lib.ptr(self.flags), _lib.ptr(self.active), *self._g(),
+                  _lib.ptr(self.work), _lib.stream())
+        _lib.call("ntd_pcg_update_residual", _lib.ptr(self.a), _lib.ptr(self.b), _lib.ptr(self.x),
+                  _lib.ptr(self.r), _lib.ptr(self.p), _lib.ptr(self.ap), _lib.ptr(self.state),
+                  _lib.ptr(self.flags), _lib.ptr(self.active), _lib.ptr(self.history), self.max_iters,
+                  *self._g(), _lib.ptr(self.work), _lib.stream())
+
+    def direction(self, z):
+        _lib.call("ntd_pcg_direction", _lib.ptr(self.r), _lib.ptr(z), _lib.ptr(self.p), _lib.ptr(self.state),
+                  _lib.ptr(self.active), self.n, self.batch, _lib.ptr(self.work), _lib.stream())
+
+    def read_flags(self):
+        """Synchronising D2H copy of flags and scalars (pinned)."""
+        self.host_flags.copy_(self.flags, non_blocking=True)
+        self.host_state.copy_(self.state, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self.host_flags, self.host_state
+
+    def solve(self, b, tol, precond_apply=None, callback=None):
+        """Run PCG to completion.  precond_apply(r, z, active) -> z (device),
+        or None for plain CG.  callback(it, x_dev, relres_host_array)."""
+        self.init(b, tol)
+        fl, _ = self.read_flags()
+        if not bool(fl[:, _lib.NTD_FL["ACTIVE"]].any()):
+            return 0
+        z = self.r if precond_apply is None else precond_apply(self.r, self.z, self.active)
+        self.start(z)
+        it = 0
+        for it in range(1, self.max_iters + 1):
+            self.step_update()
+            fl, st = self.read_flags()
+            if callback is not None:
+                callback(it, fl, st)
+            if not bool(fl[:, _lib.NTD_FL["ACTIVE"]].any()):
+                break
+            if precond_apply is not None:
+                z = precond_apply(self.r, self.z, self.active)
+            self.direction(z)
+        return it

@@ -1,0 +1,129 @@
+"""GPU parity of the product path (C ABI via the drop-in API) against the
+reference's own outputs (tests/golden, generated from /root/reference by
+tests/golden/gen_golden.py) and against the CPU oracle.
+
+Bars: spmv and ILU0 bitwise; NTD factor bands and NTD / combined applies
+<= 1e-10 relative (BASELINE.json north_star); PCG iteration counts within
++-1 and final relres < tol.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, grid_of
+
+pytestmark = pytest.mark.gpu
+
+APPLY_TOL = 1e-10  # north_star: preconditioner apply relative error <= 1e-10 (fp64)
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    den = np.abs(b).max()
+    return float(np.abs(a - b).max() / (den if den > 0 else 1.0))
+
+
+@pytest.fixture(scope="module")
+def ntd():
+    import paper_1909_09771_b200 as m
+    return m
+
+
+def names(golden):
+    return [str(n) for n in golden["names"]]
+
+
+def test_spmv_bitwise(ntd, golden):
+    for name in names(golden):
+        nx, ny, nz = grid_of(name)
+        a = ntd.BandedMatrix(nx, ny, nz, golden[name + "/A"])
+        y = ntd.spmv(a, golden[name + "/v"])
+        assert np.array_equal(y, golden[name + "/spmv"]), name
+
+
+def test_factor_bands_match_reference(ntd, golden):
+    for name in names(golden):
+        nx, ny, nz = grid_of(name)
+        a = ntd.BandedMatrix(nx, ny, nz, golden[name + "/A"])
+        pre = ntd.factor_level3(a)
+        want = golden[name + "/pre"]
+        got = pre.host()
+        # l2,u2,l3,u3 are copies / elementwise corrections: compare per band
+        for i in range(7):
+            assert rel(got[i], want[i]) <= APPLY_TOL, (name, i, rel(got[i], want[i]))
+
+
+def test_ntd_apply_matches_reference(ntd, golden):
+    for name in names(golden):
+        nx, ny, nz = grid_of(name)
+        want = golden[name + "/ntd"]
+        pre = ntd.PreconBands(nx, ny, nz, *golden[name + "/pre"])
+        x = ntd.ntd_apply(pre, golden[name + "/v"])
+        assert rel(x, want) <= APPLY_TOL, (name, rel(x, want))
+        # and with the GPU's own factor
+        a = ntd.BandedMatrix(nx, ny, nz, golden[name + "/A"])
+        x2 = ntd.ntd_apply(ntd.factor_level3(a), golden[name + "/v"])
+        assert rel(x2, want) <= APPLY_TOL, (name, rel(x2, want))
+
+
+def test_ilu0_bitwise(ntd, golden):
+    for name in names(golden):
+        if name + "/ilu" not in golden:
+            continue
+        nx, ny, nz = grid_of(name)
+        a = ntd.BandedMatrix(nx, ny, nz, golden[name + "/A"])
+        f = ntd.build_block_ilu0(a)
+        assert f.split == int(golden[name + "/ilu_split"][0])
+        assert np.array_equal(f.data, golden[name + "/ilu"]), name
+        z = ntd.ilu0_apply(f, golden[name + "/v"])
+        assert np.array_equal(z, golden[name + "/ilu_apply"]), name
+
+
+def test_combined_apply_and_pcg(ntd, golden):
+    for name in names(golden):
+        if name + "/combined" not in golden:
+            continue
+        nx, ny, nz = grid_of(name)
+        a = ntd.BandedMatrix(nx, ny, nz, golden[name + "/A"])
+        cp = ntd.CombinedPrecond(a)
+        z = ntd.combined_apply(cp, golden[name + "/v"])
+        assert rel(z, golden[name + "/combined"]) <= APPLY_TOL, name
+        b = golden[name + "/spmv"]
+        x, st = ntd.pcg(a, b, cp, tol=1e-8, max_iters=100)
+        it_ref, conv_ref = (int(v) for v in golden[name + "/pcg_iters"])
+        assert st.converged == bool(conv_ref), name
+        assert abs(st.iterations - it_ref) <= 1, (name, st.iterations, it_ref)
+        assert st.final_relres < 1e-8
+
+
+def test_baseline_configs_1_2(ntd):
+    from paper_1909_09771_b200 import problems
+    with open(os.path.join(GOLDEN, "configs.json")) as fh:
+        cfgs = json.load(fh)
+    for key, rec in cfgs.items():
+        cfg = int(key)
+        data, x_true, (nx, ny, nz) = problems.baseline_config(cfg)
+        a = ntd.BandedMatrix(nx, ny, nz, data)
+        idx = rec["sample_idx"]
+        b = ntd.spmv(a, x_true)
+        assert [float(b[i]) for i in idx] == rec["b"]["sample"]
+        pre = ntd.factor_level3(a)
+        for nm in ("l1", "u1", "l2", "u2", "m_recip"):
+            got = np.array([getattr(pre, nm)[i] for i in idx])
+            want = np.array(rec["pre_" + nm]["sample"])
+            assert rel(got, want) <= APPLY_TOL, (cfg, nm)
+        v = np.random.default_rng(rec["apply_v_seed"]).uniform(-1.0, 1.0, a.n_rows)
+        x = ntd.ntd_apply(pre, v)
+        assert rel(x[idx], rec["ntd_apply"]["sample"]) <= APPLY_TOL
+        f = ntd.build_block_ilu0(a)
+        z = ntd.ilu0_apply(f, v)
+        assert [float(z[i]) for i in idx] == rec["ilu_apply"]["sample"]
+        cp = ntd.CombinedPrecond(a)
+        assert rel(ntd.combined_apply(cp, v)[idx], rec["combined"]["sample"]) <= APPLY_TOL
+        xs, st = ntd.pcg(a, b, cp, tol=1e-8, max_iters=200)
+        assert st.converged and st.final_relres < 1e-8
+        assert abs(st.iterations - rec["pcg_iters"]) <= 1, (cfg, st.iterations, rec["pcg_iters"])
