@@ -1,0 +1,375 @@
+"""NTD-PCG benchmark (driver contract: one JSON line from rank 0).
+
+Workload: BASELINE.json config 4 -- a batch of 64 independent 96^3 diffusion
+systems (seeded cellwise log-normal kappa on 4^3 blocks, Dirichlet faces,
+b = A x_true), ntd+ilu0 PCG to relative residual 1e-8 from x0 = 0.  One
+"step" = one full batched PCG solve (all systems to convergence).  The 64
+systems are sharded across ranks (rank r solves systems [64r/N, 64(r+1)/N)),
+each rank builds its systems from their seeds; no data-path collective, one
+NCCL all_gather of per-system statistics at the end.
+
+Metric: PCG Munknowns/s = sum over systems of N * iterations / solve time
+(the reference's "M unknown-iter/s").  `value` is device-timed
+with inputs resident; `e2e` adds the host->device copy of b and the
+device->host copy of x every step (public BatchSolver API).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ntd|reference]
+"""
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+# reference iteration counts for config 4, systems 0..63 (reference package
+# run on the same seeded inputs)
+CFG4_REF_ITERS = [21, 21, 24, 21, 22, 22, 20, 20, 20, 24, 22, 23, 20, 21, 19, 21, 23, 20, 23, 20, 19, 23, 20, 25,
+                  22, 22, 22, 23, 21, 23, 21, 20, 21, 25, 21, 24, 21, 22, 21, 21, 19, 20, 23, 20, 25, 21, 25, 21,
+                  20, 22, 23, 21, 20, 21, 21, 21, 20, 21, 21, 21, 23, 20, 23, 22]
+
+METRIC = "pcg_munknowns_per_s"
+UNIT = "Munknown-iterations/s"
+NTD_APPLY_BYTES_PER_UNKNOWN = 48  # canonical algorithmic bytes
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ntd", choices=["ntd", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--systems", type=int, default=None, help="batch size (config 4: 64)")
+    ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--cpu-systems", type=int, default=None, help="CPU baseline sample size")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def shard(total, world, rank):
+    return list(range(total * rank // world, total * (rank + 1) // world))
+
+
+def system_inputs(cfg, s):
+    from paper_1909_09771_b200 import problems
+    data, x_true, grid = problems.baseline_config(cfg, s)
+    return data, x_true, grid
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- CPU leg
+def cpu_solve_systems(cfg, systems, threads, tol):
+    """Oracle (C restatement of the reference) PCG on `systems`, `threads`
+    systems at a time.  Returns (unknown-iterations, solve seconds wall,
+    setup seconds wall, iterations list)."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    inputs = [system_inputs(cfg, s) for s in systems]
+    built = []
+
+    def setup(inp):
+        data, x_true, (nx, ny, nz) = inp
+        b = oracle.spmv(data, x_true, nx, ny, nz)
+        pre = oracle.factor_level3(data, nx, ny, nz)
+        ilu = oracle.build_block_ilu0(data, nx, ny, nz)
+        return data, b, (nx, ny, nz), pre, ilu
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        built = list(ex.map(setup, inputs))
+    t_setup = time.perf_counter() - t0
+
+    def solve(item):
+        data, b, (nx, ny, nz), pre, ilu = item
+        _, it, conv, _ = oracle.pcg(data, b, nx, ny, nz, tol=tol, pre=pre, ilu=ilu)
+        return nx * ny * nz * it, it
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        res = list(ex.map(solve, built))
+    t_solve = time.perf_counter() - t0
+    return sum(r[0] for r in res), t_solve, t_setup, [r[1] for r in res]
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    sample = args.cpu_systems or min(cores, 8)
+    cfg = args.config
+    n_sys = args.systems or (64 if cfg == 4 else 1)
+    systems = list(range(min(sample, n_sys)))
+    for _ in range(args.warmup):
+        cpu_solve_systems(cfg, systems[:1], 1, args.tol)
+    vals, ts = [], []
+    for _ in range(args.steps):
+        work, t, _, iters = cpu_solve_systems(cfg, systems, sample, args.tol)
+        vals.append(work / t / 1e6)
+        ts.append(t)
+    v = float(np.median(vals))
+    desc = (f"{len(systems)} of the {n_sys} config-{cfg} systems per step, each a full ntd+ilu0 PCG solve "
+            f"to {args.tol:g} by the C oracle (restatement of the reference kernels), one system per thread")
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(ts)), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": f"cfg{cfg}", "systems": n_sys, "grid": "96^3" if cfg == 4 else None,
+                      "precond": "ntd+ilu0", "tol": args.tol, "parallelism": "cpu-threads"},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": sample, "kind": "port", "sample": desc},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------- GPU leg
+def run_ntd(args):
+    import torch
+    import torch.distributed as dist
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1909_09771_b200 import _lib
+    from paper_1909_09771_b200 import device as D
+    from paper_1909_09771_b200.batch import BatchSolver
+
+    cfg = args.config
+    n_total = args.systems or (64 if cfg == 4 else 1)
+    mine = shard(n_total, world, rank)
+    inputs = [system_inputs(cfg, s) for s in mine]
+    nx, ny, nz = inputs[0][2]
+    n = nx * ny * nz
+    B = len(mine)
+    a_host = np.stack([inp[0] for inp in inputs])
+    a_dev = torch.from_numpy(a_host).cuda()
+    del a_host
+    xt_dev = torch.from_numpy(np.stack([inp[1] for inp in inputs])).cuda()
+    del inputs
+    b_dev = torch.empty_like(xt_dev)
+    _lib.call("ntd_spmv", _lib.ptr(a_dev), _lib.ptr(xt_dev), _lib.ptr(b_dev), nx, ny, nz, B, None, _lib.stream())
+    b_host = b_dev.cpu().pin_memory()
+    x_host = torch.empty_like(b_host).pin_memory()
+
+    solver = BatchSolver(a_dev, nx, ny, nz, "ntd+ilu0", max_iters=200)
+    solver.setup()
+    setup_s = solver.setup_seconds
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up
+    res = None
+    for _ in range(args.warmup):
+        res = solver.solve(b_dev, args.tol)
+    barrier()
+    # ---- device-timed steps (inputs resident)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    _lib.reset_launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        ev[0].record()
+        work_local = 0
+        for _ in range(args.steps):
+            res = solver.solve(b_dev, args.tol)
+            work_local += n * sum(res.iterations)
+        ev[1].record()
+        barrier()
+    launches = _lib.launch_count()
+    t_dev = ev[0].elapsed_time(ev[1]) / 1e3
+    # ---- e2e through the public API with host buffers
+    ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    barrier()
+    ev2[0].record()
+    work_e2e = 0
+    for _ in range(args.steps):
+        b_in = b_host.to("cuda", non_blocking=True)
+        r2 = solver.solve(b_in, args.tol)
+        x_host.copy_(r2.x, non_blocking=True)
+        work_e2e += n * sum(r2.iterations)
+    ev2[1].record()
+    barrier()
+    t_e2e = ev2[0].elapsed_time(ev2[1]) / 1e3
+    # ---- dominant kernel: batched NTD apply, CUDA events on its stream
+    v = torch.rand_like(b_dev)
+    xa = torch.empty_like(v)
+    wk = torch.empty(B * n, dtype=torch.float64, device="cuda")
+    R = 5
+    for _ in range(2):
+        D.ntd_apply(solver.precond.pre, v, nx, ny, nz, B, x=xa, work=wk)
+    e3 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e3[0].record()
+    for _ in range(R):
+        D.ntd_apply(solver.precond.pre, v, nx, ny, nz, B, x=xa, work=wk)
+    e3[1].record()
+    torch.cuda.synchronize()
+    t_apply = e3[0].elapsed_time(e3[1]) / 1e3 / R
+    # ILU0 apply and spmv for context
+    e4 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e4[0].record()
+    for _ in range(R):
+        D.ilu0_apply(solver.precond.ilu, solver.precond.split, v, nx, ny, nz, B, z=xa)
+    e4[1].record()
+    e5 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e5[0].record()
+    for _ in range(R):
+        _lib.call("ntd_spmv", _lib.ptr(a_dev), _lib.ptr(v), _lib.ptr(xa), nx, ny, nz, B, None, _lib.stream())
+    e5[1].record()
+    torch.cuda.synchronize()
+    t_ilu = e4[0].elapsed_time(e4[1]) / 1e3 / R
+    t_spmv = e5[0].elapsed_time(e5[1]) / 1e3 / R
+
+    # ---- reductions over ranks
+    stats = torch.tensor([[s, it, int(cv), rr] for s, it, cv, rr in
+                          zip(mine, res.iterations, res.converged, res.final_relres)],
+                         dtype=torch.float64, device="cuda")
+    times = torch.tensor([t_dev, t_e2e, t_apply, t_ilu, t_spmv, setup_s], dtype=torch.float64, device="cuda")
+    work = torch.tensor([work_local, work_e2e, launches], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+        dist.all_reduce(work, op=dist.ReduceOp.SUM)
+        sizes = [len(shard(n_total, world, r)) for r in range(world)]
+        pad = torch.zeros((max(sizes), 4), dtype=torch.float64, device="cuda")
+        pad[:B] = stats
+        gathered = [torch.zeros_like(pad) for _ in range(world)]
+        dist.all_gather(gathered, pad)
+        stats = torch.cat([g[:sz] for g, sz in zip(gathered, sizes)])
+    times = times.cpu().tolist()
+    work = work.cpu().tolist()
+    stats = stats.cpu().numpy()
+    if rank == 0:
+        t_dev, t_e2e, t_apply, t_ilu, t_spmv, setup_s = times
+        value = work[0] / t_dev / 1e6
+        e2e = work[1] / t_e2e / 1e6
+        iters = [int(v) for v in stats[:, 1]]
+        sys_ids = [int(v) for v in stats[:, 0]]
+        ref_match = None
+        if cfg == 4:
+            ref_match = sum(abs(it - CFG4_REF_ITERS[s]) <= 1 for s, it in zip(sys_ids, iters))
+        apply_bytes = NTD_APPLY_BYTES_PER_UNKNOWN * n * B  # per launch on this rank
+        achieved = apply_bytes / t_apply / 1e9
+        peak = _measured_peak()
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE config recipe, SURVEY.md 8(d))",
+            "config": {"workload": f"cfg{cfg}", "systems": n_total, "grid": f"{nx}x{ny}x{nz}",
+                       "precond": "ntd+ilu0", "tol": args.tol, "parallelism": f"batch-shard x{world}",
+                       "l2": "inputs larger than L2 (each batch vector %.0f MB)" % (8 * n * B / 1e6)},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n * B * world,
+                    "d2h_bytes_per_step": 8 * n * B * world},
+            "roofline": {"kernel": "ntd_apply (batched, rank 0 shard)", "bound": "hbm",
+                         "achieved": achieved, "peak": peak[0], "unit": "GB/s", "frac": achieved / peak[0],
+                         "peak_source": peak[1], "traffic": None,
+                         "bytes_per_unknown": NTD_APPLY_BYTES_PER_UNKNOWN, "apply_ms": 1e3 * t_apply,
+                         "apply_munknowns_per_s": n * B / t_apply / 1e6},
+            "kernels_ms": {"ntd_apply": 1e3 * t_apply, "ilu0_apply": 1e3 * t_ilu, "spmv": 1e3 * t_spmv},
+            "setup_seconds": setup_s,
+            "iterations": {"min": min(iters), "max": max(iters), "mean": float(np.mean(iters)),
+                           "within_1_of_reference": ref_match, "systems": len(iters)},
+            "max_final_relres": float(stats[:, 3].max()),
+            "all_converged": bool(stats[:, 2].all()),
+            "gpu_launches": int(work[2]),
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(args)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _measured_peak():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_baseline(args):
+    cores = os.cpu_count() or 1
+    sample = args.cpu_systems or min(cores, 8)
+    systems = list(range(sample))
+    work, t, _, iters = cpu_solve_systems(args.config, systems, sample, args.tol)
+    return {"value": work / t / 1e6, "unit": UNIT, "cores": sample, "kind": "port",
+            "sample": f"{sample} config-{args.config} systems, full ntd+ilu0 PCG solve each (C oracle), "
+                      f"one system per host thread; solve wall {t:.1f} s, iterations {iters}"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ntd(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -45,6 +45,23 @@ _SIGS = {
 
 EXPORTED = tuple(_SIGS)
 
+# kernels launched by one successful call of each entry point (counted for
+# bench.py's gpu_launches; see the launch sites in csrc/)
+KERNELS_PER_CALL = {
+    "ntd_spmv": 1, "ntd_residual": 1, "ntd_dot": 2, "ntd_pcg_init": 3, "ntd_pcg_start": 3,
+    "ntd_pcg_spmv_alpha": 2, "ntd_pcg_update_residual": 3, "ntd_pcg_direction": 3, "ntd_factor": 1,
+    "ntd_apply": 1, "ntd_ilu0_factor": 2, "ntd_ilu0_apply": 1,
+}
+_launches = [0]
+
+
+def reset_launch_count():
+    _launches[0] = 0
+
+
+def launch_count():
+    return _launches[0]
+
 
 class NativeUnavailable(RuntimeError):
     """libntdgpu.so is missing or no CUDA device is available."""
@@ -88,6 +105,7 @@ def stream():
 def call(name, *args):
     fn = getattr(load(), name)
     rc = fn(*args)
+    _launches[0] += KERNELS_PER_CALL.get(name, 0)
     if rc != 0:
         msg = (_lib.ntd_last_error() or b"").decode()
         if rc == -1:

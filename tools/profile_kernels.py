@@ -1,0 +1,31 @@
+"""Launch the hot kernels on a config-4 sub-batch for ncu (debug/profiling aid).
+
+    python tools/profile_kernels.py [systems]
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1909_09771_b200 import _lib, problems  # noqa: E402
+from paper_1909_09771_b200 import device as D  # noqa: E402
+from paper_1909_09771_b200.batch import BatchSolver  # noqa: E402
+
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+ins = [problems.baseline_config(4, s) for s in range(B)]
+nx, ny, nz = ins[0][2]
+a = torch.from_numpy(np.stack([i[0] for i in ins])).cuda()
+xt = torch.from_numpy(np.stack([i[1] for i in ins])).cuda()
+b = torch.empty_like(xt)
+_lib.call("ntd_spmv", _lib.ptr(a), _lib.ptr(xt), _lib.ptr(b), nx, ny, nz, B, None, _lib.stream())
+s = BatchSolver(a, nx, ny, nz).setup()
+v = torch.rand_like(b)
+x = torch.empty_like(b)
+for _ in range(2):
+    D.ntd_apply(s.precond.pre, v, nx, ny, nz, B, x=x)
+    D.ilu0_apply(s.precond.ilu, s.precond.split, v, nx, ny, nz, B, z=x)
+    D.residual(a, v, x, nx, ny, nz, B)
+torch.cuda.synchronize()
+print("ok")
