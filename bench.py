@@ -258,14 +258,14 @@ def run_ntd(args):
     # ---- dominant kernel: batched NTD apply, CUDA events on its stream
     v = torch.rand_like(b_dev)
     xa = torch.empty_like(v)
-    wk = torch.empty(B * n, dtype=torch.float64, device="cuda")
+    wk = torch.empty(3 * B * n, dtype=torch.float64, device="cuda")
     R = 5
     for _ in range(2):
-        D.ntd_apply(solver.precond.pre, v, nx, ny, nz, B, x=xa, work=wk)
+        D.ntd_apply(solver.precond.pre, v, nx, ny, nz, B, x=xa, work=wk, solve=solver.precond.solve)
     e3 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     e3[0].record()
     for _ in range(R):
-        D.ntd_apply(solver.precond.pre, v, nx, ny, nz, B, x=xa, work=wk)
+        D.ntd_apply(solver.precond.pre, v, nx, ny, nz, B, x=xa, work=wk, solve=solver.precond.solve)
     e3[1].record()
     torch.cuda.synchronize()
     t_apply = e3[0].elapsed_time(e3[1]) / 1e3 / R

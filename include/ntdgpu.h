@@ -117,13 +117,24 @@ int64_t ntd_factor_work_doubles(int64_t nx, int64_t ny, int64_t nz,
 int ntd_factor(const double *a, double *pre, double *work, int64_t *status,
                int64_t nx, int64_t ny, int64_t nz, int64_t batch, void *stream);
 
+/* Solve arrays of a factor, derived data for the apply: the factor bands
+ * m_recip, -(l1*m_recip), -(u1*m_recip), l2, u2, l3, u3 re-laid per grid line
+ * in the apply's slot layout (chain coefficients precomputed; the reference
+ * forms them inside _chain_scaled/_chain_unit, ntd_solve.py:20-104).
+ * solve: >= ntd_solve_doubles (0 = grid served by the direct path; then pass
+ * solve = NULL to ntd_apply). */
+int64_t ntd_solve_doubles(int64_t nx, int64_t ny, int64_t nz, int64_t batch);
+int ntd_solve_bands(const double *pre, double *solve, int64_t nx, int64_t ny,
+                    int64_t nz, int64_t batch, void *stream);
+
 /* Apply: x = B^{-1} b, ntd_apply (ntd_solve.py:188-322).  b is not modified.
+ * solve: from ntd_solve_bands, or NULL (then formed in work).
  * work: >= ntd_apply_work_doubles. */
 int64_t ntd_apply_work_doubles(int64_t nx, int64_t ny, int64_t nz,
                                int64_t batch);
-int ntd_apply(const double *pre, const double *b, double *x, double *work,
-              int64_t nx, int64_t ny, int64_t nz, int64_t batch,
-              const int32_t *active, void *stream);
+int ntd_apply(const double *pre, const double *solve, const double *b,
+              double *x, double *work, int64_t nx, int64_t ny, int64_t nz,
+              int64_t batch, const int32_t *active, void *stream);
 
 /* -------- Block ILU0 (ilu0.py) ------------------------------------------
  * Factor of blkdiag(A[:split,:split], A[split:,split:]) on the 7-band

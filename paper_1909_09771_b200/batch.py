@@ -33,7 +33,8 @@ class _NtdPrecond:
 
     def device_apply(self, r_dev, z_dev, active=None):
         return D.ntd_apply(self.pre.bands, r_dev, self.a.nx, self.a.ny, self.a.nz, 1, x=z_dev,
-                           work=self.workspace.scratch, active=active)
+                           work=self.workspace.work(self.a.nx, self.a.ny, self.a.nz), active=active,
+                           solve=self.pre.solve)
 
     def __call__(self, r):
         from .ntd_solve import ntd_apply

@@ -1,7 +1,10 @@
 // ntd.cu -- C-ABI entry points of the NTD setup / apply kernels
 // (ntd_kernels.cuh); per-K instantiations live in ntd_k<K>.cu so they
 // compile in parallel.  K = ceil(nx/32) cells per lane per chain.
+#include <stdlib.h>
+
 #include "ntd_kernels.cuh"
+#include "ntd_apply_sl.cuh"
 
 // instantiated K values (ntd_k<K>.cu); a line of nx cells uses the
 // smallest instantiated K >= ceil(nx/32).
@@ -33,17 +36,94 @@ static int pick_k(i64 nx)
 
 extern "C" int64_t ntd_max_nx(void) { return 32 * MAX_K; }
 
-extern "C" int64_t ntd_apply_work_doubles(int64_t nx, int64_t ny, int64_t nz, int64_t batch)
+// Slot-layout (SL) path: K values with an instantiated SL kernel and a ring
+// that fits in shared memory.
+static int sl_depth(int K)
 {
-    return nx * ny * nz * batch;
+    if (K > 11) return 0;
+    const size_t per_stage = (size_t)4 * sl::RSEG * sl::lr_of(K) * 8;
+    return per_stage * 4 <= 200 * 1024 ? 4 : (per_stage * 2 <= 200 * 1024 ? 2 : 0);
 }
 
-extern "C" int ntd_apply(const double *pre, const double *b, double *x, double *work, int64_t nx, int64_t ny,
-                         int64_t nz, int64_t batch, const int32_t *active, void *stream)
+static i64 sl_doubles(i64 nx, i64 ny, i64 nz)
+{
+    const int K = pick_k(nx);
+    return K > 0 ? ny * nz * (i64)sl::lr_of(K) : 0;
+}
+
+extern "C" int64_t ntd_solve_doubles(int64_t nx, int64_t ny, int64_t nz, int64_t batch)
+{
+    const int K = pick_k(nx);
+    if (K <= 0 || !sl_depth(K)) return 0;
+    return (int64_t)sl::SL_N * sl_doubles(nx, ny, nz) * batch;
+}
+
+extern "C" int64_t ntd_apply_work_doubles(int64_t nx, int64_t ny, int64_t nz, int64_t batch)
+{
+    const i64 n = nx * ny * nz * batch;
+    const i64 s = sl_doubles(nx, ny, nz) * batch;
+    const i64 w = 3 * s + (i64)sl::SL_N * s;  // b, x, xs in SL (+ solve arrays if not given)
+    return w > n ? w : n;
+}
+
+extern "C" int ntd_solve_bands(const double *pre, double *solve, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+                               void *stream)
+{
+    if (!pre || !solve || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
+    const int K = pick_k(nx);
+    if (K <= 0 || !sl_depth(K)) return NTD_ENOTSUP;
+    const i64 lines = ny * nz;
+    i64 total = lines * sl::lr_of(K) * batch;
+    i64 blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    sl::k_solve_sl<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(pre, solve, (int)nx, lines, K, batch);
+    return ntd::check_launch("ntd_solve_bands");
+}
+
+static unsigned grid_for(i64 total)
+{
+    i64 blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    return (unsigned)(blocks > 0 ? blocks : 1);
+}
+
+extern "C" int ntd_apply(const double *pre, const double *solve, const double *b, double *x, double *work,
+                         int64_t nx, int64_t ny, int64_t nz, int64_t batch, const int32_t *active, void *stream)
 {
     if (!pre || !b || !x || !work || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
-    int K = pick_k(nx);
-    NTD_DISPATCH(launch_apply_k, pre, b, x, work, (int)nx, (int)ny, (int)nz, batch, active, (cudaStream_t)stream);
+    const int K = pick_k(nx);
+    const char *force = getenv("NTD_APPLY_PATH");
+    const int depth = K > 0 ? sl_depth(K) : 0;
+    const bool aligned = ((uintptr_t)work % 16 == 0) && (!solve || (uintptr_t)solve % 16 == 0);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (depth && aligned && !(force && force[0] == 'd')) {
+        const i64 lines = ny * nz, s = sl_doubles(nx, ny, nz) * batch;
+        double *bsl = work, *xsl = work + s, *xssl = work + 2 * s;
+        if (!solve) {
+            double *sv = work + 3 * s;
+            int rc = ntd_solve_bands(pre, sv, nx, ny, nz, batch, stream);
+            if (rc) return rc;
+            solve = sv;
+        }
+        // x/xs SL buffers: pad slots must read as zero (zero chain maps)
+        if (cudaMemsetAsync(xsl, 0, sizeof(double) * 2 * s, st) != cudaSuccess) return ntd::check_launch("memset");
+        sl::k_to_sl<<<grid_for(s), 256, 0, st>>>(b, bsl, (int)nx, lines, K, batch);
+        int rc = ntd::check_launch("ntd_apply to_sl");
+        if (rc) return rc;
+        switch (K) {
+#define SLCASE(KK)                                                                                                \
+    case KK:                                                                                                       \
+        rc = launch_apply_sl_k<KK>(solve, bsl, xsl, xssl, (int)nx, (int)ny, (int)nz, batch, active, st, depth);    \
+        break;
+            SLCASE(1) SLCASE(2) SLCASE(3) SLCASE(4) SLCASE(5) SLCASE(6) SLCASE(8) SLCASE(11)
+#undef SLCASE
+        default: return NTD_ENOTSUP;
+        }
+        if (rc) return rc;
+        sl::k_from_sl<<<grid_for(nx * lines * batch), 256, 0, st>>>(xsl, x, (int)nx, lines, K, batch);
+        return ntd::check_launch("ntd_apply from_sl");
+    }
+    NTD_DISPATCH(launch_apply_k, pre, b, x, work, (int)nx, (int)ny, (int)nz, batch, active, st);
 }
 
 extern "C" int64_t ntd_factor_work_doubles(int64_t nx, int64_t ny, int64_t nz, int64_t batch)

@@ -1,3 +1,5 @@
 // instantiation of the NTD kernels for K=5 cells per lane (see ntd.cu)
 #include "ntd_kernels.cuh"
+#include "ntd_apply_sl.cuh"
 NTD_INSTANTIATE(5)
+NTD_INSTANTIATE_SL(5)

@@ -122,43 +122,169 @@ __device__ __forceinline__ void finalize(const PlaneIO &io, const LineGeom<K> &g
     }
 }
 
+// Operands of one lower-phase line: factors, right-hand-side parts and the
+// level-2 coupling.  Loaded one line ahead (register double buffer).
+template <int K>
+struct LOps {
+    double mr[K], oL[K], oU[K], r0[K], c1[K], y1[K], cp[K];
+    double mrt, l1t, u1t, r0t, c1t, y1t, cpt;
+};
+// Operands of one upper-phase line.
+template <int K>
+struct UOps {
+    double mr[K], oL[K], oU[K], cp[K], y[K], xo[K];
+    double mrt, l1t, u1t, cpt, yt, xot;
+};
+
+// Level-3 right-hand-side parts of a line: rhs = r0 - c1*y1 (M_LOWER3),
+// c1*y1 (M_UPPER3) or r0 (M_SETUP).  For the twist plane (both neighbours)
+// r0 already has the l3 term removed (loaded eagerly; one plane per apply).
+template <int K, int MODE>
+__device__ __forceinline__ void load_rhs_parts(const FactorPtrs &F, const PlaneIO &io, const LineGeom<K> &g, i64 lb,
+                                               i64 ll, i64 nxy, LOps<K> &o)
+{
+#pragma unroll
+    for (int k = 0; k <= K; k++) {
+        const bool tw = k == K;
+        double r0 = 0.0, c1 = 0.0, y1 = 0.0;
+        if (tw || g.valid(k)) {
+            const int c = tw ? g.t : g.cell(k);
+            const i64 r = lb + c;
+            if (MODE == M_LOWER3) {
+                r0 = io.b[r];
+                if (io.hasM && io.hasP) {
+                    r0 -= F.l3[r] * io.x[r - nxy];
+                    c1 = F.u3[r];
+                    y1 = io.x[r + nxy];
+                } else if (io.hasM) {
+                    c1 = F.l3[r];
+                    y1 = io.x[r - nxy];
+                } else if (io.hasP) {
+                    c1 = F.u3[r];
+                    y1 = io.x[r + nxy];
+                }
+            } else if (MODE == M_UPPER3) {
+                c1 = io.nbrUp ? F.u3[r] : F.l3[r];
+                y1 = io.nbrUp ? io.x[r + nxy] : io.x[r - nxy];
+            } else {
+                r0 = io.useg[ll + c];
+            }
+        }
+        if (tw) {
+            o.r0t = r0;
+            o.c1t = c1;
+            o.y1t = y1;
+        } else {
+            o.r0[k] = r0;
+            o.c1[k] = c1;
+            o.y1[k] = y1;
+        }
+    }
+}
+
+template <int K, int MODE>
+__device__ __forceinline__ void rhs_of(const LOps<K> &o, double (&rhs)[K], double &rhst)
+{
+#pragma unroll
+    for (int k = 0; k < K; k++)
+        rhs[k] = MODE == M_LOWER3 ? o.r0[k] - o.c1[k] * o.y1[k] : (MODE == M_UPPER3 ? o.c1[k] * o.y1[k] : o.r0[k]);
+    rhst = MODE == M_LOWER3 ? o.r0t - o.c1t * o.y1t : (MODE == M_UPPER3 ? o.c1t * o.y1t : o.r0t);
+}
+
+template <int K, int MODE>
+__device__ __forceinline__ void load_lops(const FactorPtrs &F, const PlaneIO &io, const LineGeom<K> &g, i64 pb,
+                                          int q, int nx, i64 nxy, const double *cpl, bool has_cpl, LOps<K> &o)
+{
+    const i64 lb = pb + (i64)q * nx, ll = (i64)q * nx;
+    load_line_factors(g, F.mr, F.l1, F.u1, lb, o.mr, o.oL, o.oU, o.mrt, o.l1t, o.u1t);
+    load_rhs_parts<K, MODE>(F, io, g, lb, ll, nxy, o);
+    if (has_cpl) {
+        load_slots(g, cpl, lb, o.cp, o.cpt);
+    } else {
+#pragma unroll
+        for (int k = 0; k < K; k++) o.cp[k] = 0.0;
+        o.cpt = 0.0;
+    }
+}
+
+template <int K, int MODE>
+__device__ __forceinline__ void load_uops(const FactorPtrs &F, const PlaneIO &io, const LineGeom<K> &g, i64 pb,
+                                          int q, int nx, const double *cpl, UOps<K> &o)
+{
+    const i64 lb = pb + (i64)q * nx, ll = (i64)q * nx;
+    load_line_factors(g, F.mr, F.l1, F.u1, lb, o.mr, o.oL, o.oU, o.mrt, o.l1t, o.u1t);
+    load_slots(g, cpl, lb, o.cp, o.cpt);
+    load_lowerstore<K, MODE>(io, g, lb, ll, o.y, o.yt);
+    if (MODE == M_UPPER3) load_slots(g, io.x, lb, o.xo, o.xot);
+}
+
+// Warp-cooperative L2 prefetch of rows [r0, r1) of an array.
+__device__ __forceinline__ void prefetch_rows(const double *p, i64 r0, i64 r1)
+{
+    if (!p || r1 <= r0) return;
+    const char *c = (const char *)(p + r0);
+    const i64 bytes = (r1 - r0) * 8;
+    for (i64 off = (i64)(threadIdx.x & 31) * 128; off < bytes; off += 32 * 128) prefetch_l2(c + off);
+}
+
+// Prefetch into L2 the part of plane `npb` this warp will touch.
+__device__ __forceinline__ void prefetch_plane(const FactorPtrs &F, const double *e1, const double *e2, i64 npb,
+                                               int nx, int ny, int w2)
+{
+    const int t2 = (ny - 1) / 2;
+    const i64 r0 = npb + (w2 == 0 ? 0 : (i64)t2 * nx);
+    const i64 r1 = npb + (w2 == 0 ? (i64)(t2 + 1) * nx : (i64)ny * nx);
+    prefetch_rows(F.mr, r0, r1);
+    prefetch_rows(F.l1, r0, r1);
+    prefetch_rows(F.u1, r0, r1);
+    prefetch_rows(F.l2, r0, r1);
+    prefetch_rows(F.u2, r0, r1);
+    prefetch_rows(e1, r0, r1);
+    prefetch_rows(e2, r0, r1);
+}
+
 // Twisted solve of one factored plane (ntd_solve.py:140-185) by a warp pair.
 // w2: warp within the pair (0 = ascending lines, 1 = descending lines).
 // ex: this pair's shared exchange buffer [2 parity][2 warps][32K+1].
+// next_pb >= 0: L2-prefetch that plane (arrays F.* and pf1/pf2) meanwhile.
 template <int K, int MODE>
 __device__ void plane_solve(const FactorPtrs &F, const PlaneIO &io, i64 pb, int nx, int ny, int w2, int bar_id,
-                            double *ex, int &parity)
+                            double *ex, int &parity, i64 next_pb = -1, const double *pf1 = nullptr,
+                            const double *pf2 = nullptr)
 {
     const int lane = threadIdx.x & 31;
     const LineGeom<K> g(nx, lane);
     const i64 nxy = (i64)nx * ny;
     const int t2 = (ny - 1) / 2;
+    if (next_pb >= 0) prefetch_plane(F, pf1, pf2, next_pb, nx, ny, w2);
     double xprev[K], xprevt = 0.0;
 #pragma unroll
     for (int k = 0; k < K; k++) xprev[k] = 0.0;
     // ---------------- level-2 lower sweep, ends inward (ntd_solve.py:147-171)
     const int cnt = w2 == 0 ? t2 : (ny - 1 - t2);
     const double *cplL = w2 == 0 ? F.l2 : F.u2;  // b -= l2*x[r-nx] | u2*x[r+nx]
-    for (int i = 0; i < cnt; i++) {
-        int q = w2 == 0 ? i : ny - 1 - i;
-        i64 lb = pb + (i64)q * nx, ll = (i64)q * nx;
-        double mr[K], oL[K], oU[K], mrt, l1t, u1t;
-        load_line_factors(g, F.mr, F.l1, F.u1, lb, mr, oL, oU, mrt, l1t, u1t);
+    auto qlow = [&](int i) { return w2 == 0 ? i : ny - 1 - i; };
+    auto lower_body = [&](const LOps<K> &o, int i) {
+        const int q = qlow(i);
+        const i64 lb = pb + (i64)q * nx, ll = (i64)q * nx;
         double rhs[K], rhst;
-        rhs_lower<K, MODE>(F, io, g, lb, ll, nxy, rhs, rhst);
-        if (i > 0) {
-            double c[K], ct;
-            load_slots(g, cplL, lb, c, ct);
+        rhs_of<K, MODE>(o, rhs, rhst);
 #pragma unroll
-            for (int k = 0; k < K; k++) rhs[k] -= c[k] * xprev[k];
-            rhst -= ct * xprevt;
-        }
+        for (int k = 0; k < K; k++) rhs[k] -= o.cp[k] * xprev[k];
+        rhst -= o.cpt * xprevt;
         double x[K], xt;
-        line_solve(g, mr, oL, oU, rhs, rhst, mrt, l1t, u1t, x, xt);
+        line_solve(g, o.mr, o.oL, o.oU, rhs, rhst, o.mrt, o.l1t, o.u1t, x, xt);
         store_lower<K, MODE>(io, g, lb, ll, x, xt);
 #pragma unroll
         for (int k = 0; k < K; k++) xprev[k] = x[k];
         xprevt = xt;
+    };
+    {
+        for (int i = 0; i < cnt; i++) {
+            LOps<K> oa;
+            load_lops<K, MODE>(F, io, g, pb, qlow(i), nx, nxy, cplL, i > 0, oa);
+            lower_body(oa, i);
+        }
     }
     // ---------------- exchange the lines next to the twist
     const int stride = 32 * K + 1;
@@ -181,55 +307,104 @@ __device__ void plane_solve(const FactorPtrs &F, const PlaneIO &io, i64 pb, int 
     }
     xat = w2 == 0 ? xprevt : xot;
     xdt = w2 == 0 ? xot : xprevt;
-    // ---------------- twist line (ntd_solve.py:172-177), both warps
+    // ---------------- twist line (ntd_solve.py:172-177), both warps; its
+    // operands are read after the barrier (x of the twist line of the
+    // neighbouring plane was written by the other warp).
+    const double *cplU = w2 == 0 ? F.u2 : F.l2;  // bs = u2*x[r+nx] | l2*x[r-nx]
     double xT[K], xTt;
+    UOps<K> ua, ub;
     {
         const int q = t2;
-        i64 lb = pb + (i64)q * nx, ll = (i64)q * nx;
-        double mr[K], oL[K], oU[K], mrt, l1t, u1t;
-        load_line_factors(g, F.mr, F.l1, F.u1, lb, mr, oL, oU, mrt, l1t, u1t);
+        const i64 lb = pb + (i64)q * nx, ll = (i64)q * nx;
+        LOps<K> o;
+        load_lops<K, MODE>(F, io, g, pb, q, nx, nxy, F.l2, t2 > 0, o);
+        double cu[K], cut;
+        if (t2 < ny - 1) load_slots(g, F.u2, lb, cu, cut);
+        if (cnt > 0) load_uops<K, MODE>(F, io, g, pb, w2 == 0 ? t2 - 1 : t2 + 1, nx, cplU, ua);
         double rhs[K], rhst;
-        rhs_lower<K, MODE>(F, io, g, lb, ll, nxy, rhs, rhst);
-        if (t2 > 0) {
-            double c[K], ct;
-            load_slots(g, F.l2, lb, c, ct);
+        rhs_of<K, MODE>(o, rhs, rhst);
 #pragma unroll
-            for (int k = 0; k < K; k++) rhs[k] -= c[k] * xa[k];
-            rhst -= ct * xat;
-        }
+        for (int k = 0; k < K; k++) rhs[k] -= o.cp[k] * xa[k];
+        rhst -= o.cpt * xat;
         if (t2 < ny - 1) {
-            double c[K], ct;
-            load_slots(g, F.u2, lb, c, ct);
 #pragma unroll
-            for (int k = 0; k < K; k++) rhs[k] -= c[k] * xd[k];
-            rhst -= ct * xdt;
+            for (int k = 0; k < K; k++) rhs[k] -= cu[k] * xd[k];
+            rhst -= cut * xdt;
         }
-        line_solve(g, mr, oL, oU, rhs, rhst, mrt, l1t, u1t, xT, xTt);
+        line_solve(g, o.mr, o.oL, o.oU, rhs, rhst, o.mrt, o.l1t, o.u1t, xT, xTt);
         if (w2 == 0) finalize<K, MODE>(io, g, lb, ll, xT, xTt);
     }
     // ---------------- level-2 upper sweep, twist outward (ntd_solve.py:178-185)
     double xn[K], xnt = xTt;
 #pragma unroll
     for (int k = 0; k < K; k++) xn[k] = xT[k];
-    const double *cplU = w2 == 0 ? F.u2 : F.l2;  // bs = u2*x[r+nx] | l2*x[r-nx]
-    for (int i = 0; i < cnt; i++) {
-        int q = w2 == 0 ? t2 - 1 - i : t2 + 1 + i;
-        i64 lb = pb + (i64)q * nx, ll = (i64)q * nx;
-        double mr[K], oL[K], oU[K], mrt, l1t, u1t;
-        load_line_factors(g, F.mr, F.l1, F.u1, lb, mr, oL, oU, mrt, l1t, u1t);
-        double c[K], ct, y[K], yt;
-        load_slots(g, cplU, lb, c, ct);
-        load_lowerstore<K, MODE>(io, g, lb, ll, y, yt);
-        double bs[K], bst = ct * xnt;
+    auto qup = [&](int i) { return w2 == 0 ? t2 - 1 - i : t2 + 1 + i; };
+    auto upper_body = [&](const UOps<K> &o, int i) {
+        const int q = qup(i);
+        const i64 lb = pb + (i64)q * nx, ll = (i64)q * nx;
+        double bs[K], bst = o.cpt * xnt;
 #pragma unroll
-        for (int k = 0; k < K; k++) bs[k] = c[k] * xn[k];
+        for (int k = 0; k < K; k++) bs[k] = o.cp[k] * xn[k];
         double xs[K], xst;
-        line_solve(g, mr, oL, oU, bs, bst, mrt, l1t, u1t, xs, xst);
+        line_solve(g, o.mr, o.oL, o.oU, bs, bst, o.mrt, o.l1t, o.u1t, xs, xst);
 #pragma unroll
-        for (int k = 0; k < K; k++) xn[k] = y[k] - xs[k];
-        xnt = yt - xst;
-        finalize<K, MODE>(io, g, lb, ll, xn, xnt);
+        for (int k = 0; k < K; k++) xn[k] = o.y[k] - xs[k];
+        xnt = o.yt - xst;
+        if (MODE == M_UPPER3) {
+            double nv[K];
+#pragma unroll
+            for (int k = 0; k < K; k++) nv[k] = o.xo[k] - xn[k];
+            store_slots(g, io.x, lb, nv, o.xot - xnt);
+        } else {
+            finalize<K, MODE>(io, g, lb, ll, xn, xnt);
+        }
+    };
+    for (int i = 0; i < cnt; i++) {
+        if (i > 0) load_uops<K, MODE>(F, io, g, pb, qup(i), nx, cplU, ua);
+        upper_body(ua, i);
     }
+}
+
+#ifdef NTD_TIMING
+__device__ unsigned long long g_ntd_timing[8][8];
+#define TSTAMP(v) long long v = clock64()
+#define TACC(slot, a, b) \
+    if ((threadIdx.x & 31) == 0 && blockIdx.x == 0) atomicAdd(&g_ntd_timing[threadIdx.x >> 5][slot], (unsigned long long)((b) - (a)))
+#else
+#define TSTAMP(v)
+#define TACC(slot, a, b)
+#endif
+
+// ---- TMA / mbarrier helpers (1-D bulk copies)
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(void *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(void *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(void *bar, unsigned parity)
+{
+    unsigned ok = 0;
+    const unsigned a = smem_u32(bar);
+    while (!ok) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned bytes, void *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 
 // =============================================================== apply
@@ -256,16 +431,20 @@ __global__ void __launch_bounds__(128) k_ntd_apply(const double *__restrict__ pr
     // level-3 lower sweep, both halves (ntd_solve.py:198-221)
     io.nbrUp = false;
     if (pair == 0) {
+        prefetch_plane(F, io.b, F.l3, 0, nx, ny, w2);
         for (int p = 0; p < t3; p++) {
             io.hasM = p > 0;
             io.hasP = false;
-            plane_solve<K, M_LOWER3>(F, io, (i64)p * nxy, nx, ny, w2, bar, myex, parity);
+            plane_solve<K, M_LOWER3>(F, io, (i64)p * nxy, nx, ny, w2, bar, myex, parity, (i64)(p + 1) * nxy,
+                                     io.b, F.l3);
         }
     } else {
+        prefetch_plane(F, io.b, F.u3, (i64)(nz - 1) * nxy, nx, ny, w2);
         for (int p = nz - 1; p > t3; p--) {
             io.hasM = false;
             io.hasP = p < nz - 1;
-            plane_solve<K, M_LOWER3>(F, io, (i64)p * nxy, nx, ny, w2, bar, myex, parity);
+            plane_solve<K, M_LOWER3>(F, io, (i64)p * nxy, nx, ny, w2, bar, myex, parity,
+                                     p - 1 > t3 ? (i64)(p - 1) * nxy : -1, io.b, F.u3);
         }
     }
     __syncthreads();
@@ -279,12 +458,16 @@ __global__ void __launch_bounds__(128) k_ntd_apply(const double *__restrict__ pr
     // level-3 upper sweep (ntd_solve.py:233-253)
     if (pair == 0) {
         io.nbrUp = true;
+        if (t3 > 0) prefetch_plane(F, F.u3, io.x, (i64)(t3 - 1) * nxy, nx, ny, w2);
         for (int p = t3 - 1; p >= 0; p--)
-            plane_solve<K, M_UPPER3>(F, io, (i64)p * nxy, nx, ny, w2, bar, myex, parity);
+            plane_solve<K, M_UPPER3>(F, io, (i64)p * nxy, nx, ny, w2, bar, myex, parity,
+                                     p > 0 ? (i64)(p - 1) * nxy : -1, F.u3, io.x);
     } else {
         io.nbrUp = false;
+        if (t3 + 1 < nz) prefetch_plane(F, F.l3, io.x, (i64)(t3 + 1) * nxy, nx, ny, w2);
         for (int p = t3 + 1; p < nz; p++)
-            plane_solve<K, M_UPPER3>(F, io, (i64)p * nxy, nx, ny, w2, bar, myex, parity);
+            plane_solve<K, M_UPPER3>(F, io, (i64)p * nxy, nx, ny, w2, bar, myex, parity,
+                                     p + 1 < nz ? (i64)(p + 1) * nxy : -1, F.l3, io.x);
     }
 }
 

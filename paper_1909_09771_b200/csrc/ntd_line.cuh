@@ -41,37 +41,38 @@ __device__ __forceinline__ void line_solve(const LineGeom<K> &g, const double (&
                                            const double (&offU)[K], const double (&rhs)[K], double bt, double mrt,
                                            double l1t, double u1t, double (&x)[K], double &xt)
 {
-    double Ap[K], Cp[K];
-    // ---- lower phase: x_j = (rhs_j - offL_j x_{j-1}) mr_j, x_{-1} = 0
+    // ---- lower phase: x_j = (rhs_j - offL_j x_{j-1}) mr_j, x_{-1} = 0.
+    // Each lane composes its K affine maps, a 16-lane Kogge-Stone scan gives
+    // the carry into the lane, and the lane re-walks its K slots from it
+    // (no per-slot prefix storage: keeps registers for operand prefetch).
     double A = 1.0, C = 0.0;
 #pragma unroll
     for (int k = 0; k < K; k++) {
-        double a = 1.0, c = 0.0;
         if (g.valid(k)) {
-            a = -offL[k] * mr[k];
-            c = rhs[k] * mr[k];
+            const double a = -offL[k] * mr[k];
+            C = fma(a, C, rhs[k] * mr[k]);
+            A = a * A;
         }
-        C = fma(a, C, c);
-        A = a * A;
-        Ap[k] = A;
-        Cp[k] = C;
     }
 #pragma unroll
     for (int d = 1; d < 16; d <<= 1) {
-        double Ao = __shfl_up_sync(FULL_MASK, A, d, 16);
-        double Co = __shfl_up_sync(FULL_MASK, C, d, 16);
+        const double Ao = __shfl_up_sync(FULL_MASK, A, d, 16);
+        const double Co = __shfl_up_sync(FULL_MASK, C, d, 16);
         if (g.s >= d) {
             C = fma(A, Co, C);
             A = A * Ao;
         }
     }
-    double xin = __shfl_up_sync(FULL_MASK, C, 1, 16);
-    if (g.s == 0) xin = 0.0;
+    double xc = __shfl_up_sync(FULL_MASK, C, 1, 16);
+    if (g.s == 0) xc = 0.0;
 #pragma unroll
-    for (int k = 0; k < K; k++) x[k] = fma(Ap[k], xin, Cp[k]);
+    for (int k = 0; k < K; k++) {
+        if (g.valid(k)) xc = fma(-offL[k] * mr[k], xc, rhs[k] * mr[k]);
+        x[k] = xc;  // padding slots carry the chain end through
+    }
     // ---- twist row (ntd_solve.py:115-121)
-    double xa = __shfl_sync(FULL_MASK, x[K - 1], 15);
-    double xd = __shfl_sync(FULL_MASK, x[K - 1], 31);
+    const double xa = __shfl_sync(FULL_MASK, x[K - 1], 15);
+    const double xd = __shfl_sync(FULL_MASK, x[K - 1], 31);
     double acc = bt;
     if (g.t > 0) acc -= l1t * xa;
     if (g.t < g.n - 1) acc -= u1t * xd;
@@ -82,30 +83,31 @@ __device__ __forceinline__ void line_solve(const LineGeom<K> &g, const double (&
     C = 0.0;
 #pragma unroll
     for (int k = K - 1; k >= 0; k--) {
-        double a = 1.0, c = 0.0;
         if (g.valid(k)) {
-            a = -(mr[k] * offU[k]);
-            c = x[k];
+            const double a = -(mr[k] * offU[k]);
+            C = fma(a, C, x[k]);
+            A = a * A;
         }
-        C = fma(a, C, c);
-        A = a * A;
-        Ap[k] = A;
-        Cp[k] = C;
     }
 #pragma unroll
     for (int d = 1; d < 16; d <<= 1) {
-        double Ao = __shfl_down_sync(FULL_MASK, A, d, 16);
-        double Co = __shfl_down_sync(FULL_MASK, C, d, 16);
+        const double Ao = __shfl_down_sync(FULL_MASK, A, d, 16);
+        const double Co = __shfl_down_sync(FULL_MASK, C, d, 16);
         if (g.s + d < 16) {
             C = fma(A, Co, C);
             A = A * Ao;
         }
     }
-    double An = __shfl_down_sync(FULL_MASK, A, 1, 16);
-    double Cn = __shfl_down_sync(FULL_MASK, C, 1, 16);
-    double xin2 = (g.s == 15) ? xt : fma(An, xt, Cn);
+    const double An = __shfl_down_sync(FULL_MASK, A, 1, 16);
+    const double Cn = __shfl_down_sync(FULL_MASK, C, 1, 16);
+    xc = (g.s == 15) ? xt : fma(An, xt, Cn);
 #pragma unroll
-    for (int k = 0; k < K; k++) x[k] = fma(Ap[k], xin2, Cp[k]);
+    for (int k = K - 1; k >= 0; k--) {
+        if (g.valid(k)) {
+            xc = fma(-(mr[k] * offU[k]), xc, x[k]);
+            x[k] = xc;
+        }
+    }
 }
 
 // Load the per-slot factor operands of one line whose cells start at `base`.

@@ -42,14 +42,25 @@ def ntd_factor(a_dev, nx, ny, nz, batch):
     return pre, status.cpu()
 
 
-def ntd_apply(pre_dev, b_dev, nx, ny, nz, batch, x=None, work=None, active=None):
+def solve_bands(pre_dev, nx, ny, nz, batch):
+    """Apply-side solve arrays of a factor (slot layout, chain coefficients
+    precomputed); None when the grid uses the direct apply path."""
+    size = _lib.load().ntd_solve_doubles(nx, ny, nz, batch)
+    if size == 0:
+        return None
+    sv = torch.empty(size, dtype=torch.float64, device=_dev())
+    _lib.call("ntd_solve_bands", _lib.ptr(pre_dev), _lib.ptr(sv), nx, ny, nz, batch, _lib.stream())
+    return sv
+
+
+def ntd_apply(pre_dev, b_dev, nx, ny, nz, batch, x=None, work=None, active=None, solve=None):
     lib = _lib.load()
     if x is None:
         x = torch.empty_like(b_dev)
-    if work is None:
+    if work is None or work.numel() < lib.ntd_apply_work_doubles(nx, ny, nz, batch):
         work = torch.empty(lib.ntd_apply_work_doubles(nx, ny, nz, batch), dtype=torch.float64, device=_dev())
-    _lib.call("ntd_apply", _lib.ptr(pre_dev), _lib.ptr(b_dev), _lib.ptr(x), _lib.ptr(work), nx, ny, nz, batch,
-              _lib.ptr(active), _lib.stream())
+    _lib.call("ntd_apply", _lib.ptr(pre_dev), _lib.ptr(solve), _lib.ptr(b_dev), _lib.ptr(x), _lib.ptr(work), nx,
+              ny, nz, batch, _lib.ptr(active), _lib.stream())
     return x
 
 
@@ -93,11 +104,12 @@ class CombinedDevice:
     """Symmetric ILU0 -> NTD -> ILU0 preconditioner on B systems
     (precond_pcg.py:28-65), all buffers preallocated on the device."""
 
-    def __init__(self, a_dev, nx, ny, nz, batch, pre=None, ilu=None, split=None):
+    def __init__(self, a_dev, nx, ny, nz, batch, pre=None, ilu=None, split=None, solve=None):
         self.a, self.nx, self.ny, self.nz, self.batch = a_dev, nx, ny, nz, batch
         n = nx * ny * nz
         self.n = n
         self.pre = pre
+        self.solve = solve if solve is not None else solve_bands(pre, nx, ny, nz, batch)
         self.ilu = ilu
         self.split = n // 2 if split is None else split
         shape = (batch, n)
@@ -113,7 +125,7 @@ class CombinedDevice:
         g = (self.nx, self.ny, self.nz, self.batch)
         ilu0_apply(self.ilu, self.split, r, *g, z=self.w, active=active)
         residual(self.a, r, self.w, *g, t=self.t, active=active)
-        ntd_apply(self.pre, self.t, *g, x=self.xn, work=self.work, active=active)
+        ntd_apply(self.pre, self.t, *g, x=self.xn, work=self.work, active=active, solve=self.solve)
         residual(self.a, r, self.w, *g, t=self.t, v=self.xn, z_out=z, active=active)
         ilu0_apply(self.ilu, self.split, self.t, *g, z=self.xn, acc=z, active=active)
         return z

@@ -61,10 +61,18 @@ class PreconBands:
         self.twist2 = twist_index(self.ny) if twist2 is None else twist2
         self.twist3 = twist_index(self.nz) if twist3 is None else twist3
         self._host = None
+        self._solve = None
 
     @property
     def n_rows(self):
         return self.nx * self.ny * self.nz
+
+    @property
+    def solve(self):
+        """Apply-side solve arrays on the device (derived from the bands, cached)."""
+        if self._solve is None:
+            self._solve = D.solve_bands(self.bands, self.nx, self.ny, self.nz, 1)
+        return self._solve
 
     def host(self):
         if self._host is None:

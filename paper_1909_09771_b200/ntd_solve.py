@@ -26,7 +26,13 @@ class SolveWorkspace:
 
     def __init__(self, n):
         self.n = int(n)
-        self.scratch = torch.empty(self.n, dtype=torch.float64, device=torch.device("cuda"))
+        self.scratch = None  # sized on first use (depends on the grid shape)
+
+    def work(self, nx, ny, nz):
+        need = _lib.load().ntd_apply_work_doubles(nx, ny, nz, 1)
+        if self.scratch is None or self.scratch.numel() < need:
+            self.scratch = torch.empty(need, dtype=torch.float64, device=torch.device("cuda"))
+        return self.scratch
 
 
 def chain_bidiagonal_solve(diag_recip, offdiag, b, direction="forward", lanes=CHAIN_LANES):
@@ -58,6 +64,6 @@ def ntd_apply(pre, b, workers=1, lanes=CHAIN_LANES, workspace=None):
     if shape_of(b) != (n,):
         raise ValueError(f"rhs length {shape_of(b)} does not match {n} rows")
     bd = as_device(b)
-    work = workspace.scratch if workspace is not None else None
-    x = D.ntd_apply(pre.bands, bd, pre.nx, pre.ny, pre.nz, 1, work=work)
+    work = workspace.work(pre.nx, pre.ny, pre.nz) if workspace is not None else None
+    x = D.ntd_apply(pre.bands, bd, pre.nx, pre.ny, pre.nz, 1, work=work, solve=pre.solve)
     return like_input(x, b)

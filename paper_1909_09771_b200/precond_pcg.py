@@ -55,7 +55,8 @@ class CombinedPrecond:
         self.workspace = SolveWorkspace(a.n_rows)
         self._ad = a.device_data()
         self._dev = D.CombinedDevice(self._ad, a.nx, a.ny, a.nz, 1, pre=self.ntd.bands,
-                                     ilu=self.ilu.device_data, split=self.ilu.split)
+                                     ilu=self.ilu.device_data, split=self.ilu.split,
+                                     solve=self.ntd.solve)
         torch.cuda.current_stream().synchronize()
         self.setup_seconds = perf_counter() - t0
 

@@ -47,10 +47,10 @@ for cfg in (1, 2, 3):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     bd = torch.from_numpy(vv).cuda()
-    ntd.device.ntd_apply(cp.ntd.bands, bd, nx, ny, nz, 1)
+    ntd.device.ntd_apply(cp.ntd.bands, bd, nx, ny, nz, 1, solve=cp.ntd.solve)
     ev0.record()
     for _ in range(5):
-        ntd.device.ntd_apply(cp.ntd.bands, bd, nx, ny, nz, 1)
+        ntd.device.ntd_apply(cp.ntd.bands, bd, nx, ny, nz, 1, solve=cp.ntd.solve)
     ev1.record(); torch.cuda.synchronize()
     print(f"cfg{cfg}: iters {st.iterations} relres {st.final_relres:.3e} setup {ts:.3f}s solve {tsol:.3f}s "
           f"factor_err {ef:.1e} apply_err {ea:.1e} apply_ms {ev0.elapsed_time(ev1)/5:.3f}", flush=True)

@@ -1,0 +1,47 @@
+// Timing breakdown of the warp-specialised NTD apply (debug aid).
+// nvcc -DNTD_TIMING ... micro_apply.cu ../paper_1909_09771_b200/csrc/blas.cu
+#include <cstdio>
+#include <vector>
+#include "ntd_kernels.cuh"
+#include "ntd_apply_v3.cuh"
+
+int main(int argc, char **argv)
+{
+    const int nx = 96, ny = 96, nz = 96, B = 8;
+    const long n = (long)nx * ny * nz;
+    std::vector<double> h(7 * n * B);
+    for (long s = 0; s < B; s++)
+        for (long i = 0; i < n; i++) {
+            double *p = h.data() + s * 7 * n;
+            p[i] = -0.15; p[n + i] = -0.15; p[2 * n + i] = -0.1; p[3 * n + i] = -0.1;
+            p[4 * n + i] = -0.05; p[5 * n + i] = -0.05; p[6 * n + i] = 0.3;
+        }
+    double *pre, *b, *x, *w;
+    cudaMalloc(&pre, 8 * 7 * n * B); cudaMalloc(&b, 8 * n * B); cudaMalloc(&x, 8 * n * B); cudaMalloc(&w, 8 * n * B);
+    cudaMemcpy(pre, h.data(), 8 * 7 * n * B, cudaMemcpyHostToDevice);
+    cudaMemset(b, 0, 8 * n * B);
+    double *sv; cudaMalloc(&sv, 8 * 2 * n * B); cudaMemset(sv, 0, 8 * 2 * n * B);
+    size_t smem = (size_t)4 * 4 * v3::A_N * (nx + 2 * v3::PAD) * 8;
+    cudaFuncSetAttribute(v3::k_apply<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    v3::k_apply<3, 4><<<B, 256, smem>>>(pre, sv, b, x, w, nx, ny, nz, nullptr);
+    cudaDeviceSynchronize();
+    unsigned long long zero[64] = {0};
+    cudaMemcpyToSymbol(g_ntd_timing, zero, sizeof(zero));
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    v3::k_apply<3, 4><<<B, 256, smem>>>(pre, sv, b, x, w, nx, ny, nz, nullptr);
+    cudaEventRecord(e1);
+    cudaDeviceSynchronize();
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    unsigned long long t[8][8];
+    cudaMemcpyFromSymbol(t, g_ntd_timing, sizeof(t));
+    printf("apply %.3f ms  err=%s\n", ms, cudaGetErrorString(cudaGetLastError()));
+    const char *names[] = {"ldg+wait", "lds+rhs", "-", "solve", "store", "-", "-", ""};
+    double steps = 9409.0 / 1.0;
+    for (int w = 0; w < 4; w++) {
+        printf("warp %d:", w);
+        for (int k = 0; k < 7; k++) printf(" %s=%.0f", names[k], t[w][k] / steps);
+        printf("  (cycles per line-step, /9409)\n");
+    }
+    return 0;
+}

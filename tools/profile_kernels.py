@@ -24,7 +24,7 @@ s = BatchSolver(a, nx, ny, nz).setup()
 v = torch.rand_like(b)
 x = torch.empty_like(b)
 for _ in range(2):
-    D.ntd_apply(s.precond.pre, v, nx, ny, nz, B, x=x)
+    D.ntd_apply(s.precond.pre, v, nx, ny, nz, B, x=x, solve=s.precond.solve)
     D.ilu0_apply(s.precond.ilu, s.precond.split, v, nx, ny, nz, B, z=x)
     D.residual(a, v, x, nx, ny, nz, B)
 torch.cuda.synchronize()
