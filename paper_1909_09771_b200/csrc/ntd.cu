@@ -41,7 +41,7 @@ extern "C" int64_t ntd_max_nx(void) { return 32 * MAX_K; }
 static int sl_depth(int K)
 {
     if (K > 11) return 0;
-    const size_t per_stage = (size_t)4 * sl::RSEG * sl::lr_of(K) * 8;
+    const size_t per_stage = (size_t)4 * sl::stage_of(K) * 8;
     return per_stage * 4 <= 200 * 1024 ? 4 : (per_stage * 2 <= 200 * 1024 ? 2 : 0);
 }
 
@@ -55,14 +55,15 @@ extern "C" int64_t ntd_solve_doubles(int64_t nx, int64_t ny, int64_t nz, int64_t
 {
     const int K = pick_k(nx);
     if (K <= 0 || !sl_depth(K)) return 0;
-    return (int64_t)sl::SL_N * sl_doubles(nx, ny, nz) * batch;
+    return (int64_t)sl::recd_of(K) * ny * nz * batch;
 }
 
 extern "C" int64_t ntd_apply_work_doubles(int64_t nx, int64_t ny, int64_t nz, int64_t batch)
 {
     const i64 n = nx * ny * nz * batch;
     const i64 s = sl_doubles(nx, ny, nz) * batch;
-    const i64 w = 3 * s + (i64)sl::SL_N * s;  // b, x, xs in SL (+ solve arrays if not given)
+    const int K = pick_k(nx);
+    const i64 w = 3 * s + (K > 0 ? (i64)sl::recd_of(K) * ny * nz * batch : 0);  // b, x, xs in SL (+ solve records)
     return w > n ? w : n;
 }
 
@@ -77,7 +78,15 @@ extern "C" int ntd_solve_bands(const double *pre, double *solve, int64_t nx, int
     i64 blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     sl::k_solve_sl<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(pre, solve, (int)nx, lines, K, batch);
-    return ntd::check_launch("ntd_solve_bands");
+    int rc = ntd::check_launch("ntd_solve_bands");
+    if (rc) return rc;
+    switch (K) {
+#define PREPCASE(KK) \
+    case KK: return launch_prep_sl_k<KK>(solve, lines * batch, (cudaStream_t)stream);
+        PREPCASE(1) PREPCASE(2) PREPCASE(3) PREPCASE(4) PREPCASE(5) PREPCASE(6) PREPCASE(8) PREPCASE(11)
+#undef PREPCASE
+    default: return NTD_ENOTSUP;
+    }
 }
 
 static unsigned grid_for(i64 total)

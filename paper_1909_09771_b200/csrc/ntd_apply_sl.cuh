@@ -23,13 +23,23 @@
 // values of this plane) are loaded by the solver one line ahead.
 #pragma once
 #include "ntd_kernels.cuh"
+#include "ntd_line4.cuh"
 
 namespace sl {
 
+#ifndef NTD_SL_PREFETCH_PLANES
+#define NTD_SL_PREFETCH_PLANES 0
+#endif
+constexpr bool PREFETCH_PLANES = NTD_SL_PREFETCH_PLANES;  // whole-next-plane L2 prefetch (off: the TMA ring runs far enough ahead)
+
 enum { SL_MR = 0, SL_NL, SL_NU, SL_L2, SL_U2, SL_L3, SL_U3, SL_N };  // solve arrays (SL)
-constexpr int RSEG = 7;                                             // ring segments per stage
+constexpr int NPREP = 15;  // LinePrep coefficients per lane, stored [coef][lane] after the arrays
 
 __host__ __device__ constexpr int lr_of(int K) { return 32 * K + 2; }
+// doubles per line of the solve record: 7 SL arrays + the line's scan coefficients
+__host__ __device__ constexpr int recd_of(int K) { return SL_N * lr_of(K) + NPREP * 32; }
+// ring stage: one solve record + one extra line (b or xo)
+__host__ __device__ constexpr int stage_of(int K) { return recd_of(K) + lr_of(K); }
 
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(void *bar)
@@ -107,16 +117,17 @@ static __global__ void k_solve_sl(const double *__restrict__ pre, double *__rest
             if (j >= 0) c = nx - 1 - j;
         }
         const double *p = pre + s * 7 * n;
-        double *o = solve + s * SL_N * nsl;
+        // record-major: [system][line][array][LR] -> one bulk copy per line
+        double *o = solve + (s * lines + line) * (i64)(SL_N * LR + NPREP * 32) + r;
         const i64 g = line * nx + c;
         const double m = c >= 0 ? p[6 * n + g] : 0.0;
-        o[SL_MR * nsl + el] = m;
-        o[SL_NL * nsl + el] = c >= 0 ? -(p[g] * m) : 0.0;
-        o[SL_NU * nsl + el] = c >= 0 ? -(p[n + g] * m) : 0.0;
-        o[SL_L2 * nsl + el] = c >= 0 ? p[2 * n + g] : 0.0;
-        o[SL_U2 * nsl + el] = c >= 0 ? p[3 * n + g] : 0.0;
-        o[SL_L3 * nsl + el] = c >= 0 ? p[4 * n + g] : 0.0;
-        o[SL_U3 * nsl + el] = c >= 0 ? p[5 * n + g] : 0.0;
+        o[SL_MR * LR] = m;
+        o[SL_NL * LR] = c >= 0 ? -(p[g] * m) : 0.0;
+        o[SL_NU * LR] = c >= 0 ? -(p[n + g] * m) : 0.0;
+        o[SL_L2 * LR] = c >= 0 ? p[2 * n + g] : 0.0;
+        o[SL_U2 * LR] = c >= 0 ? p[3 * n + g] : 0.0;
+        o[SL_L3 * LR] = c >= 0 ? p[4 * n + g] : 0.0;
+        o[SL_U3 * LR] = c >= 0 ? p[5 * n + g] : 0.0;
     }
 }
 
@@ -182,7 +193,7 @@ __device__ __forceinline__ void line_solve(int s, int n, int t, const double (&a
 
 // ---------------------------------------------------------------- data
 struct SlArrays {  // one system, SL
-    const double *a[SL_N];
+    const double *solve;  // record-major solve records [line][recd_of(K)]
     const double *b;
     double *x, *xs;
     i64 nsl;
@@ -218,25 +229,32 @@ __device__ __forceinline__ void ld_rec(const double *rec, const LaneSl<K> &L, do
 template <int K>
 __device__ __forceinline__ void st_rec(double *rec, const LaneSl<K> &L, const double (&v)[K], double vt, int lane)
 {
+    (void)lane;
 #pragma unroll
     for (int k = 0; k < K; k++) rec[L.base + k] = v[k];
-    if (lane == 0) rec[L.tw] = vt;
+    rec[L.tw] = vt;  // every lane holds the same twist value: branch-free
 }
 
 // ring of D stages x RSEG line records per solver warp
-enum { G_MR = 0, G_NL, G_NU, G_CP, G_R0, G_C1, G_C2 };  // lower: all; upper: R0 = xo
+constexpr int G_X = SL_N;      // ring segment holding b (lower lines of LOWER3) or xo (upper lines of UPPER3)
+constexpr int G_PREP = SL_N + 1;  // the record's scan coefficients
 
 template <int K, int D>
 struct Ring {
     double *base;
     unsigned long long *full, *empty;
-    __device__ __forceinline__ double *seg(int st, int g) const { return base + ((size_t)st * RSEG + g) * lr_of(K); }
+    __device__ __forceinline__ double *seg(int st, int g) const
+    {
+        double *b0 = base + (size_t)st * stage_of(K);
+        return g < SL_N ? b0 + g * lr_of(K) : (g == G_X ? b0 + recd_of(K) : b0 + SL_N * lr_of(K));
+    }
 };
 
 struct PlaneDesc {
     i64 prec;      // record index of the plane's first line (plane * ny)
     int mode;      // M_LOWER3 / M_UPPER3
     bool hasM, hasP, nbrUp;
+    bool up;       // lower sweep: the level-3 neighbour is plane p+1 (descending half)
 };
 
 struct Seq {
@@ -244,6 +262,47 @@ struct Seq {
     __device__ __forceinline__ int qlow(int i) const { return w2 == 0 ? i : ny - 1 - i; }
     __device__ __forceinline__ int qup(int i) const { return w2 == 0 ? t2 - 1 - i : t2 + 1 + i; }
 };
+
+__device__ __forceinline__ LinePrep read_prep(const double *pp, int lane)
+{
+    LinePrep P;
+    P.p1 = pp[0 * 32 + lane];
+    P.p2 = pp[1 * 32 + lane];
+    P.p3 = pp[2 * 32 + lane];
+    P.e0 = pp[3 * 32 + lane];
+    P.e1 = pp[4 * 32 + lane];
+    P.e2 = pp[5 * 32 + lane];
+    P.e3 = pp[6 * 32 + lane];
+    P.q1 = pp[7 * 32 + lane];
+    P.q2 = pp[8 * 32 + lane];
+    P.q3 = pp[9 * 32 + lane];
+    P.f0 = pp[10 * 32 + lane];
+    P.f1 = pp[11 * 32 + lane];
+    P.f2 = pp[12 * 32 + lane];
+    P.f3 = pp[13 * 32 + lane];
+    P.bex = pp[14 * 32 + lane];
+    return P;
+}
+
+// scan coefficients of every line (setup): one warp per line
+template <int K>
+__global__ void k_prep_sl(double *__restrict__ solve, i64 lines_total)
+{
+    constexpr int LR = lr_of(K);
+    const int lane = threadIdx.x & 31;
+    const i64 line = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+    if (line >= lines_total) return;
+    double *rec = solve + line * (i64)recd_of(K);
+    const LaneSl<K> L(lane);
+    double aL[K], aU[K];
+    ld_rec(rec + (L.desc ? SL_NU : SL_NL) * LR, L, aL);
+    ld_rec(rec + (L.desc ? SL_NL : SL_NU) * LR, L, aU);
+    const LinePrep P = line_prep<K>(lane & 15, aL, aU);
+    double *pp = rec + SL_N * LR;
+    const double v[NPREP] = {P.p1, P.p2, P.p3, P.e0, P.e1, P.e2, P.e3, P.q1, P.q2, P.q3, P.f0, P.f1, P.f2, P.f3, P.bex};
+#pragma unroll
+    for (int c = 0; c < NPREP; c++) pp[c * 32 + lane] = v[c];
+}
 
 // ---------------- producer: bulk copies of one plane's line records
 template <int K, int D>
@@ -253,41 +312,20 @@ __device__ void produce_plane(const SlArrays &S, const PlaneDesc &P, const Seq &
     const int lane = threadIdx.x & 31;
     constexpr int LR = lr_of(K);
     const unsigned rbytes = LR * 8u;
-    const i64 nyl = Q.ny;
-    const double *cplL = Q.w2 == 0 ? S.a[SL_L2] : S.a[SL_U2];
-    const double *cplU = Q.w2 == 0 ? S.a[SL_U2] : S.a[SL_L2];
-    const double *c1 = nullptr, *c2 = nullptr;
-    if (P.mode == M_LOWER3) {
-        if (P.hasM) c1 = S.a[SL_L3];
-        if (P.hasP) (c1 ? c2 : c1) = S.a[SL_U3];
-    } else {
-        c1 = P.nbrUp ? S.a[SL_U3] : S.a[SL_L3];
-    }
+    const unsigned recbytes = recd_of(K) * 8u;
     for (int ph = 0; ph < 2; ph++) {
         for (int i = 0; i < Q.cnt; i++, rec++) {
             if (lane == 0) {
                 const int st = rec % D;
-                if (rec >= (unsigned)D) mbar_wait(&R.empty[st], ((rec / D) + 1) & 1);
+                if (rec >= (unsigned)D) mbar_wait_lazy(&R.empty[st], ((rec / D) + 1) & 1);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 unsigned long long *bar = &R.full[st];
                 const int q = ph == 0 ? Q.qlow(i) : Q.qup(i);
-                const i64 off = (P.prec + q) * (i64)LR;
-                (void)nyl;
-                unsigned narr = 3;
-                if (ph == 0) narr += (i > 0) + (P.mode == M_LOWER3) + (c1 != nullptr) + (c2 != nullptr);
-                else narr += 1 + (P.mode == M_UPPER3);
-                mbar_expect_tx(bar, narr * rbytes);
-                tma_load_1d(R.seg(st, G_MR), S.a[SL_MR] + off, rbytes, bar);
-                tma_load_1d(R.seg(st, G_NL), S.a[SL_NL] + off, rbytes, bar);
-                tma_load_1d(R.seg(st, G_NU), S.a[SL_NU] + off, rbytes, bar);
-                if (ph == 0) {
-                    if (i > 0) tma_load_1d(R.seg(st, G_CP), cplL + off, rbytes, bar);
-                    if (P.mode == M_LOWER3) tma_load_1d(R.seg(st, G_R0), S.b + off, rbytes, bar);
-                    if (c1) tma_load_1d(R.seg(st, G_C1), c1 + off, rbytes, bar);
-                    if (c2) tma_load_1d(R.seg(st, G_C2), c2 + off, rbytes, bar);
-                } else {
-                    tma_load_1d(R.seg(st, G_CP), cplU + off, rbytes, bar);
-                    if (P.mode == M_UPPER3) tma_load_1d(R.seg(st, G_R0), S.x + off, rbytes, bar);
-                }
+                const i64 line = P.prec + q;
+                const bool extra = ph == 0 ? P.mode == M_LOWER3 : P.mode == M_UPPER3;
+                mbar_expect_tx(bar, recbytes + (extra ? rbytes : 0u));
+                tma_load_1d(R.seg(st, 0), S.solve + line * (i64)recd_of(K), recbytes, bar);
+                if (extra) tma_load_1d(R.seg(st, G_X), (ph == 0 ? S.b : S.x) + line * (i64)LR, rbytes, bar);
             }
         }
     }
@@ -295,7 +333,7 @@ __device__ void produce_plane(const SlArrays &S, const PlaneDesc &P, const Seq &
 }
 
 // ---------------- solver: one plane
-template <int K, int D>
+template <int K, int D, int MODE, bool TWO>
 __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q, int nx, int bar_id, double *ex,
                             int &parity, const Ring<K, D> &R, const LaneSl<K> &L, unsigned &rec)
 {
@@ -305,16 +343,32 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
     const i64 plr = (i64)ny * LR;  // plane stride in SL
     const bool lower3 = P.mode == M_LOWER3;
     // x-dependent neighbour planes
-    const double *y1 = nullptr, *y2 = nullptr;
+    // Neighbour planes.  A missing neighbour has an exactly-zero l3/u3
+    // coefficient (first/last plane), so it is pointed at this plane's own
+    // (finite, zero-initialised) x record instead of branching.
+    const double *y1, *y2 = S.x;
+    int gC1;
     if (lower3) {
-        if (P.hasM) y1 = S.x - plr;
-        if (P.hasP) (y1 ? y2 : y1) = S.x + plr;
+        if (TWO) {
+            gC1 = SL_L3;
+            y1 = P.hasM ? S.x - plr : S.x;
+            y2 = P.hasP ? S.x + plr : S.x;
+        } else if (P.up) {
+            gC1 = SL_U3;
+            y1 = P.hasP ? S.x + plr : S.x;
+        } else {
+            gC1 = SL_L3;
+            y1 = P.hasM ? S.x - plr : S.x;
+        }
     } else {
+        gC1 = P.nbrUp ? SL_U3 : SL_L3;
         y1 = P.nbrUp ? S.x + plr : S.x - plr;
     }
     double *xlow = lower3 ? S.x : S.xs;  // lower-sweep store of this plane
-    const int gL = L.desc ? G_NU : G_NL, gU = L.desc ? G_NL : G_NU;
+    const int gL = L.desc ? SL_NU : SL_NL, gU = L.desc ? SL_NL : SL_NU;
+    const int gCL = w2 == 0 ? SL_L2 : SL_U2, gCU = w2 == 0 ? SL_U2 : SL_L2;
     auto recp = [&](const double *base, int q) { return base + (P.prec + q) * (i64)LR; };
+    auto srec = [&](int a, int q) { return S.solve + (P.prec + q) * (i64)recd_of(K) + a * LR; };
     auto recw = [&](double *base, int q) { return base + (P.prec + q) * (i64)LR; };
     double xprev[K], xprevt = 0.0;
 #pragma unroll
@@ -324,8 +378,8 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
 #pragma unroll
     for (int k = 0; k < K; k++) n1[k] = n2[k] = 0.0;
     if (cnt > 0) {
-        if (y1) ld_rec(recp(y1, Q.qlow(0)), L, n1, n1t);
-        if (y2) ld_rec(recp(y2, Q.qlow(0)), L, n2, n2t);
+        ld_rec(recp(y1, Q.qlow(0)), L, n1, n1t);
+        if (TWO) ld_rec(recp(y2, Q.qlow(0)), L, n2, n2t);
     }
     for (int i = 0; i < cnt; i++, rec++) {
         double v1[K], v1t = n1t, v2[K], v2t = n2t;
@@ -335,52 +389,64 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
             v2[k] = n2[k];
         }
         if (i + 1 < cnt) {
-            if (y1) ld_rec(recp(y1, Q.qlow(i + 1)), L, n1, n1t);
-            if (y2) ld_rec(recp(y2, Q.qlow(i + 1)), L, n2, n2t);
+            ld_rec(recp(y1, Q.qlow(i + 1)), L, n1, n1t);
+            if (TWO) ld_rec(recp(y2, Q.qlow(i + 1)), L, n2, n2t);
         }
         const int st = rec % D;
+        TSTAMP(q1);
         mbar_wait(&R.full[st], (rec / D) & 1);
+        TSTAMP(q2);
+        TACC(0, q1, q2);
         double aL[K], mr[K], aU[K], rhs[K], mrt, nlt, nut, rhst;
-        ld_rec(R.seg(st, G_MR), L, mr, mrt);
+        ld_rec(R.seg(st, SL_MR), L, mr, mrt);
         ld_rec(R.seg(st, gL), L, aL);
         ld_rec(R.seg(st, gU), L, aU);
-        nlt = R.seg(st, G_NL)[L.tw];
-        nut = R.seg(st, G_NU)[L.tw];
+        nlt = R.seg(st, SL_NL)[L.tw];
+        nut = R.seg(st, SL_NU)[L.tw];
         if (lower3) {
-            ld_rec(R.seg(st, G_R0), L, rhs, rhst);
-            if (y1) {
+            ld_rec(R.seg(st, G_X), L, rhs, rhst);
+            {
                 double c[K], ct;
-                ld_rec(R.seg(st, G_C1), L, c, ct);
+                ld_rec(R.seg(st, gC1), L, c, ct);
 #pragma unroll
                 for (int k = 0; k < K; k++) rhs[k] -= c[k] * v1[k];
                 rhst -= ct * v1t;
             }
-            if (y2) {
+            if (TWO) {
                 double c[K], ct;
-                ld_rec(R.seg(st, G_C2), L, c, ct);
+                ld_rec(R.seg(st, SL_U3), L, c, ct);
 #pragma unroll
                 for (int k = 0; k < K; k++) rhs[k] -= c[k] * v2[k];
                 rhst -= ct * v2t;
             }
         } else {
             double c[K], ct;
-            ld_rec(R.seg(st, G_C1), L, c, ct);
+            ld_rec(R.seg(st, gC1), L, c, ct);
 #pragma unroll
             for (int k = 0; k < K; k++) rhs[k] = c[k] * v1[k];
             rhst = ct * v1t;
         }
-        if (i > 0) {
-            double cp[K], cpt;
-            ld_rec(R.seg(st, G_CP), L, cp, cpt);
+        {
+            double cp[K], cpt;  // line 0: xprev = 0, so the term vanishes
+            ld_rec(R.seg(st, gCL), L, cp, cpt);
 #pragma unroll
             for (int k = 0; k < K; k++) rhs[k] -= cp[k] * xprev[k];
             rhst -= cpt * xprevt;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&R.empty[st]);
+        const int st_rel = st;
+        TSTAMP(q3);
+        TACC(1, q2, q3);
         double x[K], xt;
-        line_solve<K>(s, nx, t, aL, mr, aU, rhs, rhst, mrt, nlt, nut, x, xt);
+        { const LinePrep PP_ = read_prep(R.seg(st_rel, G_PREP), lane); double cr_[K];
+#pragma unroll
+        for (int k_ = 0; k_ < K; k_++) cr_[k_] = (rhs)[k_] * mr[k_];
+        line_solve4<K>(PP_, nx, t, aL, cr_, aU, (rhst) * mrt, nlt, nut, x, xt); }
+        TSTAMP(q4);
+        TACC(2, q3, q4);
+        mbar_arrive(&R.empty[st_rel]);
         st_rec(recw(xlow, Q.qlow(i)), L, x, xt, lane);
+        TSTAMP(q5);
+        TACC(3, q4, q5);
 #pragma unroll
         for (int k = 0; k < K; k++) xprev[k] = x[k];
         xprevt = xt;
@@ -414,16 +480,16 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
     {
         const int q = t2;
         double aL[K], mr[K], aU[K], mrt, nlt, nut, rhs[K], rhst;
-        ld_rec(recp(S.a[SL_MR], q), L, mr, mrt);
-        ld_rec(recp(L.desc ? S.a[SL_NU] : S.a[SL_NL], q), L, aL);
-        ld_rec(recp(L.desc ? S.a[SL_NL] : S.a[SL_NU], q), L, aU);
-        nlt = recp(S.a[SL_NL], q)[L.tw];
-        nut = recp(S.a[SL_NU], q)[L.tw];
+        ld_rec(srec(SL_MR, q), L, mr, mrt);
+        ld_rec(srec(gL, q), L, aL);
+        ld_rec(srec(gU, q), L, aU);
+        nlt = srec(SL_NL, q)[L.tw];
+        nut = srec(SL_NU, q)[L.tw];
         if (lower3) {
             ld_rec(recp(S.b, q), L, rhs, rhst);
             if (P.hasM) {
                 double c[K], ct, y[K], yt;
-                ld_rec(recp(S.a[SL_L3], q), L, c, ct);
+                ld_rec(srec(SL_L3, q), L, c, ct);
                 ld_rec(recp(S.x - plr, q), L, y, yt);
 #pragma unroll
                 for (int k = 0; k < K; k++) rhs[k] -= c[k] * y[k];
@@ -431,7 +497,7 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
             }
             if (P.hasP) {
                 double c[K], ct, y[K], yt;
-                ld_rec(recp(S.a[SL_U3], q), L, c, ct);
+                ld_rec(srec(SL_U3, q), L, c, ct);
                 ld_rec(recp(S.x + plr, q), L, y, yt);
 #pragma unroll
                 for (int k = 0; k < K; k++) rhs[k] -= c[k] * y[k];
@@ -439,7 +505,7 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
             }
         } else {
             double c[K], ct, y[K], yt;
-            ld_rec(recp(P.nbrUp ? S.a[SL_U3] : S.a[SL_L3], q), L, c, ct);
+            ld_rec(srec(gC1, q), L, c, ct);
             ld_rec(recp(y1, q), L, y, yt);
 #pragma unroll
             for (int k = 0; k < K; k++) rhs[k] = c[k] * y[k];
@@ -447,20 +513,23 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
         }
         if (t2 > 0) {
             double c[K], ct;
-            ld_rec(recp(S.a[SL_L2], q), L, c, ct);
+            ld_rec(srec(SL_L2, q), L, c, ct);
 #pragma unroll
             for (int k = 0; k < K; k++) rhs[k] -= c[k] * xa[k];
             rhst -= ct * xat;
         }
         if (t2 < ny - 1) {
             double c[K], ct;
-            ld_rec(recp(S.a[SL_U2], q), L, c, ct);
+            ld_rec(srec(SL_U2, q), L, c, ct);
 #pragma unroll
             for (int k = 0; k < K; k++) rhs[k] -= c[k] * xd[k];
             rhst -= ct * xdt;
         }
         if (cnt > 0) ld_rec(recp(xlow, Q.qup(0)), L, yv, yvt);  // first upper line's lower value
-        line_solve<K>(s, nx, t, aL, mr, aU, rhs, rhst, mrt, nlt, nut, xn, xnt);
+        { const LinePrep PP_ = line_prep<K>(s, aL, aU); double cr_[K];
+#pragma unroll
+        for (int k_ = 0; k_ < K; k_++) cr_[k_] = (rhs)[k_] * mr[k_];
+        line_solve4<K>(PP_, nx, t, aL, cr_, aU, (rhst) * mrt, nlt, nut, xn, xnt); }
         if (w2 == 0) {
             if (lower3) {
                 st_rec(recw(S.x, q), L, xn, xnt, lane);
@@ -482,21 +551,24 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
         const int st = rec % D;
         mbar_wait(&R.full[st], (rec / D) & 1);
         double aL[K], mr[K], aU[K], cp[K], mrt, nlt, nut, cpt;
-        ld_rec(R.seg(st, G_MR), L, mr, mrt);
+        ld_rec(R.seg(st, SL_MR), L, mr, mrt);
         ld_rec(R.seg(st, gL), L, aL);
         ld_rec(R.seg(st, gU), L, aU);
-        nlt = R.seg(st, G_NL)[L.tw];
-        nut = R.seg(st, G_NU)[L.tw];
-        ld_rec(R.seg(st, G_CP), L, cp, cpt);
+        nlt = R.seg(st, SL_NL)[L.tw];
+        nut = R.seg(st, SL_NU)[L.tw];
+        ld_rec(R.seg(st, gCU), L, cp, cpt);
         double xo[K], xot = 0.0;
-        if (!lower3) ld_rec(R.seg(st, G_R0), L, xo, xot);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&R.empty[st]);
+        if (!lower3) ld_rec(R.seg(st, G_X), L, xo, xot);
+        const int st_rel = st;
         double bs[K];
 #pragma unroll
         for (int k = 0; k < K; k++) bs[k] = cp[k] * xn[k];
         double xs[K], xst;
-        line_solve<K>(s, nx, t, aL, mr, aU, bs, cpt * xnt, mrt, nlt, nut, xs, xst);
+        { const LinePrep PP_ = read_prep(R.seg(st_rel, G_PREP), lane); double cr_[K];
+#pragma unroll
+        for (int k_ = 0; k_ < K; k_++) cr_[k_] = (bs)[k_] * mr[k_];
+        line_solve4<K>(PP_, nx, t, aL, cr_, aU, (cpt * xnt) * mrt, nlt, nut, xs, xst); }
+        mbar_arrive(&R.empty[st_rel]);
 #pragma unroll
         for (int k = 0; k < K; k++) xn[k] = y[k] - xs[k];
         xnt = yt - xst;
@@ -533,7 +605,7 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
     if (active && !active[sys]) return;
     const i64 nsl = (i64)nz * ny * LR;
     SlArrays S;
-    for (int a = 0; a < SL_N; a++) S.a[a] = solve + (sys * SL_N + a) * nsl;
+    S.solve = solve + sys * (i64)nz * ny * recd_of(K);
     S.b = bsl + sys * nsl;
     S.x = xsl + sys * nsl;
     S.xs = xssl + sys * nsl;
@@ -542,13 +614,13 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
     const bool producer = warp >= 4;
     const int sw = warp & 3, pair = sw >> 1, w2 = sw & 1, bar = 1 + pair;
     Ring<K, D> R;
-    R.base = sl_ring + (size_t)sw * D * RSEG * LR;
+    R.base = sl_ring + (size_t)sw * D * stage_of(K);
     R.full = bars[sw];
     R.empty = bars[sw] + D;
     if (!producer && lane == 0) {
         for (int st = 0; st < D; st++) {
             mbar_init(&R.full[st], 1);
-            mbar_init(&R.empty[st], 1);
+            mbar_init(&R.empty[st], 32);  // every solver lane arrives: no divergent branch
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -567,8 +639,9 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
     // warp's row range of a plane (for L2 prefetch)
     const i64 wr0 = w2 == 0 ? 0 : (i64)Q.t2 * LR, wr1 = w2 == 0 ? (i64)(Q.t2 + 1) * LR : plr;
     auto prefetch_plane_sl = [&](int p, bool upper) {
+        if (!PREFETCH_PLANES) return;
         const i64 b0 = (i64)p * plr;
-        for (int a = 0; a < SL_N; a++) prefetch_sl(S.a[a], b0 + wr0, b0 + wr1);
+        prefetch_sl(S.solve, (b0 + wr0) / LR * recd_of(K), (b0 + wr1) / LR * recd_of(K));
         prefetch_sl(upper ? S.x : S.b, b0 + wr0, b0 + wr1);
     };
     // level-3 lower sweep (ntd_solve.py:198-221)
@@ -582,11 +655,12 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
         P.hasM = pair == 0 && p > 0;
         P.hasP = pair == 1 && p < nz - 1;
         P.nbrUp = false;
+        P.up = pair == 1;
         if (producer) {
             if (i + 1 < nlow) prefetch_plane_sl(pair == 0 ? p + 1 : p - 1, false);
             produce_plane<K, D>(S, P, Q, R, rec);
         } else {
-            solve_plane<K, D>(S, P, Q, nx, bar, myex, parity, R, L, rec);
+            solve_plane<K, D, M_LOWER3, false>(S, P, Q, nx, bar, myex, parity, R, L, rec);
         }
     }
     __syncthreads();
@@ -598,11 +672,12 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
         P.hasM = t3 > 0;
         P.hasP = t3 < nz - 1;
         P.nbrUp = false;
+        P.up = false;
         if (producer) {
             fence_proxy_async();
             produce_plane<K, D>(S, P, Q, R, rec);
         } else {
-            solve_plane<K, D>(S, P, Q, nx, bar, myex, parity, R, L, rec);
+            solve_plane<K, D, M_LOWER3, true>(S, P, Q, nx, bar, myex, parity, R, L, rec);
         }
     }
     __syncthreads();
@@ -616,11 +691,12 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
         P.mode = M_UPPER3;
         P.hasM = P.hasP = false;
         P.nbrUp = pair == 0;
+        P.up = false;
         if (producer) {
             if (i + 1 < nlow) prefetch_plane_sl(pair == 0 ? p - 1 : p + 1, true);
             produce_plane<K, D>(S, P, Q, R, rec);
         } else {
-            solve_plane<K, D>(S, P, Q, nx, bar, myex, parity, R, L, rec);
+            solve_plane<K, D, M_UPPER3, false>(S, P, Q, nx, bar, myex, parity, R, L, rec);
         }
     }
 }
@@ -628,15 +704,24 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
 }  // namespace sl
 
 template <int K>
+int launch_prep_sl_k(double *solve, i64 lines_total, cudaStream_t st);
+template <int K>
 int launch_apply_sl_k(const double *solve, const double *bsl, double *xsl, double *xssl, int nx, int ny, int nz,
                       i64 batch, const int32_t *active, cudaStream_t st, int depth);
 
 #define NTD_INSTANTIATE_SL(K)                                                                                     \
     template <>                                                                                                    \
+    int launch_prep_sl_k<K>(double *solve, i64 lines_total, cudaStream_t st)                                      \
+    {                                                                                                              \
+        const i64 threads = lines_total * 32;                                                                      \
+        sl::k_prep_sl<K><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(solve, lines_total);                  \
+        return ntd::check_launch("ntd_solve_bands prep");                                                          \
+    }                                                                                                              \
+    template <>                                                                                                    \
     int launch_apply_sl_k<K>(const double *solve, const double *bsl, double *xsl, double *xssl, int nx, int ny,    \
                              int nz, i64 batch, const int32_t *active, cudaStream_t st, int depth)                 \
     {                                                                                                              \
-        size_t smem = (size_t)4 * depth * sl::RSEG * sl::lr_of(K) * 8;                                             \
+        size_t smem = (size_t)4 * depth * sl::stage_of(K) * 8;                                                     \
         cudaError_t e = depth == 4                                                                                 \
             ? cudaFuncSetAttribute(sl::k_apply<K, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)      \
             : cudaFuncSetAttribute(sl::k_apply<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \

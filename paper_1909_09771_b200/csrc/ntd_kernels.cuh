@@ -399,6 +399,22 @@ __device__ __forceinline__ void mbar_wait(void *bar, unsigned parity)
             : "memory");
     }
 }
+// Producer-side wait: poll with back-off so a waiting producer warp does not
+// steal issue slots from the solver warp sharing its SM sub-partition.
+__device__ __forceinline__ void mbar_wait_lazy(void *bar, unsigned parity)
+{
+    unsigned ok = 0;
+    const unsigned a = smem_u32(bar);
+    while (true) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (ok) break;
+        __nanosleep(96);
+    }
+}
 __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned bytes, void *bar)
 {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(

@@ -3,7 +3,7 @@
 #include <cstdio>
 #include <vector>
 #include "ntd_kernels.cuh"
-#include "ntd_apply_v3.cuh"
+#include "ntd_apply_sl.cuh"
 
 int main(int argc, char **argv)
 {
@@ -20,23 +20,30 @@ int main(int argc, char **argv)
     cudaMalloc(&pre, 8 * 7 * n * B); cudaMalloc(&b, 8 * n * B); cudaMalloc(&x, 8 * n * B); cudaMalloc(&w, 8 * n * B);
     cudaMemcpy(pre, h.data(), 8 * 7 * n * B, cudaMemcpyHostToDevice);
     cudaMemset(b, 0, 8 * n * B);
-    double *sv; cudaMalloc(&sv, 8 * 2 * n * B); cudaMemset(sv, 0, 8 * 2 * n * B);
-    size_t smem = (size_t)4 * 4 * v3::A_N * (nx + 2 * v3::PAD) * 8;
-    cudaFuncSetAttribute(v3::k_apply<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    v3::k_apply<3, 4><<<B, 256, smem>>>(pre, sv, b, x, w, nx, ny, nz, nullptr);
+    const int K = 3, LR = sl::lr_of(K);
+    const long nsl = (long)ny * nz * LR;
+    double *sv, *bs, *xs, *xss;
+    const long nrec = (long)ny * nz * sl::recd_of(K); cudaMalloc(&sv, 8 * nrec * B); cudaMalloc(&bs, 8 * nsl * B); cudaMalloc(&xs, 8 * nsl * B); cudaMalloc(&xss, 8 * nsl * B);
+    std::vector<double> hs(nrec * B);
+    for (long i = 0; i < nrec * B; i++) { long a = (i % sl::recd_of(K)) / LR; hs[i] = a == 0 ? 0.3 : (a < 3 ? -0.05 : (a < 7 ? -0.1 : 0.01)); }
+    cudaMemcpy(sv, hs.data(), 8 * nrec * B, cudaMemcpyHostToDevice);
+    cudaMemset(bs, 0, 8 * nsl * B); cudaMemset(xs, 0, 8 * nsl * B); cudaMemset(xss, 0, 8 * nsl * B);
+    size_t smem = (size_t)4 * 4 * sl::stage_of(K) * 8;
+    cudaFuncSetAttribute(sl::k_apply<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sl::k_apply<3, 4><<<B, 256, smem>>>(sv, bs, xs, xss, nx, ny, nz, nullptr);
     cudaDeviceSynchronize();
     unsigned long long zero[64] = {0};
     cudaMemcpyToSymbol(g_ntd_timing, zero, sizeof(zero));
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    v3::k_apply<3, 4><<<B, 256, smem>>>(pre, sv, b, x, w, nx, ny, nz, nullptr);
+    sl::k_apply<3, 4><<<B, 256, smem>>>(sv, bs, xs, xss, nx, ny, nz, nullptr);
     cudaEventRecord(e1);
     cudaDeviceSynchronize();
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     unsigned long long t[8][8];
     cudaMemcpyFromSymbol(t, g_ntd_timing, sizeof(t));
     printf("apply %.3f ms  err=%s\n", ms, cudaGetErrorString(cudaGetLastError()));
-    const char *names[] = {"ldg+wait", "lds+rhs", "-", "solve", "store", "-", "-", ""};
+    const char *names[] = {"mbar", "lds+rhs", "solve", "store", "-", "-", "-", ""};
     double steps = 9409.0 / 1.0;
     for (int w = 0; w < 4; w++) {
         printf("warp %d:", w);
