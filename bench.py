@@ -273,7 +273,8 @@ def run_ntd(args):
     e4 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     e4[0].record()
     for _ in range(R):
-        D.ilu0_apply(solver.precond.ilu, solver.precond.split, v, nx, ny, nz, B, z=xa)
+        D.ilu0_apply(solver.precond.ilu, solver.precond.split, v, nx, ny, nz, B, z=xa, skew=solver.precond.skew,
+                     work=solver.precond.skew_work)
     e4[1].record()
     e5 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     e5[0].record()

@@ -151,6 +151,23 @@ int ntd_ilu0_apply(const double *f, int64_t split, const double *r, double *z,
                    double *acc, int64_t nx, int64_t ny, int64_t nz,
                    int64_t batch, const int32_t *active, void *stream);
 
+/* Skewed-layout ILU0 solves (same arithmetic, bitwise equal; coalesced
+ * per-step rows).  Available when split is a multiple of nx*ny:
+ * ntd_ilu0_skew_doubles returns 0 otherwise.  coef is built once from the
+ * factor f by ntd_ilu0_skew_build; work >= ntd_ilu0_skew_work_doubles.
+ * z and/or acc receive the result (acc += z). */
+int64_t ntd_ilu0_skew_doubles(int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+                              int64_t split);
+int ntd_ilu0_skew_build(const double *f, double *coef, int64_t split,
+                        int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+                        void *stream);
+int64_t ntd_ilu0_skew_work_doubles(int64_t nx, int64_t ny, int64_t nz,
+                                   int64_t batch);
+int ntd_ilu0_skew_apply(const double *coef, int64_t split, const double *r,
+                        double *z, double *acc, double *work, int64_t nx,
+                        int64_t ny, int64_t nz, int64_t batch,
+                        const int32_t *active, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -43,6 +43,10 @@ _SIGS = {
     "ntd_apply": (_INT, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_ilu0_factor": (_INT, [_P, _P, _I, _P, _I, _I, _I, _I, _P]),
     "ntd_ilu0_apply": (_INT, [_P, _I, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
+    "ntd_ilu0_skew_doubles": (_I, [_I, _I, _I, _I, _I]),
+    "ntd_ilu0_skew_build": (_INT, [_P, _P, _I, _I, _I, _I, _I, _P]),
+    "ntd_ilu0_skew_work_doubles": (_I, [_I, _I, _I, _I]),
+    "ntd_ilu0_skew_apply": (_INT, [_P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -52,7 +56,8 @@ EXPORTED = tuple(_SIGS)
 KERNELS_PER_CALL = {
     "ntd_spmv": 1, "ntd_residual": 1, "ntd_dot": 2, "ntd_pcg_init": 3, "ntd_pcg_start": 3,
     "ntd_pcg_spmv_alpha": 2, "ntd_pcg_update_residual": 3, "ntd_pcg_direction": 3, "ntd_factor": 1,
-    "ntd_apply": 3, "ntd_solve_bands": 1, "ntd_ilu0_factor": 2, "ntd_ilu0_apply": 1,
+    "ntd_apply": 3, "ntd_solve_bands": 1, "ntd_ilu0_factor": 2, "ntd_ilu0_apply": 1, "ntd_ilu0_skew_build": 1,
+    "ntd_ilu0_skew_apply": 3,
 }
 _launches = [0]
 

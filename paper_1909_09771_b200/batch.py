@@ -50,7 +50,7 @@ class _IluPrecond:
 
     def device_apply(self, r_dev, z_dev, active=None):
         return D.ilu0_apply(self.f.device_data, self.f.split, r_dev, self.a.nx, self.a.ny, self.a.nz, 1,
-                            z=z_dev, active=active)
+                            z=z_dev, active=active, skew=self.f.skew())
 
     def __call__(self, r):
         from .ilu0 import ilu0_apply

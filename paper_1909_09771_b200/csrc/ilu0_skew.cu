@@ -1,0 +1,304 @@
+// ilu0_skew.cu -- block ILU0 triangular solves in the skewed unit layout.
+//
+// Same arithmetic, in the same order, as ilu0.cu / the reference
+// (_ilu0_apply_half, /root/reference/pkg/src/ntdprecon/ilu0.py:95-114), so the
+// result is bitwise identical.  What changes is the data layout: a "unit" is
+// 32 consecutive grid lines of one plane, processed by one warp as a skewed
+// wavefront (lane L handles cell i = tau - L of line 32g + L at step tau), and
+// every array the sweep touches is stored per unit as
+//     [tau = 0 .. nx+30][lane 0..31]
+// so each step reads / writes one contiguous 256-byte row (coalesced; the
+// reference-layout version touches 32 different lines per instruction).  The
+// index guards of the reference (i-1 >= lo, ...) are folded into the stored
+// coefficients (0 where the reference skips the term), so the step is
+// branch-free: acc - 0*z == acc for the finite z the sweep produces.
+//
+// Applies when the half split is a plane boundary (split % (nx*ny) == 0, true
+// for every BASELINE config); ntd_ilu0_apply falls back to ilu0.cu otherwise.
+#include "common.cuh"
+
+namespace skew {
+
+constexpr int WARPS = 16;
+constexpr int PF = 4;  // steps of operand look-ahead (registers)
+
+struct Geom {
+    int nx, ny, nz, G, T;  // groups per plane, steps per unit (nx + 31)
+    i64 nxy, n;
+    i64 units;             // nz * G
+    __device__ __host__ Geom(int nx_, int ny_, int nz_)
+    {
+        nx = nx_;
+        ny = ny_;
+        nz = nz_;
+        G = (ny + 31) / 32;
+        T = nx + 31;
+        nxy = (i64)nx * ny;
+        n = nxy * nz;
+        units = (i64)nz * G;
+    }
+    __device__ __host__ i64 skew_size() const { return units * T * 32; }  // per system, per array
+};
+
+// unit-local (tau, lane) -> natural row, or -1 when the slot holds no cell
+__device__ __forceinline__ i64 slot_row(const Geom &g, i64 u, int tau, int lane)
+{
+    const i64 k = u / g.G;
+    const int grp = (int)(u - k * g.G);
+    const int i = tau - lane, j = grp * 32 + lane;
+    if (i < 0 || i >= g.nx || j >= g.ny) return -1;
+    return i + (i64)g.nx * j + g.nxy * k;
+}
+
+// factor -> skewed coefficient records (setup).  Per system:
+//   fw[u][tau][3][32] = c2, c1, c0  (forward, guards folded in)
+//   bw[u][tau][4][32] = c4, c5, c6, f3  (backward; f3 = 1 on empty slots)
+__global__ void k_build(const double *__restrict__ f, double *__restrict__ fw, double *__restrict__ bw, i64 split,
+                        int nx, int ny, int nz, i64 batch)
+{
+    const Geom g(nx, ny, nz);
+    const i64 per = g.units * g.T * 32;
+    for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < per * batch; e += (i64)gridDim.x * blockDim.x) {
+        const i64 s = e / per, el = e - s * per;
+        const i64 u = el / (g.T * 32);
+        const int rem = (int)(el - u * g.T * 32), tau = rem >> 5, lane = rem & 31;
+        const i64 row = slot_row(g, u, tau, lane);
+        double c2 = 0.0, c1 = 0.0, c0 = 0.0, c4 = 0.0, c5 = 0.0, c6 = 0.0, f3 = 1.0;
+        if (row >= 0) {
+            const double *fs = f + s * 7 * g.n;
+            const i64 lo = row < split ? 0 : split, hi = row < split ? split : g.n;
+            const int i = tau - lane, j = (int)((u % g.G) * 32 + lane);
+            if (i >= 1 && row - 1 >= lo) c2 = fs[2 * g.n + row];
+            if (j >= 1 && row - nx >= lo) c1 = fs[1 * g.n + row];
+            if (row - g.nxy >= lo) c0 = fs[row];
+            if (i + 1 < nx && row + 1 < hi) c4 = fs[4 * g.n + row];
+            if (j + 1 < ny && row + nx < hi) c5 = fs[5 * g.n + row];
+            if (row + g.nxy < hi) c6 = fs[6 * g.n + row];
+            f3 = fs[3 * g.n + row];
+        }
+        double *w = fw + s * per * 3 + (u * g.T + tau) * 96;
+        w[lane] = c2;
+        w[32 + lane] = c1;
+        w[64 + lane] = c0;
+        double *b = bw + s * per * 4 + (u * g.T + tau) * 128;
+        b[lane] = c4;
+        b[32 + lane] = c5;
+        b[64 + lane] = c6;
+        b[96 + lane] = f3;
+    }
+}
+
+// natural (B,N) -> skewed (B, units*T*32)
+__global__ void k_to_skew(const double *__restrict__ r, double *__restrict__ rs, int nx, int ny, int nz, i64 batch)
+{
+    const Geom g(nx, ny, nz);
+    const i64 per = g.skew_size();
+    for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < per * batch; e += (i64)gridDim.x * blockDim.x) {
+        const i64 s = e / per, el = e - s * per;
+        const i64 u = el / (g.T * 32);
+        const int rem = (int)(el - u * g.T * 32);
+        const i64 row = slot_row(g, u, rem >> 5, rem & 31);
+        rs[e] = row >= 0 ? r[s * g.n + row] : 0.0;
+    }
+}
+
+// skewed -> natural z (and acc += z, precond_pcg.py:64)
+__global__ void k_from_skew(const double *__restrict__ zs, double *__restrict__ z, double *__restrict__ acc, int nx,
+                            int ny, int nz, i64 batch, const int32_t *__restrict__ active)
+{
+    const Geom g(nx, ny, nz);
+    const i64 per = g.skew_size();
+    for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < g.n * batch; e += (i64)gridDim.x * blockDim.x) {
+        const i64 s = e / g.n, row = e - s * g.n;
+        if (active && !active[s]) continue;
+        const i64 k = row / g.nxy;
+        const i64 rr = row - k * g.nxy;
+        const int j = (int)(rr / nx), i = (int)(rr - (i64)j * nx);
+        const i64 u = k * g.G + j / 32;
+        const int lane = j & 31, tau = i + lane;
+        const double v = zs[s * per + (u * g.T + tau) * 32 + lane];
+        if (z) z[e] = v;
+        if (acc) acc[e] = add_rn(acc[e], v);
+    }
+}
+
+// progress word: unit * (T+1) + steps completed
+__device__ __forceinline__ void wait_unit(volatile unsigned long long *prog, int W, i64 unit, int steps, int T,
+                                          unsigned long long &cw, i64 &cu)
+{
+    if (unit < 0) return;
+    const unsigned long long need = (unsigned long long)unit * (T + 1) + (unsigned long long)(steps < T ? steps : T);
+    if (cu == unit && cw >= need) return;
+    unsigned long long w = 0;
+    if ((threadIdx.x & 31) == 0) {
+        do {
+            w = prog[unit % W];
+        } while (w < need);
+        __threadfence_block();
+    }
+    w = __shfl_sync(FULL_MASK, w, 0);
+    cw = w;
+    cu = unit;
+}
+
+__device__ __forceinline__ void publish(volatile unsigned long long *prog, int warp, unsigned long long word)
+{
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+        __threadfence_block();
+        prog[warp] = word;
+    }
+}
+
+// One half-system sweep.  FWD: units ascending, tau ascending; BWD: mirror.
+// in: rhs (FWD) or forward result (BWD), skewed; out: z skewed.
+template <bool FWD>
+__device__ void sweep(const Geom &g, i64 u_lo, i64 u_hi, const double *__restrict__ coef, const double *in,
+                      double *z, volatile unsigned long long *prog)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const int T = g.T, G = g.G;
+    const int NC = FWD ? 3 : 4;
+    const i64 nunits = u_hi - u_lo;
+    unsigned long long cw1 = 0, cw2 = 0;
+    i64 cu1 = -1, cu2 = -1;
+    for (i64 v = warp; v < nunits; v += W) {  // v: position in sweep order
+        const i64 u = FWD ? u_lo + v : u_hi - 1 - v;
+        const bool has_y = FWD ? (u % G) > 0 : (u % G) < G - 1;            // neighbour unit in the same plane
+        const bool has_z = FWD ? (u - G) >= u_lo : (u + G) < u_hi;         // previous plane inside the half
+        const i64 uy = FWD ? u - 1 : u + 1, uz = FWD ? u - G : u + G;
+        const i64 vy = v - 1, vz = v - G;                                   // their sweep positions
+        const double *cu_ = coef + u * (i64)T * 32 * NC;
+        const double *inu = in + u * (i64)T * 32;
+        double *zu = z + u * (i64)T * 32;
+        const double *zyu = z + uy * (i64)T * 32;
+        const double *zzu = z + uz * (i64)T * 32;
+        // register ring of look-ahead operands for steps tau .. tau+PF-1
+        double rc[PF][4], rin[PF], rzz[PF], rzy[PF];
+        auto step_tau = [&](int q) { return FWD ? q : T - 1 - q; };  // q: step index in sweep order
+        auto load = [&](int slot, int q) {
+            const int tau = step_tau(q);
+#pragma unroll
+            for (int c = 0; c < 4; c++) rc[slot][c] = c < NC ? cu_[(i64)tau * 32 * NC + c * 32 + lane] : 1.0;
+            rin[slot] = __ldcg(inu + (i64)tau * 32 + lane);
+            rzz[slot] = has_z ? __ldcg(zzu + (i64)tau * 32 + lane) : 0.0;
+            // lane 0 (FWD) / lane 31 (BWD) reads the neighbour unit's edge lane
+            const int ty = FWD ? tau + 31 : tau - 31;
+            const bool edge = FWD ? lane == 0 : lane == 31;
+            rzy[slot] = (has_y && edge && ty >= 0 && ty < T) ? __ldcg(zyu + (i64)ty * 32 + (FWD ? 31 : 0)) : 0.0;
+        };
+        // dependencies for the first PF steps
+        if (has_y) wait_unit(prog, W, vy, PF + 32, T, cw1, cu1);
+        if (has_z) wait_unit(prog, W, vz, PF, T, cw2, cu2);
+#pragma unroll
+        for (int q = 0; q < PF; q++) load(q, q);
+        double zprev = 0.0;
+        for (int q0 = 0; q0 < T; q0 += PF) {
+            // operands of steps q0+PF .. q0+2PF-1 become loadable once the
+            // neighbours are that far ahead
+            if (q0 + PF < T) {
+                if (has_y) wait_unit(prog, W, vy, q0 + 2 * PF + 32, T, cw1, cu1);
+                if (has_z) wait_unit(prog, W, vz, q0 + 2 * PF, T, cw2, cu2);
+            }
+#pragma unroll
+            for (int d = 0; d < PF; d++) {
+                const int q = q0 + d;
+                if (q >= T) break;
+                const double zn = FWD ? __shfl_up_sync(FULL_MASK, zprev, 1) : __shfl_down_sync(FULL_MASK, zprev, 1);
+                const double zy = (FWD ? lane == 0 : lane == 31) ? rzy[d] : zn;
+                double acc = rin[d];
+                acc = sub_rn(acc, mul_rn(rc[d][0], zprev));
+                acc = sub_rn(acc, mul_rn(rc[d][1], zy));
+                acc = sub_rn(acc, mul_rn(rc[d][2], rzz[d]));
+                const double zv = FWD ? acc : acc / rc[d][3];
+                zu[(i64)step_tau(q) * 32 + lane] = zv;
+                zprev = zv;
+                if (q + PF < T) load(d, q + PF);
+            }
+            if (((q0 / PF) & 1) == 1 || q0 + PF >= T)
+                publish(prog, warp, (unsigned long long)v * (T + 1) + (q0 + PF < T ? q0 + PF : T));
+        }
+        publish(prog, warp, (unsigned long long)v * (T + 1) + T);
+    }
+}
+
+__global__ void __launch_bounds__(WARPS * 32) k_apply(const double *__restrict__ fw, const double *__restrict__ bw,
+                                                      const double *__restrict__ rs, double *zf, double *zb,
+                                                      i64 split, int nx, int ny, int nz,
+                                                      const int32_t *__restrict__ active)
+{
+    __shared__ unsigned long long prog[WARPS];
+    const Geom g(nx, ny, nz);
+    const i64 sys = blockIdx.x >> 1;
+    const int half = blockIdx.x & 1;
+    if (active && !active[sys]) return;
+    const i64 ksplit = split / g.nxy;
+    const i64 u_lo = half ? ksplit * g.G : 0, u_hi = half ? g.units : ksplit * g.G;
+    if (u_lo >= u_hi) return;
+    const i64 per = g.skew_size();
+    const double *fws = fw + sys * per * 3, *bws = bw + sys * per * 4;
+    const double *rss = rs + sys * per;
+    double *zfs = zf + sys * per, *zbs = zb + sys * per;
+    if (threadIdx.x < WARPS) prog[threadIdx.x] = 0ull;
+    __syncthreads();
+    sweep<true>(g, u_lo, u_hi, fws, rss, zfs, prog);
+    __syncthreads();
+    if (threadIdx.x < WARPS) prog[threadIdx.x] = 0ull;
+    __syncthreads();
+    sweep<false>(g, u_lo, u_hi, bws, zfs, zbs, prog);
+}
+
+}  // namespace skew
+
+static unsigned grid_n(i64 total)
+{
+    i64 b = (total + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    return (unsigned)(b > 0 ? b : 1);
+}
+
+extern "C" int64_t ntd_ilu0_skew_doubles(int64_t nx, int64_t ny, int64_t nz, int64_t batch, int64_t split)
+{
+    const skew::Geom g((int)nx, (int)ny, (int)nz);
+    if (split % g.nxy != 0) return 0;  // plane-boundary split only
+    return g.skew_size() * batch * 7;  // coefficient records (3 + 4 per slot)
+}
+
+extern "C" int ntd_ilu0_skew_build(const double *f, double *coef, int64_t split, int64_t nx, int64_t ny, int64_t nz,
+                                   int64_t batch, void *stream)
+{
+    if (!f || !coef || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
+    const skew::Geom g((int)nx, (int)ny, (int)nz);
+    if (split % g.nxy != 0) return NTD_ENOTSUP;
+    const i64 per = g.skew_size();
+    skew::k_build<<<grid_n(per * batch), 256, 0, (cudaStream_t)stream>>>(f, coef, coef + per * batch * 3, split,
+                                                                         (int)nx, (int)ny, (int)nz, batch);
+    NTD_CHECK_LAUNCH("ntd_ilu0_skew_build");
+}
+
+extern "C" int64_t ntd_ilu0_skew_work_doubles(int64_t nx, int64_t ny, int64_t nz, int64_t batch)
+{
+    const skew::Geom g((int)nx, (int)ny, (int)nz);
+    return g.skew_size() * batch * 3;  // rhs, forward, backward (skewed)
+}
+
+extern "C" int ntd_ilu0_skew_apply(const double *coef, int64_t split, const double *r, double *z, double *acc,
+                                   double *work, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+                                   const int32_t *active, void *stream)
+{
+    if (!coef || !r || !work || (!z && !acc) || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
+    const skew::Geom g((int)nx, (int)ny, (int)nz);
+    if (split % g.nxy != 0) return NTD_ENOTSUP;
+    cudaStream_t st = (cudaStream_t)stream;
+    const i64 per = g.skew_size();
+    double *rs = work, *zf = work + per * batch, *zb = work + 2 * per * batch;
+    skew::k_to_skew<<<grid_n(per * batch), 256, 0, st>>>(r, rs, (int)nx, (int)ny, (int)nz, batch);
+    int rc = ntd::check_launch("ilu0 to_skew");
+    if (rc) return rc;
+    skew::k_apply<<<(unsigned)(2 * batch), skew::WARPS * 32, 0, st>>>(coef, coef + per * batch * 3, rs, zf, zb,
+                                                                      split, (int)nx, (int)ny, (int)nz, active);
+    rc = ntd::check_launch("ilu0 skew apply");
+    if (rc) return rc;
+    skew::k_from_skew<<<grid_n(g.n * batch), 256, 0, st>>>(zb, z, acc, (int)nx, (int)ny, (int)nz, batch, active);
+    NTD_CHECK_LAUNCH("ilu0 from_skew");
+}

@@ -83,7 +83,29 @@ def ilu0_factor(a_dev, nx, ny, nz, batch, split):
     return f, status.cpu()
 
 
-def ilu0_apply(f_dev, split, r_dev, nx, ny, nz, batch, z=None, acc=None, active=None):
+def ilu0_skew_build(f_dev, split, nx, ny, nz, batch):
+    """Skewed-layout coefficient records of an ILU0 factor, or None when the
+    split is not a plane boundary (then the reference-layout kernel is used)."""
+    size = _lib.load().ntd_ilu0_skew_doubles(nx, ny, nz, batch, split)
+    if size == 0:
+        return None
+    coef = torch.empty(size, dtype=torch.float64, device=_dev())
+    _lib.call("ntd_ilu0_skew_build", _lib.ptr(f_dev), _lib.ptr(coef), split, nx, ny, nz, batch, _lib.stream())
+    return coef
+
+
+def ilu0_apply(f_dev, split, r_dev, nx, ny, nz, batch, z=None, acc=None, active=None, skew=None, work=None):
+    """z = (LU)^-1 r (and/or acc += z).  skew: coefficient records from
+    ilu0_skew_build (fast path); work: scratch for it."""
+    if z is None and acc is None:
+        z = torch.empty_like(r_dev)
+    if skew is not None:
+        need = _lib.load().ntd_ilu0_skew_work_doubles(nx, ny, nz, batch)
+        if work is None or work.numel() < need:
+            work = torch.empty(need, dtype=torch.float64, device=_dev())
+        _lib.call("ntd_ilu0_skew_apply", _lib.ptr(skew), split, _lib.ptr(r_dev), _lib.ptr(z), _lib.ptr(acc),
+                  _lib.ptr(work), nx, ny, nz, batch, _lib.ptr(active), _lib.stream())
+        return z
     if z is None:
         z = torch.empty_like(r_dev)
     _lib.call("ntd_ilu0_apply", _lib.ptr(f_dev), split, _lib.ptr(r_dev), _lib.ptr(z), _lib.ptr(acc), nx, ny,
@@ -104,7 +126,7 @@ class CombinedDevice:
     """Symmetric ILU0 -> NTD -> ILU0 preconditioner on B systems
     (precond_pcg.py:28-65), all buffers preallocated on the device."""
 
-    def __init__(self, a_dev, nx, ny, nz, batch, pre=None, ilu=None, split=None, solve=None):
+    def __init__(self, a_dev, nx, ny, nz, batch, pre=None, ilu=None, split=None, solve=None, skew=None):
         self.a, self.nx, self.ny, self.nz, self.batch = a_dev, nx, ny, nz, batch
         n = nx * ny * nz
         self.n = n
@@ -112,6 +134,8 @@ class CombinedDevice:
         self.solve = solve if solve is not None else solve_bands(pre, nx, ny, nz, batch)
         self.ilu = ilu
         self.split = n // 2 if split is None else split
+        self.skew = skew if skew is not None else ilu0_skew_build(ilu, self.split, nx, ny, nz, batch)
+        self.skew_work = None
         shape = (batch, n)
         self.w = torch.empty(shape, dtype=torch.float64, device=_dev())
         self.t = torch.empty(shape, dtype=torch.float64, device=_dev())
@@ -123,11 +147,18 @@ class CombinedDevice:
         """z = M^{-1} r:  w = ilu(r); t = r - A w; z = ntd(t) + w;
         t = r - A z; z += ilu(t)   (precond_pcg.py:57-65)."""
         g = (self.nx, self.ny, self.nz, self.batch)
-        ilu0_apply(self.ilu, self.split, r, *g, z=self.w, active=active)
+        if self.skew is not None and self.skew_work is None:
+            self.skew_work = torch.empty(_lib.load().ntd_ilu0_skew_work_doubles(*g), dtype=torch.float64,
+                                         device=_dev())
+        ilu0_apply(self.ilu, self.split, r, *g, z=self.w, active=active, skew=self.skew, work=self.skew_work)
         residual(self.a, r, self.w, *g, t=self.t, active=active)
         ntd_apply(self.pre, self.t, *g, x=self.xn, work=self.work, active=active, solve=self.solve)
         residual(self.a, r, self.w, *g, t=self.t, v=self.xn, z_out=z, active=active)
-        ilu0_apply(self.ilu, self.split, self.t, *g, z=self.xn, acc=z, active=active)
+        if self.skew is not None:
+            ilu0_apply(self.ilu, self.split, self.t, *g, z=None, acc=z, active=active, skew=self.skew,
+                       work=self.skew_work)
+        else:
+            ilu0_apply(self.ilu, self.split, self.t, *g, z=self.xn, acc=z, active=active)
         return z
 
 

@@ -20,6 +20,12 @@ class ILU0Factors:
         self.nx, self.ny, self.nz, self.split = int(nx), int(ny), int(nz), int(split)
         self.device_data = as_device(data)
         self._host = None
+        self._skew = False  # lazily built skewed coefficient records (fast apply path)
+
+    def skew(self):
+        if self._skew is False:
+            self._skew = D.ilu0_skew_build(self.device_data, self.split, self.nx, self.ny, self.nz, 1)
+        return self._skew
 
     @property
     def n_rows(self):
@@ -57,7 +63,8 @@ def ilu0_apply(factors, r, workers=1):
     if shape_of(r) != (n,):
         raise ValueError(f"operand length {shape_of(r)} does not match {n} rows")
     rd = as_device(r)
-    z = D.ilu0_apply(factors.device_data, factors.split, rd, factors.nx, factors.ny, factors.nz, 1)
+    z = D.ilu0_apply(factors.device_data, factors.split, rd, factors.nx, factors.ny, factors.nz, 1,
+                     skew=factors.skew())
     return like_input(z, r)
 
 

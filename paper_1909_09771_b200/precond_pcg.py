@@ -56,7 +56,7 @@ class CombinedPrecond:
         self._ad = a.device_data()
         self._dev = D.CombinedDevice(self._ad, a.nx, a.ny, a.nz, 1, pre=self.ntd.bands,
                                      ilu=self.ilu.device_data, split=self.ilu.split,
-                                     solve=self.ntd.solve)
+                                     solve=self.ntd.solve, skew=self.ilu.skew())
         torch.cuda.current_stream().synchronize()
         self.setup_seconds = perf_counter() - t0
 
