@@ -63,7 +63,8 @@ def dist_env():
 
 
 def shard(total, world, rank):
-    return list(range(total * rank // world, total * (rank + 1) // world))
+    from paper_1909_09771_b200.dist import shard as _shard
+    return _shard(total, world, rank)
 
 
 def system_inputs(cfg, s):
@@ -285,23 +286,13 @@ def run_ntd(args):
     t_ilu = e4[0].elapsed_time(e4[1]) / 1e3 / R
     t_spmv = e5[0].elapsed_time(e5[1]) / 1e3 / R
 
-    # ---- reductions over ranks
-    stats = torch.tensor([[s, it, int(cv), rr] for s, it, cv, rr in
-                          zip(mine, res.iterations, res.converged, res.final_relres)],
-                         dtype=torch.float64, device="cuda")
-    times = torch.tensor([t_dev, t_e2e, t_apply, t_ilu, t_spmv, setup_s], dtype=torch.float64, device="cuda")
-    work = torch.tensor([work_local, work_e2e, launches], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(times, op=dist.ReduceOp.MAX)
-        dist.all_reduce(work, op=dist.ReduceOp.SUM)
-        sizes = [len(shard(n_total, world, r)) for r in range(world)]
-        pad = torch.zeros((max(sizes), 4), dtype=torch.float64, device="cuda")
-        pad[:B] = stats
-        gathered = [torch.zeros_like(pad) for _ in range(world)]
-        dist.all_gather(gathered, pad)
-        stats = torch.cat([g[:sz] for g, sz in zip(gathered, sizes)])
-    times = times.cpu().tolist()
-    work = work.cpu().tolist()
+    # ---- reductions over ranks (NCCL: max of timings, sum of work, one all_gather of stats)
+    from paper_1909_09771_b200 import dist as pdist
+    dev = torch.device("cuda", local)
+    times = pdist.reduce_max([t_dev, t_e2e, t_apply, t_ilu, t_spmv, setup_s], dev)
+    work = pdist.reduce_sum([work_local, work_e2e, launches], dev)
+    stats = pdist.gather_stats([[s, it, int(cv), rr] for s, it, cv, rr in
+                                zip(mine, res.iterations, res.converged, res.final_relres)], n_total, dev)
     stats = stats.cpu().numpy()
     if rank == 0:
         t_dev, t_e2e, t_apply, t_ilu, t_spmv, setup_s = times

@@ -1,0 +1,217 @@
+"""Drop-in API behaviour on the GPU, following the reference suite
+(/root/reference/pkg/tests/test_precond_pcg.py, test_ntd_factor.py,
+test_ntd_solve.py, test_ilu0.py): edge cases, error behaviour, properties
+(linearity, symmetry, rowsum filter), batch == single solves, determinism,
+and BASELINE config 3/4 against the CPU oracle and the reference's
+iteration counts."""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ntd():
+    import paper_1909_09771_b200 as m
+    return m
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    d = np.abs(b).max()
+    return float(np.abs(a - b).max() / (d if d else 1.0))
+
+
+# ---------------------------------------------------------------- pcg semantics
+def test_identity_converges_in_one_iteration(ntd, rng):
+    a = ntd.BandedMatrix(9, 1, 1)
+    a.data[3] = 1.0
+    b = rng.standard_normal(9)
+    x, st = ntd.pcg(a, b, tol=1e-12)
+    assert st.iterations == 1 and st.converged
+    assert np.abs(x - b).max() <= 1e-14
+
+
+def test_zero_rhs_short_circuits(ntd):
+    a = ntd.BandedMatrix(4, 1, 1)
+    a.data[3] = 1.0
+    x, st = ntd.pcg(a, np.zeros(4))
+    assert st.iterations == 0 and st.converged and np.array_equal(x, np.zeros(4))
+
+
+def test_indefinite_matrix_breaks_down(ntd):
+    a = ntd.BandedMatrix(3, 1, 1)
+    a.data[3] = [-1.0, -1.0, -1.0]
+    with pytest.raises(ntd.DivergenceError, match="breakdown"):
+        ntd.pcg(a, np.ones(3))
+
+
+def test_max_iters_reached_is_not_an_error(ntd):
+    a = ntd.assemble(ntd.GridSpec(8, 8, 8), 1)
+    x, st = ntd.pcg(a, ntd.make_rhs(a), tol=1e-14, max_iters=3)
+    assert not st.converged and st.iterations == 3 and len(st.relres_history) == 3
+
+
+def test_stats_bookkeeping_and_callback(ntd):
+    a = ntd.assemble(ntd.GridSpec(6, 6, 6), 3)
+    b = ntd.make_rhs(a)
+    seen = []
+    x, st = ntd.pcg(a, b, tol=1e-8, callback=lambda it, xx, rr: seen.append((it, rr)))
+    assert st.converged and len(st.relres_history) == st.iterations
+    assert st.final_relres == st.relres_history[-1]
+    assert [it for it, _ in seen] == list(range(1, st.iterations + 1))
+    recomputed = np.linalg.norm(b - ntd.spmv(a, x)) / np.linalg.norm(b)
+    assert abs(recomputed - st.final_relres) <= 1e-6
+
+
+def test_plain_cg_iterations_match_oracle(ntd):
+    a = ntd.assemble(ntd.GridSpec(20, 20, 20), 3)
+    b = ntd.make_rhs(a)
+    x, st = ntd.pcg(a, b, tol=1e-7, max_iters=500)
+    xo, it, conv, _ = oracle.pcg(a.data, b, 20, 20, 20, kind="none", tol=1e-7, max_iters=500)
+    assert st.converged and conv and abs(st.iterations - it) <= 1
+    assert rel(x, xo) <= 1e-8
+
+
+def test_generic_callable_preconditioner(ntd):
+    """pcg accepts any callable r -> z (precond_pcg.py:71-74)."""
+    a = ntd.assemble(ntd.GridSpec(10, 9, 8), 2)
+    b = ntd.make_rhs(a, "manufactured")
+    cp = ntd.CombinedPrecond(a)
+    x1, s1 = ntd.pcg(a, b, cp, tol=1e-9)
+    x2, s2 = ntd.pcg(a, b, lambda r: ntd.combined_apply(cp, r), tol=1e-9)
+    assert s1.iterations == s2.iterations
+    assert rel(x1, x2) <= 1e-12
+
+
+def test_energy_norm_decreases(ntd):
+    a = ntd.assemble(ntd.GridSpec(12, 12, 12), 1)
+    b = ntd.make_rhs(a, "manufactured")
+    ones = np.ones(a.n_rows)
+    en = []
+    ntd.pcg(a, b, ntd.CombinedPrecond(a), tol=1e-10, max_iters=100,
+            callback=lambda it, x, rr: en.append((x - ones) @ ntd.spmv(a, x - ones)))
+    en = np.array(en)
+    assert np.all(np.diff(en) <= 1e-12 * en[0])
+
+
+# ---------------------------------------------------------------- factor / apply
+def test_factor_errors_name_plane_and_row(ntd):
+    a = ntd.assemble(ntd.GridSpec(4, 4, 4), 3)
+    a.data[3, 21] = 0.0
+    a.data[2, 21] = a.data[4, 21] = a.data[1, 21] = a.data[5, 21] = 0.0
+    a.data[0, 21] = a.data[6, 21] = 0.0
+    with pytest.raises(ntd.FactorizationError, match="plane"):
+        ntd.factor_level3(a)
+    with pytest.raises(ntd.FactorizationError, match="row"):
+        ntd.build_block_ilu0(a)
+
+
+def test_rowsum_filter_property(ntd):
+    """B^{-1} A 1 = 1 to <= 1e-11 (tests/test_ntd_factor.py:196-203)."""
+    for field in (1, 2, 3):
+        a = ntd.assemble(ntd.GridSpec(9, 8, 7), field)
+        pre = ntd.factor_level3(a)
+        y = ntd.ntd_apply(pre, ntd.spmv(a, np.ones(a.n_rows)))
+        assert np.abs(y - 1.0).max() <= 1e-11
+
+
+def test_apply_linear_and_symmetric(ntd, rng):
+    a = ntd.assemble(ntd.GridSpec(8, 7, 6), 2)
+    pre = ntd.factor_level3(a)
+    n = a.n_rows
+    u, v = rng.standard_normal(n), rng.standard_normal(n)
+    lin = ntd.ntd_apply(pre, 2.0 * u - 3.0 * v) - (2.0 * ntd.ntd_apply(pre, u) - 3.0 * ntd.ntd_apply(pre, v))
+    assert np.abs(lin).max() <= 1e-12 * np.abs(ntd.ntd_apply(pre, u)).max() * 10
+    assert abs(u @ ntd.ntd_apply(pre, v) - v @ ntd.ntd_apply(pre, u)) <= 1e-11 * abs(u @ ntd.ntd_apply(pre, v)) + 1e-13
+
+
+def test_apply_does_not_clobber_input_and_is_deterministic(ntd, rng):
+    a = ntd.assemble(ntd.GridSpec(16, 12, 10), 1)
+    pre = ntd.factor_level3(a)
+    b = rng.standard_normal(a.n_rows)
+    keep = b.copy()
+    x1 = ntd.ntd_apply(pre, b)
+    x2 = ntd.ntd_apply(pre, b)
+    assert np.array_equal(b, keep) and np.array_equal(x1, x2)
+
+
+def test_direct_and_slot_layout_paths_agree(ntd, rng):
+    """The slot-layout TMA kernel and the direct-load kernel compute the same
+    operator (forced with NTD_APPLY_PATH=direct)."""
+    import torch
+    from paper_1909_09771_b200 import device as D
+    a = ntd.assemble(ntd.GridSpec(24, 20, 18), 2)
+    pre = ntd.factor_level3(a)
+    b = torch.from_numpy(rng.standard_normal(a.n_rows)).cuda()
+    x_sl = D.ntd_apply(pre.bands, b, 24, 20, 18, 1, solve=pre.solve)
+    os.environ["NTD_APPLY_PATH"] = "direct"
+    try:
+        x_d = D.ntd_apply(pre.bands, b, 24, 20, 18, 1)
+    finally:
+        del os.environ["NTD_APPLY_PATH"]
+    assert rel(x_sl.cpu().numpy(), x_d.cpu().numpy()) <= 1e-13
+
+
+def test_dump_load_roundtrip(ntd, tmp_path):
+    a = ntd.assemble(ntd.GridSpec(5, 4, 3), 2)
+    pre = ntd.factor_level3(a)
+    p = tmp_path / "pre.bin"
+    ntd.dump_precon_bands(pre, p)
+    back = ntd.load_precon_bands(p)
+    assert np.array_equal(back.host(), pre.host())
+    v = np.linspace(-1, 1, a.n_rows)
+    assert np.array_equal(ntd.ntd_apply(back, v), ntd.ntd_apply(pre, v))
+
+
+def test_level1_level2_known_answers(ntd):
+    line = ntd.LineBands(np.array([2.0, 2.0, 2.0]), np.array([0.0, -1.0, -1.0]), np.array([-1.0, -1.0, 0.0]))
+    mr = ntd.factor_level1(line)
+    np.testing.assert_allclose(1.0 / mr, [2.0, 1.0, 2.0], rtol=1e-15)
+    line2 = ntd.LineBands(np.array([2.0, 2.0]), np.array([0.0, -1.0]), np.array([-1.0, 0.0]))
+    np.testing.assert_allclose(1.0 / ntd.factor_level1(line2), [1.5, 2.0], rtol=1e-15)
+
+
+# ---------------------------------------------------------------- BASELINE configs
+def test_config3_against_oracle(ntd):
+    from paper_1909_09771_b200 import problems
+    data, xt, (nx, ny, nz) = problems.baseline_config(3)
+    a = ntd.BandedMatrix(nx, ny, nz, data)
+    b = ntd.spmv(a, xt)
+    pre = ntd.factor_level3(a)
+    pre_o = oracle.factor_level3(data, nx, ny, nz)
+    assert rel(pre.host(), pre_o) <= 1e-10
+    v = np.random.default_rng(3).uniform(-1, 1, a.n_rows)
+    assert rel(ntd.ntd_apply(pre, v), oracle.ntd_apply(pre_o, v, nx, ny, nz)) <= 1e-10
+    f, split = oracle.build_block_ilu0(data, nx, ny, nz)
+    g = ntd.build_block_ilu0(a)
+    assert np.array_equal(g.data, f)
+    assert np.array_equal(ntd.ilu0_apply(g, v), oracle.ilu0_apply(f, split, v, nx, ny, nz))
+    x, st = ntd.pcg(a, b, ntd.CombinedPrecond(a), tol=1e-8)
+    assert st.converged and st.iterations == 10 and st.final_relres < 1e-8  # reference: 10
+
+
+def test_batch_matches_single_and_reference_iterations(ntd):
+    """Config-4 systems 0 and 63 in one batch: identical to single-system
+    solves bit for bit, iteration counts of the reference (21, 22)."""
+    import torch
+    from paper_1909_09771_b200 import problems
+    from paper_1909_09771_b200.batch import BatchSolver
+    ins = [problems.baseline_config(4, s) for s in (0, 63)]
+    nx, ny, nz = ins[0][2]
+    A = torch.from_numpy(np.stack([d for d, _, _ in ins])).cuda()
+    xs = torch.from_numpy(np.stack([x for _, x, _ in ins])).cuda()
+    bsys = [ntd.spmv(ntd.BandedMatrix(nx, ny, nz, d), x) for d, x, _ in ins]
+    solver = BatchSolver(A, nx, ny, nz).setup()
+    res = solver.solve(torch.from_numpy(np.stack(bsys)).cuda(), 1e-8)
+    assert res.iterations == [21, 22] and all(res.converged) and max(res.final_relres) < 1e-8
+    for k, (d, _, _) in enumerate(ins):
+        a = ntd.BandedMatrix(nx, ny, nz, d)
+        x, st = ntd.pcg(a, bsys[k], ntd.CombinedPrecond(a), tol=1e-8)
+        assert st.iterations == res.iterations[k]
+        assert np.array_equal(x, res.x[k].cpu().numpy())
