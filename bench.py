@@ -318,7 +318,8 @@ def run_ntd(args):
                     "d2h_bytes_per_step": 8 * n * B * world},
             "roofline": {"kernel": "ntd_apply (batched, rank 0 shard)", "bound": "hbm",
                          "achieved": achieved, "peak": peak[0], "unit": "GB/s", "frac": achieved / peak[0],
-                         "peak_source": peak[1], "traffic": None,
+                         "peak_source": peak[1], "traffic": _traffic(cfg, B),
+                         "traffic_unit": "bytes per launch (ncu dram read+write)",
                          "bytes_per_unknown": NTD_APPLY_BYTES_PER_UNKNOWN, "apply_ms": 1e3 * t_apply,
                          "apply_munknowns_per_s": n * B / t_apply / 1e6},
             "kernels_ms": {"ntd_apply": 1e3 * t_apply, "ilu0_apply": 1e3 * t_ilu, "spmv": 1e3 * t_spmv},
@@ -335,6 +336,16 @@ def run_ntd(args):
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _traffic(cfg, systems):
+    """ncu-measured DRAM bytes per launch of the dominant kernel (profiles/)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "roofline_traffic.json")) as fh:
+            rec = json.load(fh).get(f"cfg{cfg}-{systems}")
+        return None if rec is None else float(rec["bytes_per_launch"])
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 def _measured_peak():
