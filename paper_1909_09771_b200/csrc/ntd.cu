@@ -63,7 +63,8 @@ extern "C" int64_t ntd_apply_work_doubles(int64_t nx, int64_t ny, int64_t nz, in
     const i64 n = nx * ny * nz * batch;
     const i64 s = sl_doubles(nx, ny, nz) * batch;
     const int K = pick_k(nx);
-    const i64 w = 3 * s + (K > 0 ? (i64)sl::recd_of(K) * ny * nz * batch : 0);  // b, x, xs in SL (+ solve records)
+    // b, x, xs in SL, a zero plane (+ solve records when the caller has none)
+    const i64 w = K > 0 ? 3 * s + ny * (i64)sl::lr_of(K) + (i64)sl::recd_of(K) * ny * nz * batch : 0;
     return w > n ? w : n;
 }
 
@@ -107,29 +108,30 @@ extern "C" int ntd_apply(const double *pre, const double *solve, const double *b
     cudaStream_t st = (cudaStream_t)stream;
     if (depth && aligned && !(force && force[0] == 'd')) {
         const i64 lines = ny * nz, s = sl_doubles(nx, ny, nz) * batch;
-        double *bsl = work, *xsl = work + s, *xssl = work + 2 * s;
+        double *bsl = work, *xsl = work + s, *xssl = work + 2 * s, *zpl = work + 3 * s;
+        const i64 zn = ny * (i64)sl::lr_of(K);
         if (!solve) {
-            double *sv = work + 3 * s;
+            double *sv = zpl + zn;
             int rc = ntd_solve_bands(pre, sv, nx, ny, nz, batch, stream);
             if (rc) return rc;
             solve = sv;
         }
-        // x/xs SL buffers: pad slots must read as zero (zero chain maps)
-        if (cudaMemsetAsync(xsl, 0, sizeof(double) * 2 * s, st) != cudaSuccess) return ntd::check_launch("memset");
-        sl::k_to_sl<<<grid_for(s), 256, 0, st>>>(b, bsl, (int)nx, lines, K, batch);
+        // the missing level-3 neighbour of the first/last plane reads zeros
+        if (cudaMemsetAsync(zpl, 0, sizeof(double) * zn, st) != cudaSuccess) return ntd::check_launch("memset");
+        sl::k_to_sl<<<grid_for(s), 256, 0, st>>>(b, pre, bsl, (int)nx, lines, K, batch);
         int rc = ntd::check_launch("ntd_apply to_sl");
         if (rc) return rc;
         switch (K) {
 #define SLCASE(KK)                                                                                                \
     case KK:                                                                                                       \
-        rc = launch_apply_sl_k<KK>(solve, bsl, xsl, xssl, (int)nx, (int)ny, (int)nz, batch, active, st, depth);    \
+        rc = launch_apply_sl_k<KK>(solve, bsl, xsl, xssl, zpl, (int)nx, (int)ny, (int)nz, batch, active, st, depth);    \
         break;
             SLCASE(1) SLCASE(2) SLCASE(3) SLCASE(4) SLCASE(5) SLCASE(6) SLCASE(8) SLCASE(11)
 #undef SLCASE
         default: return NTD_ENOTSUP;
         }
         if (rc) return rc;
-        sl::k_from_sl<<<grid_for(nx * lines * batch), 256, 0, st>>>(xsl, x, (int)nx, lines, K, batch);
+        sl::k_from_sl<<<grid_for(nx * lines * batch), 256, 0, st>>>(xsl, x, (int)nx, lines, K, batch, active);
         return ntd::check_launch("ntd_apply from_sl");
     }
     NTD_DISPATCH(launch_apply_k, pre, b, x, work, (int)nx, (int)ny, (int)nz, batch, active, st);

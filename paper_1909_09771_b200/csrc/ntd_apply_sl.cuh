@@ -11,35 +11,47 @@
 // length, start padding: r < P holds 0).  Lane s of half h owns slots
 // k = 0..K-1 at region index s*K + k, so its K values are contiguous
 // (immediate-offset shared loads, fully coalesced global loads/stores) and
-// padded slots are zero maps that need no branches.  The factor (and its
-// chain coefficients NL = -(l1*m), NU = -(u1*m)) is converted to SL once at
-// setup (ntd_solve_bands); b is converted on entry and x back on exit.
+// padded slots are zero maps that need no branches.  The factor is converted
+// to solve records once at setup (ntd_solve_bands); b is converted (and
+// scaled by m) on entry and x converted back on exit.
 //
 // Per line step the solver waits on an mbarrier, reads its slots from a
 // D-deep ring of line records streamed by 1-D bulk TMA (issued by the
-// producer warp), forms the right-hand side, runs two 16-lane Kogge-Stone
-// affine scans (ntd_line: lower and upper chains of the twisted line
-// solve) and stores x.  x-dependent operands (neighbour plane, lower-sweep
-// values of this plane) are loaded by the solver one line ahead.
+// producer warp), forms the scan constants, runs the radix-4 16-lane scans
+// of the twisted line solve (ntd_line4.cuh) and stores x.  x-dependent
+// operands (neighbour plane, lower-sweep values of this plane) are loaded by
+// the solver one line ahead.
 #pragma once
 #include "ntd_kernels.cuh"
 #include "ntd_line4.cuh"
 
 namespace sl {
 
-#ifndef NTD_SL_PREFETCH_PLANES
-#define NTD_SL_PREFETCH_PLANES 0
-#endif
-constexpr bool PREFETCH_PLANES = NTD_SL_PREFETCH_PLANES;  // whole-next-plane L2 prefetch (off: the TMA ring runs far enough ahead)
-
-enum { SL_MR = 0, SL_NL, SL_NU, SL_L2, SL_U2, SL_L3, SL_U3, SL_N };  // solve arrays (SL)
-constexpr int NPREP = 15;  // LinePrep coefficients per lane, stored [coef][lane] after the arrays
-
+// Solve record of one line (record-major, [system][line][RECD]):
+//   [ NL | NU | PREP (NPREP x 32) | L2' | U2' | L3' | U3' ]
+// NL = -(l1 m), NU = -(u1 m) are the chain coefficients, PREP the line's
+// factor-only scan coefficients, and the couplings are pre-multiplied by the
+// level-1 pivot reciprocal m (c' = c m), as is b on entry (b' = b m), so the
+// solver forms the scan constants cr = b' - sum c' y directly and m itself is
+// never streamed.  A phase copies only the block [NL|NU|PREP] plus the
+// couplings it reads.
+constexpr int NPREP = 11;  // stored LinePrep coefficients per lane ([coef][lane]); p1, e0, q1, f0 are rebuilt
 __host__ __device__ constexpr int lr_of(int K) { return 32 * K + 2; }
-// doubles per line of the solve record: 7 SL arrays + the line's scan coefficients
-__host__ __device__ constexpr int recd_of(int K) { return SL_N * lr_of(K) + NPREP * 32; }
-// ring stage: one solve record + one extra line (b or xo)
-__host__ __device__ constexpr int stage_of(int K) { return recd_of(K) + lr_of(K); }
+__host__ __device__ constexpr int o_nl(int K) { return 0; }
+__host__ __device__ constexpr int o_nu(int K) { return lr_of(K); }
+__host__ __device__ constexpr int o_prep(int K) { return 2 * lr_of(K); }
+__host__ __device__ constexpr int blk_of(int K) { return 2 * lr_of(K) + NPREP * 32; }  // [NL|NU|PREP]
+__host__ __device__ constexpr int o_l2(int K) { return blk_of(K); }
+__host__ __device__ constexpr int o_u2(int K) { return blk_of(K) + lr_of(K); }
+__host__ __device__ constexpr int o_l3(int K) { return blk_of(K) + 2 * lr_of(K); }
+__host__ __device__ constexpr int o_u3(int K) { return blk_of(K) + 3 * lr_of(K); }
+__host__ __device__ constexpr int recd_of(int K) { return blk_of(K) + 4 * lr_of(K); }
+// ring stage: [block | S0: in-plane coupling | S1: C1 | S2: C2 | X: b' or xo]
+__host__ __device__ constexpr int rs0_of(int K) { return blk_of(K); }
+__host__ __device__ constexpr int rs1_of(int K) { return blk_of(K) + lr_of(K); }
+__host__ __device__ constexpr int rs2_of(int K) { return blk_of(K) + 2 * lr_of(K); }
+__host__ __device__ constexpr int rx_of(int K) { return blk_of(K) + 3 * lr_of(K); }
+__host__ __device__ constexpr int stage_of(int K) { return blk_of(K) + 4 * lr_of(K); }
 
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(void *bar)
@@ -56,78 +68,76 @@ __device__ __forceinline__ int sl_index(int c, int n, int K)
     return 16 * K + 1 + (n - 1 - c) + (16 * K - (n - 1 - t));  // desc: r = j + P1, j = n-1-c
 }
 
-// natural (B, N) <-> SL (B, N_SL).  One thread per SL element / cell.
-static __global__ void k_to_sl(const double *__restrict__ src, double *__restrict__ dst, int nx, i64 lines, int K,
-                        i64 batch)
+// cell of SL element r of a line (-1: padding)
+__device__ __forceinline__ int sl_cell(int r, int nx, int K)
 {
-    const int LR = lr_of(K);
-    const i64 total = lines * LR * batch;
     const int t = (nx - 1) / 2;
     const int P0 = 16 * K - t, P1 = 16 * K - (nx - 1 - t);
+    int c = -1;
+    if (r < 16 * K) {
+        const int j = r - P0;
+        if (j >= 0) c = j;
+    } else if (r == 16 * K) {
+        c = t;
+    } else if (r < 32 * K + 1) {
+        const int j = r - (16 * K + 1) - P1;
+        if (j >= 0) c = nx - 1 - j;
+    }
+    return c;
+}
+
+// b (B, N) -> b' = b m in SL (B, N_SL).  One thread per SL element.
+static __global__ void k_to_sl(const double *__restrict__ src, const double *__restrict__ pre,
+                               double *__restrict__ dst, int nx, i64 lines, int K, i64 batch)
+{
+    const int LR = lr_of(K);
+    const i64 total = lines * LR * batch, n = lines * nx;
     for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total; e += (i64)gridDim.x * blockDim.x) {
         const i64 line = e / LR;  // global line over batch
         const int r = (int)(e - line * LR);
-        int c = -1;
-        if (r < 16 * K) {
-            const int j = r - P0;
-            if (j >= 0) c = j;
-        } else if (r == 16 * K) {
-            c = t;
-        } else if (r < 32 * K + 1) {
-            const int j = r - (16 * K + 1) - P1;
-            if (j >= 0) c = nx - 1 - j;
-        }
-        dst[e] = c >= 0 ? src[line * nx + c] : 0.0;
+        const int c = sl_cell(r, nx, K);
+        const i64 s = line / lines, g = line * nx + c;
+        dst[e] = c >= 0 ? src[g] * pre[s * 6 * n + 6 * n + g] : 0.0;  // pre[s][6][cell]: m
     }
 }
 
+// x in SL -> natural; systems masked off by `active` get x = 0
 static __global__ void k_from_sl(const double *__restrict__ src, double *__restrict__ dst, int nx, i64 lines, int K,
-                          i64 batch)
+                                 i64 batch, const int32_t *__restrict__ active)
 {
     const int LR = lr_of(K);
     const i64 total = lines * nx * batch;
     for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total; e += (i64)gridDim.x * blockDim.x) {
         const i64 line = e / nx;
         const int c = (int)(e - line * nx);
-        dst[e] = src[line * LR + sl_index(c, nx, K)];
+        const bool on = !active || active[line / lines];
+        dst[e] = on ? src[line * LR + sl_index(c, nx, K)] : 0.0;
     }
 }
 
-// solve arrays in SL from a factor (B,7,N): mr, -(l1 mr), -(u1 mr), l2, u2, l3, u3
+// solve records from a factor (B,7,N): NL, NU, (PREP by k_prep_sl), m l2, m u2, m l3, m u3
 static __global__ void k_solve_sl(const double *__restrict__ pre, double *__restrict__ solve, int nx, i64 lines, int K,
-                           i64 batch)
+                                  i64 batch)
 {
-    const int LR = lr_of(K);
+    const int LR = lr_of(K), RECD = recd_of(K);
     const i64 nsl = lines * LR, n = lines * nx;
     const i64 total = nsl * batch;
-    const int t = (nx - 1) / 2;
-    const int P0 = 16 * K - t, P1 = 16 * K - (nx - 1 - t);
     for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total; e += (i64)gridDim.x * blockDim.x) {
         const i64 s = e / nsl, el = e - s * nsl;
         const i64 line = el / LR;
         const int r = (int)(el - line * LR);
-        int c = -1;
-        if (r < 16 * K) {
-            const int j = r - P0;
-            if (j >= 0) c = j;
-        } else if (r == 16 * K) {
-            c = t;
-        } else if (r < 32 * K + 1) {
-            const int j = r - (16 * K + 1) - P1;
-            if (j >= 0) c = nx - 1 - j;
-        }
+        const int c = sl_cell(r, nx, K);
         const double *p = pre + s * 7 * n;
-        // record-major: [system][line][array][LR] -> one bulk copy per line
-        double *o = solve + (s * lines + line) * (i64)(SL_N * LR + NPREP * 32) + r;
+        double *o = solve + (s * lines + line) * (i64)RECD + r;
         const i64 g = line * nx + c;
-        const double m = c >= 0 ? p[6 * n + g] : 0.0;
-        o[SL_MR * LR] = m;
-        o[SL_NL * LR] = c >= 0 ? -(p[g] * m) : 0.0;
-        o[SL_NU * LR] = c >= 0 ? -(p[n + g] * m) : 0.0;
-        o[SL_L2 * LR] = c >= 0 ? p[2 * n + g] : 0.0;
-        o[SL_U2 * LR] = c >= 0 ? p[3 * n + g] : 0.0;
-        o[SL_L3 * LR] = c >= 0 ? p[4 * n + g] : 0.0;
-        o[SL_U3 * LR] = c >= 0 ? p[5 * n + g] : 0.0;
+        const bool on = c >= 0;
+        const double m = on ? p[6 * n + g] : 0.0;
+        o[o_nl(K)] = on ? -(p[g] * m) : 0.0;
+        o[o_nu(K)] = on ? -(p[n + g] * m) : 0.0;
+        o[o_l2(K)] = on ? p[2 * n + g] * m : 0.0;
+        o[o_u2(K)] = on ? p[3 * n + g] * m : 0.0;
+        o[o_l3(K)] = on ? p[4 * n + g] * m : 0.0;
+        o[o_u3(K)] = on ? p[5 * n + g] * m : 0.0;
     }
 }
 
@@ -194,9 +204,9 @@ __device__ __forceinline__ void line_solve(int s, int n, int t, const double (&a
 // ---------------------------------------------------------------- data
 struct SlArrays {  // one system, SL
     const double *solve;  // record-major solve records [line][recd_of(K)]
-    const double *b;
+    const double *b;      // b' = b m
     double *x, *xs;
-    i64 nsl;
+    const double *zero;   // one plane of zero records: the missing level-3 neighbour
 };
 
 // per-lane slot access (lane base inside a record)
@@ -227,32 +237,26 @@ __device__ __forceinline__ void ld_rec(const double *rec, const LaneSl<K> &L, do
     for (int k = 0; k < K; k++) v[k] = rec[L.base + k];
 }
 template <int K>
-__device__ __forceinline__ void st_rec(double *rec, const LaneSl<K> &L, const double (&v)[K], double vt, int lane)
+__device__ __forceinline__ void st_rec(double *rec, const LaneSl<K> &L, const double (&v)[K], double vt)
 {
-    (void)lane;
 #pragma unroll
     for (int k = 0; k < K; k++) rec[L.base + k] = v[k];
     rec[L.tw] = vt;  // every lane holds the same twist value: branch-free
 }
 
-// ring of D stages x RSEG line records per solver warp
-constexpr int G_X = SL_N;      // ring segment holding b (lower lines of LOWER3) or xo (upper lines of UPPER3)
-constexpr int G_PREP = SL_N + 1;  // the record's scan coefficients
-
+// ring of D stages per solver warp
 template <int K, int D>
 struct Ring {
     double *base;
     unsigned long long *full, *empty;
-    __device__ __forceinline__ double *seg(int st, int g) const
-    {
-        double *b0 = base + (size_t)st * stage_of(K);
-        return g < SL_N ? b0 + g * lr_of(K) : (g == G_X ? b0 + recd_of(K) : b0 + SL_N * lr_of(K));
-    }
+    __device__ __forceinline__ double *stage(int st) const { return base + (size_t)st * stage_of(K); }
 };
 
 struct PlaneDesc {
     i64 prec;      // record index of the plane's first line (plane * ny)
     int mode;      // M_LOWER3 / M_UPPER3
+    int c1;        // record offset of the level-3 coupling C1 (two: L3 then U3 = C2)
+    bool two;      // both level-3 neighbours (twist plane)
     bool hasM, hasP, nbrUp;
     bool up;       // lower sweep: the level-3 neighbour is plane p+1 (descending half)
 };
@@ -263,24 +267,34 @@ struct Seq {
     __device__ __forceinline__ int qup(int i) const { return w2 == 0 ? t2 - 1 - i : t2 + 1 + i; }
 };
 
-__device__ __forceinline__ LinePrep read_prep(const double *pp, int lane)
+// stored scan coefficients + the four rebuilt ones (same expressions as line_prep)
+template <int K>
+__device__ __forceinline__ LinePrep read_prep(const double *pp, int lane, const double (&aL)[K],
+                                              const double (&aU)[K])
 {
+    const int s = lane & 15;
     LinePrep P;
-    P.p1 = pp[0 * 32 + lane];
-    P.p2 = pp[1 * 32 + lane];
-    P.p3 = pp[2 * 32 + lane];
-    P.e0 = pp[3 * 32 + lane];
-    P.e1 = pp[4 * 32 + lane];
-    P.e2 = pp[5 * 32 + lane];
-    P.e3 = pp[6 * 32 + lane];
-    P.q1 = pp[7 * 32 + lane];
-    P.q2 = pp[8 * 32 + lane];
-    P.q3 = pp[9 * 32 + lane];
-    P.f0 = pp[10 * 32 + lane];
-    P.f1 = pp[11 * 32 + lane];
-    P.f2 = pp[12 * 32 + lane];
-    P.f3 = pp[13 * 32 + lane];
-    P.bex = pp[14 * 32 + lane];
+    double A0 = 1.0, B0 = 1.0;
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        A0 *= aL[k];
+        B0 *= aU[k];
+    }
+    P.p1 = s >= 1 ? A0 : 0.0;
+    P.e0 = s >= 1 ? 1.0 : 0.0;
+    P.q1 = s <= 14 ? B0 : 0.0;
+    P.f0 = s <= 14 ? 1.0 : 0.0;
+    P.p2 = pp[0 * 32 + lane];
+    P.p3 = pp[1 * 32 + lane];
+    P.e1 = pp[2 * 32 + lane];
+    P.e2 = pp[3 * 32 + lane];
+    P.e3 = pp[4 * 32 + lane];
+    P.q2 = pp[5 * 32 + lane];
+    P.q3 = pp[6 * 32 + lane];
+    P.f1 = pp[7 * 32 + lane];
+    P.f2 = pp[8 * 32 + lane];
+    P.f3 = pp[9 * 32 + lane];
+    P.bex = pp[10 * 32 + lane];
     return P;
 }
 
@@ -288,32 +302,37 @@ __device__ __forceinline__ LinePrep read_prep(const double *pp, int lane)
 template <int K>
 __global__ void k_prep_sl(double *__restrict__ solve, i64 lines_total)
 {
-    constexpr int LR = lr_of(K);
     const int lane = threadIdx.x & 31;
     const i64 line = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
     if (line >= lines_total) return;
     double *rec = solve + line * (i64)recd_of(K);
     const LaneSl<K> L(lane);
     double aL[K], aU[K];
-    ld_rec(rec + (L.desc ? SL_NU : SL_NL) * LR, L, aL);
-    ld_rec(rec + (L.desc ? SL_NL : SL_NU) * LR, L, aU);
+    ld_rec(rec + (L.desc ? o_nu(K) : o_nl(K)), L, aL);
+    ld_rec(rec + (L.desc ? o_nl(K) : o_nu(K)), L, aU);
     const LinePrep P = line_prep<K>(lane & 15, aL, aU);
-    double *pp = rec + SL_N * LR;
-    const double v[NPREP] = {P.p1, P.p2, P.p3, P.e0, P.e1, P.e2, P.e3, P.q1, P.q2, P.q3, P.f0, P.f1, P.f2, P.f3, P.bex};
+    double *pp = rec + o_prep(K);
+    const double v[NPREP] = {P.p2, P.p3, P.e1, P.e2, P.e3, P.q2, P.q3, P.f1, P.f2, P.f3, P.bex};
 #pragma unroll
     for (int c = 0; c < NPREP; c++) pp[c * 32 + lane] = v[c];
 }
 
-// ---------------- producer: bulk copies of one plane's line records
+// ---------------- producer: bulk copies of what each line step reads
+//   lower sweep:  block, in-plane coupling (L2' / U2' by half), C1 (+C2), b' (LOWER3)
+//   upper sweep:  block, in-plane coupling (U2' / L2'), xo (UPPER3)
 template <int K, int D>
 __device__ void produce_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q, const Ring<K, D> &R,
                               unsigned &rec)
 {
     const int lane = threadIdx.x & 31;
     constexpr int LR = lr_of(K);
-    const unsigned rbytes = LR * 8u;
-    const unsigned recbytes = recd_of(K) * 8u;
+    constexpr unsigned lb = LR * 8u, bb = blk_of(K) * 8u;
+    const bool lower3 = P.mode == M_LOWER3;
     for (int ph = 0; ph < 2; ph++) {
+        const int cpl = (ph == 0) == (Q.w2 == 0) ? o_l2(K) : o_u2(K);
+        const unsigned nc = ph == 0 ? (P.two ? 2u : 1u) : 0u;
+        const bool extra = ph == 0 ? lower3 : !lower3;
+        const unsigned bytes = bb + lb + nc * lb + (extra ? lb : 0u);
         for (int i = 0; i < Q.cnt; i++, rec++) {
             if (lane == 0) {
                 const int st = rec % D;
@@ -322,14 +341,28 @@ __device__ void produce_plane(const SlArrays &S, const PlaneDesc &P, const Seq &
                 unsigned long long *bar = &R.full[st];
                 const int q = ph == 0 ? Q.qlow(i) : Q.qup(i);
                 const i64 line = P.prec + q;
-                const bool extra = ph == 0 ? P.mode == M_LOWER3 : P.mode == M_UPPER3;
-                mbar_expect_tx(bar, recbytes + (extra ? rbytes : 0u));
-                tma_load_1d(R.seg(st, 0), S.solve + line * (i64)recd_of(K), recbytes, bar);
-                if (extra) tma_load_1d(R.seg(st, G_X), (ph == 0 ? S.b : S.x) + line * (i64)LR, rbytes, bar);
+                const double *src = S.solve + line * (i64)recd_of(K);
+                double *dst = R.stage(st);
+                mbar_expect_tx(bar, bytes);
+                tma_load_1d(dst, src, bb, bar);
+                tma_load_1d(dst + rs0_of(K), src + cpl, lb, bar);
+                if (nc) tma_load_1d(dst + rs1_of(K), src + P.c1, nc * lb, bar);
+                if (extra) tma_load_1d(dst + rx_of(K), (ph == 0 ? S.b : S.x) + line * (i64)LR, lb, bar);
             }
         }
     }
     __syncwarp();
+}
+
+template <int K>
+__device__ __forceinline__ void sub_mul(double (&r)[K], double &rt, const double *c, const LaneSl<K> &L,
+                                        const double (&y)[K], double yt)
+{
+    double cv[K], ct;
+    ld_rec(c, L, cv, ct);
+#pragma unroll
+    for (int k = 0; k < K; k++) r[k] -= cv[k] * y[k];
+    rt -= ct * yt;
 }
 
 // ---------------- solver: one plane
@@ -338,38 +371,30 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
                             int &parity, const Ring<K, D> &R, const LaneSl<K> &L, unsigned &rec)
 {
     constexpr int LR = lr_of(K);
-    const int lane = threadIdx.x & 31, s = lane & 15, w2 = Q.w2;
+    const int lane = threadIdx.x & 31, w2 = Q.w2;
     const int ny = Q.ny, t2 = Q.t2, cnt = Q.cnt, t = (nx - 1) / 2;
     const i64 plr = (i64)ny * LR;  // plane stride in SL
     const bool lower3 = P.mode == M_LOWER3;
-    // x-dependent neighbour planes
-    // Neighbour planes.  A missing neighbour has an exactly-zero l3/u3
-    // coefficient (first/last plane), so it is pointed at this plane's own
-    // (finite, zero-initialised) x record instead of branching.
-    const double *y1, *y2 = S.x;
-    int gC1;
+    // Plane bases (line q of a plane at base + q*LR).  A missing level-3
+    // neighbour (first/last plane) has an exactly-zero coupling; it reads the
+    // zero plane instead of branching.
+    double *xpl = S.x + P.prec * LR;
+    const double *y1, *y2 = S.zero;
     if (lower3) {
         if (TWO) {
-            gC1 = SL_L3;
-            y1 = P.hasM ? S.x - plr : S.x;
-            y2 = P.hasP ? S.x + plr : S.x;
+            y1 = P.hasM ? xpl - plr : S.zero;
+            y2 = P.hasP ? xpl + plr : S.zero;
         } else if (P.up) {
-            gC1 = SL_U3;
-            y1 = P.hasP ? S.x + plr : S.x;
+            y1 = P.hasP ? xpl + plr : S.zero;
         } else {
-            gC1 = SL_L3;
-            y1 = P.hasM ? S.x - plr : S.x;
+            y1 = P.hasM ? xpl - plr : S.zero;
         }
     } else {
-        gC1 = P.nbrUp ? SL_U3 : SL_L3;
-        y1 = P.nbrUp ? S.x + plr : S.x - plr;
+        y1 = P.nbrUp ? xpl + plr : xpl - plr;
     }
-    double *xlow = lower3 ? S.x : S.xs;  // lower-sweep store of this plane
-    const int gL = L.desc ? SL_NU : SL_NL, gU = L.desc ? SL_NL : SL_NU;
-    const int gCL = w2 == 0 ? SL_L2 : SL_U2, gCU = w2 == 0 ? SL_U2 : SL_L2;
-    auto recp = [&](const double *base, int q) { return base + (P.prec + q) * (i64)LR; };
-    auto srec = [&](int a, int q) { return S.solve + (P.prec + q) * (i64)recd_of(K) + a * LR; };
-    auto recw = [&](double *base, int q) { return base + (P.prec + q) * (i64)LR; };
+    double *xlow = (lower3 ? S.x : S.xs) + P.prec * LR;  // lower-sweep store of this plane
+    const int gL = L.desc ? o_nu(K) : o_nl(K), gU = L.desc ? o_nl(K) : o_nu(K);
+    auto srec = [&](int off, int q) { return S.solve + (P.prec + q) * (i64)recd_of(K) + off; };
     double xprev[K], xprevt = 0.0;
 #pragma unroll
     for (int k = 0; k < K; k++) xprev[k] = 0.0;
@@ -378,8 +403,8 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
 #pragma unroll
     for (int k = 0; k < K; k++) n1[k] = n2[k] = 0.0;
     if (cnt > 0) {
-        ld_rec(recp(y1, Q.qlow(0)), L, n1, n1t);
-        if (TWO) ld_rec(recp(y2, Q.qlow(0)), L, n2, n2t);
+        ld_rec(y1 + Q.qlow(0) * LR, L, n1, n1t);
+        if (TWO) ld_rec(y2 + Q.qlow(0) * LR, L, n2, n2t);
     }
     for (int i = 0; i < cnt; i++, rec++) {
         double v1[K], v1t = n1t, v2[K], v2t = n2t;
@@ -389,62 +414,40 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
             v2[k] = n2[k];
         }
         if (i + 1 < cnt) {
-            ld_rec(recp(y1, Q.qlow(i + 1)), L, n1, n1t);
-            if (TWO) ld_rec(recp(y2, Q.qlow(i + 1)), L, n2, n2t);
+            ld_rec(y1 + Q.qlow(i + 1) * LR, L, n1, n1t);
+            if (TWO) ld_rec(y2 + Q.qlow(i + 1) * LR, L, n2, n2t);
         }
         const int st = rec % D;
         TSTAMP(q1);
         mbar_wait(&R.full[st], (rec / D) & 1);
         TSTAMP(q2);
         TACC(0, q1, q2);
-        double aL[K], mr[K], aU[K], rhs[K], mrt, nlt, nut, rhst;
-        ld_rec(R.seg(st, SL_MR), L, mr, mrt);
-        ld_rec(R.seg(st, gL), L, aL);
-        ld_rec(R.seg(st, gU), L, aU);
-        nlt = R.seg(st, SL_NL)[L.tw];
-        nut = R.seg(st, SL_NU)[L.tw];
+        const double *sg = R.stage(st);
+        double aL[K], aU[K], rhs[K], rhst;
+        ld_rec(sg + gL, L, aL);
+        ld_rec(sg + gU, L, aU);
+        const double nlt = sg[o_nl(K) + L.tw], nut = sg[o_nu(K) + L.tw];
         if (lower3) {
-            ld_rec(R.seg(st, G_X), L, rhs, rhst);
-            {
-                double c[K], ct;
-                ld_rec(R.seg(st, gC1), L, c, ct);
-#pragma unroll
-                for (int k = 0; k < K; k++) rhs[k] -= c[k] * v1[k];
-                rhst -= ct * v1t;
-            }
-            if (TWO) {
-                double c[K], ct;
-                ld_rec(R.seg(st, SL_U3), L, c, ct);
-#pragma unroll
-                for (int k = 0; k < K; k++) rhs[k] -= c[k] * v2[k];
-                rhst -= ct * v2t;
-            }
+            ld_rec(sg + rx_of(K), L, rhs, rhst);
+            sub_mul(rhs, rhst, sg + rs1_of(K), L, v1, v1t);
+            if (TWO) sub_mul(rhs, rhst, sg + rs2_of(K), L, v2, v2t);
         } else {
             double c[K], ct;
-            ld_rec(R.seg(st, gC1), L, c, ct);
+            ld_rec(sg + rs1_of(K), L, c, ct);
 #pragma unroll
             for (int k = 0; k < K; k++) rhs[k] = c[k] * v1[k];
             rhst = ct * v1t;
         }
-        {
-            double cp[K], cpt;  // line 0: xprev = 0, so the term vanishes
-            ld_rec(R.seg(st, gCL), L, cp, cpt);
-#pragma unroll
-            for (int k = 0; k < K; k++) rhs[k] -= cp[k] * xprev[k];
-            rhst -= cpt * xprevt;
-        }
-        const int st_rel = st;
+        sub_mul(rhs, rhst, sg + rs0_of(K), L, xprev, xprevt);  // line 0: xprev = 0
         TSTAMP(q3);
         TACC(1, q2, q3);
         double x[K], xt;
-        { const LinePrep PP_ = read_prep(R.seg(st_rel, G_PREP), lane); double cr_[K];
-#pragma unroll
-        for (int k_ = 0; k_ < K; k_++) cr_[k_] = (rhs)[k_] * mr[k_];
-        line_solve4<K>(PP_, nx, t, aL, cr_, aU, (rhst) * mrt, nlt, nut, x, xt); }
+        const LinePrep PP = read_prep<K>(sg + o_prep(K), lane, aL, aU);
+        line_solve4<K>(PP, nx, t, aL, rhs, aU, rhst, nlt, nut, x, xt);
         TSTAMP(q4);
         TACC(2, q3, q4);
-        mbar_arrive(&R.empty[st_rel]);
-        st_rec(recw(xlow, Q.qlow(i)), L, x, xt, lane);
+        mbar_arrive(&R.empty[st]);
+        st_rec(xlow + Q.qlow(i) * LR, L, x, xt);
         TSTAMP(q5);
         TACC(3, q4, q5);
 #pragma unroll
@@ -479,66 +482,44 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
     double yv[K], yvt = 0.0;
     {
         const int q = t2;
-        double aL[K], mr[K], aU[K], mrt, nlt, nut, rhs[K], rhst;
-        ld_rec(srec(SL_MR, q), L, mr, mrt);
+        double aL[K], aU[K], rhs[K], rhst;
         ld_rec(srec(gL, q), L, aL);
         ld_rec(srec(gU, q), L, aU);
-        nlt = srec(SL_NL, q)[L.tw];
-        nut = srec(SL_NU, q)[L.tw];
+        const double nlt = srec(o_nl(K), q)[L.tw], nut = srec(o_nu(K), q)[L.tw];
         if (lower3) {
-            ld_rec(recp(S.b, q), L, rhs, rhst);
+            ld_rec(S.b + (P.prec + q) * LR, L, rhs, rhst);
             if (P.hasM) {
-                double c[K], ct, y[K], yt;
-                ld_rec(srec(SL_L3, q), L, c, ct);
-                ld_rec(recp(S.x - plr, q), L, y, yt);
-#pragma unroll
-                for (int k = 0; k < K; k++) rhs[k] -= c[k] * y[k];
-                rhst -= ct * yt;
+                double y[K], yt;
+                ld_rec(xpl - plr + q * LR, L, y, yt);
+                sub_mul(rhs, rhst, srec(o_l3(K), q), L, y, yt);
             }
             if (P.hasP) {
-                double c[K], ct, y[K], yt;
-                ld_rec(srec(SL_U3, q), L, c, ct);
-                ld_rec(recp(S.x + plr, q), L, y, yt);
-#pragma unroll
-                for (int k = 0; k < K; k++) rhs[k] -= c[k] * y[k];
-                rhst -= ct * yt;
+                double y[K], yt;
+                ld_rec(xpl + plr + q * LR, L, y, yt);
+                sub_mul(rhs, rhst, srec(o_u3(K), q), L, y, yt);
             }
         } else {
             double c[K], ct, y[K], yt;
-            ld_rec(srec(gC1, q), L, c, ct);
-            ld_rec(recp(y1, q), L, y, yt);
+            ld_rec(srec(P.c1, q), L, c, ct);
+            ld_rec(y1 + q * LR, L, y, yt);
 #pragma unroll
             for (int k = 0; k < K; k++) rhs[k] = c[k] * y[k];
             rhst = ct * yt;
         }
-        if (t2 > 0) {
-            double c[K], ct;
-            ld_rec(srec(SL_L2, q), L, c, ct);
-#pragma unroll
-            for (int k = 0; k < K; k++) rhs[k] -= c[k] * xa[k];
-            rhst -= ct * xat;
-        }
-        if (t2 < ny - 1) {
-            double c[K], ct;
-            ld_rec(srec(SL_U2, q), L, c, ct);
-#pragma unroll
-            for (int k = 0; k < K; k++) rhs[k] -= c[k] * xd[k];
-            rhst -= ct * xdt;
-        }
-        if (cnt > 0) ld_rec(recp(xlow, Q.qup(0)), L, yv, yvt);  // first upper line's lower value
-        { const LinePrep PP_ = line_prep<K>(s, aL, aU); double cr_[K];
-#pragma unroll
-        for (int k_ = 0; k_ < K; k_++) cr_[k_] = (rhs)[k_] * mr[k_];
-        line_solve4<K>(PP_, nx, t, aL, cr_, aU, (rhst) * mrt, nlt, nut, xn, xnt); }
+        if (t2 > 0) sub_mul(rhs, rhst, srec(o_l2(K), q), L, xa, xat);
+        if (t2 < ny - 1) sub_mul(rhs, rhst, srec(o_u2(K), q), L, xd, xdt);
+        if (cnt > 0) ld_rec(xlow + Q.qup(0) * LR, L, yv, yvt);  // first upper line's lower value
+        const LinePrep PP = line_prep<K>(lane & 15, aL, aU);
+        line_solve4<K>(PP, nx, t, aL, rhs, aU, rhst, nlt, nut, xn, xnt);
         if (w2 == 0) {
             if (lower3) {
-                st_rec(recw(S.x, q), L, xn, xnt, lane);
+                st_rec(xpl + q * LR, L, xn, xnt);
             } else {
                 double xo[K], xot, nv[K];
-                ld_rec(recp(S.x, q), L, xo, xot);
+                ld_rec(xpl + q * LR, L, xo, xot);
 #pragma unroll
                 for (int k = 0; k < K; k++) nv[k] = xo[k] - xn[k];
-                st_rec(recw(S.x, q), L, nv, xot - xnt, lane);
+                st_rec(xpl + q * LR, L, nv, xot - xnt);
             }
         }
     }
@@ -547,28 +528,24 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
         double y[K], yt = yvt;
 #pragma unroll
         for (int k = 0; k < K; k++) y[k] = yv[k];
-        if (i + 1 < cnt) ld_rec(recp(xlow, Q.qup(i + 1)), L, yv, yvt);
+        if (i + 1 < cnt) ld_rec(xlow + Q.qup(i + 1) * LR, L, yv, yvt);
         const int st = rec % D;
         mbar_wait(&R.full[st], (rec / D) & 1);
-        double aL[K], mr[K], aU[K], cp[K], mrt, nlt, nut, cpt;
-        ld_rec(R.seg(st, SL_MR), L, mr, mrt);
-        ld_rec(R.seg(st, gL), L, aL);
-        ld_rec(R.seg(st, gU), L, aU);
-        nlt = R.seg(st, SL_NL)[L.tw];
-        nut = R.seg(st, SL_NU)[L.tw];
-        ld_rec(R.seg(st, gCU), L, cp, cpt);
+        const double *sg = R.stage(st);
+        double aL[K], aU[K], cp[K], cpt;
+        ld_rec(sg + gL, L, aL);
+        ld_rec(sg + gU, L, aU);
+        const double nlt = sg[o_nl(K) + L.tw], nut = sg[o_nu(K) + L.tw];
+        ld_rec(sg + rs0_of(K), L, cp, cpt);
         double xo[K], xot = 0.0;
-        if (!lower3) ld_rec(R.seg(st, G_X), L, xo, xot);
-        const int st_rel = st;
+        if (!lower3) ld_rec(sg + rx_of(K), L, xo, xot);
         double bs[K];
 #pragma unroll
         for (int k = 0; k < K; k++) bs[k] = cp[k] * xn[k];
         double xs[K], xst;
-        { const LinePrep PP_ = read_prep(R.seg(st_rel, G_PREP), lane); double cr_[K];
-#pragma unroll
-        for (int k_ = 0; k_ < K; k_++) cr_[k_] = (bs)[k_] * mr[k_];
-        line_solve4<K>(PP_, nx, t, aL, cr_, aU, (cpt * xnt) * mrt, nlt, nut, xs, xst); }
-        mbar_arrive(&R.empty[st_rel]);
+        const LinePrep PP = read_prep<K>(sg + o_prep(K), lane, aL, aU);
+        line_solve4<K>(PP, nx, t, aL, bs, aU, cpt * xnt, nlt, nut, xs, xst);
+        mbar_arrive(&R.empty[st]);
 #pragma unroll
         for (int k = 0; k < K; k++) xn[k] = y[k] - xs[k];
         xnt = yt - xst;
@@ -576,26 +553,17 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
             double nv[K];
 #pragma unroll
             for (int k = 0; k < K; k++) nv[k] = xo[k] - xn[k];
-            st_rec(recw(S.x, Q.qup(i)), L, nv, xot - xnt, lane);
+            st_rec(xpl + Q.qup(i) * LR, L, nv, xot - xnt);
         } else {
-            st_rec(recw(S.x, Q.qup(i)), L, xn, xnt, lane);
+            st_rec(xpl + Q.qup(i) * LR, L, xn, xnt);
         }
     }
 }
 
-// L2 prefetch of one plane's SL records this warp will read (producers)
-__device__ __forceinline__ void prefetch_sl(const double *p, i64 r0, i64 r1)
-{
-    if (!p || r1 <= r0) return;
-    const char *c = (const char *)(p + r0);
-    const i64 bytes = (r1 - r0) * 8;
-    for (i64 off = (i64)(threadIdx.x & 31) * 128; off < bytes; off += 32 * 128) prefetch_l2(c + off);
-}
-
 template <int K, int D>
 __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ solve, const double *__restrict__ bsl,
-                                                  double *xsl, double *xssl, int nx, int ny, int nz,
-                                                  const int32_t *__restrict__ active)
+                                                  double *xsl, double *xssl, const double *__restrict__ zpl, int nx,
+                                                  int ny, int nz, const int32_t *__restrict__ active)
 {
     extern __shared__ __align__(128) double sl_ring[];
     __shared__ double ex[2][2 * 2 * (32 * K + 1)];
@@ -609,7 +577,7 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
     S.b = bsl + sys * nsl;
     S.x = xsl + sys * nsl;
     S.xs = xssl + sys * nsl;
-    S.nsl = nsl;
+    S.zero = zpl;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool producer = warp >= 4;
     const int sw = warp & 3, pair = sw >> 1, w2 = sw & 1, bar = 1 + pair;
@@ -635,29 +603,20 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
     double *myex = ex[pair];
     int parity = 0;
     const int t3 = (nz - 1) / 2;
-    const i64 plr = (i64)ny * LR;
-    // warp's row range of a plane (for L2 prefetch)
-    const i64 wr0 = w2 == 0 ? 0 : (i64)Q.t2 * LR, wr1 = w2 == 0 ? (i64)(Q.t2 + 1) * LR : plr;
-    auto prefetch_plane_sl = [&](int p, bool upper) {
-        if (!PREFETCH_PLANES) return;
-        const i64 b0 = (i64)p * plr;
-        prefetch_sl(S.solve, (b0 + wr0) / LR * recd_of(K), (b0 + wr1) / LR * recd_of(K));
-        prefetch_sl(upper ? S.x : S.b, b0 + wr0, b0 + wr1);
-    };
     // level-3 lower sweep (ntd_solve.py:198-221)
     const int nlow = pair == 0 ? t3 : nz - 1 - t3;
-    if (producer) prefetch_plane_sl(pair == 0 ? 0 : nz - 1, false);
     for (int i = 0; i < nlow; i++) {
         const int p = pair == 0 ? i : nz - 1 - i;
         PlaneDesc P;
         P.prec = (i64)p * ny;
         P.mode = M_LOWER3;
+        P.two = false;
         P.hasM = pair == 0 && p > 0;
         P.hasP = pair == 1 && p < nz - 1;
         P.nbrUp = false;
         P.up = pair == 1;
+        P.c1 = P.up ? o_u3(K) : o_l3(K);
         if (producer) {
-            if (i + 1 < nlow) prefetch_plane_sl(pair == 0 ? p + 1 : p - 1, false);
             produce_plane<K, D>(S, P, Q, R, rec);
         } else {
             solve_plane<K, D, M_LOWER3, false>(S, P, Q, nx, bar, myex, parity, R, L, rec);
@@ -669,10 +628,12 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
         PlaneDesc P;
         P.prec = (i64)t3 * ny;
         P.mode = M_LOWER3;
+        P.two = true;
         P.hasM = t3 > 0;
         P.hasP = t3 < nz - 1;
         P.nbrUp = false;
         P.up = false;
+        P.c1 = o_l3(K);  // L3 then U3 (contiguous)
         if (producer) {
             fence_proxy_async();
             produce_plane<K, D>(S, P, Q, R, rec);
@@ -683,17 +644,17 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
     __syncthreads();
     if (producer) fence_proxy_async();  // x (read as xo) was written by generic stores
     // level-3 upper sweep (ntd_solve.py:233-253)
-    if (producer && nlow > 0) prefetch_plane_sl(pair == 0 ? t3 - 1 : t3 + 1, true);
     for (int i = 0; i < nlow; i++) {
         const int p = pair == 0 ? t3 - 1 - i : t3 + 1 + i;
         PlaneDesc P;
         P.prec = (i64)p * ny;
         P.mode = M_UPPER3;
+        P.two = false;
         P.hasM = P.hasP = false;
         P.nbrUp = pair == 0;
         P.up = false;
+        P.c1 = P.nbrUp ? o_u3(K) : o_l3(K);
         if (producer) {
-            if (i + 1 < nlow) prefetch_plane_sl(pair == 0 ? p - 1 : p + 1, true);
             produce_plane<K, D>(S, P, Q, R, rec);
         } else {
             solve_plane<K, D, M_UPPER3, false>(S, P, Q, nx, bar, myex, parity, R, L, rec);
@@ -706,8 +667,8 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
 template <int K>
 int launch_prep_sl_k(double *solve, i64 lines_total, cudaStream_t st);
 template <int K>
-int launch_apply_sl_k(const double *solve, const double *bsl, double *xsl, double *xssl, int nx, int ny, int nz,
-                      i64 batch, const int32_t *active, cudaStream_t st, int depth);
+int launch_apply_sl_k(const double *solve, const double *bsl, double *xsl, double *xssl, const double *zpl, int nx,
+                      int ny, int nz, i64 batch, const int32_t *active, cudaStream_t st, int depth);
 
 #define NTD_INSTANTIATE_SL(K)                                                                                     \
     template <>                                                                                                    \
@@ -718,8 +679,8 @@ int launch_apply_sl_k(const double *solve, const double *bsl, double *xsl, doubl
         return ntd::check_launch("ntd_solve_bands prep");                                                          \
     }                                                                                                              \
     template <>                                                                                                    \
-    int launch_apply_sl_k<K>(const double *solve, const double *bsl, double *xsl, double *xssl, int nx, int ny,    \
-                             int nz, i64 batch, const int32_t *active, cudaStream_t st, int depth)                 \
+    int launch_apply_sl_k<K>(const double *solve, const double *bsl, double *xsl, double *xssl, const double *zpl,   \
+                             int nx, int ny, int nz, i64 batch, const int32_t *active, cudaStream_t st, int depth)  \
     {                                                                                                              \
         size_t smem = (size_t)4 * depth * sl::stage_of(K) * 8;                                                     \
         cudaError_t e = depth == 4                                                                                 \
@@ -730,8 +691,8 @@ int launch_apply_sl_k(const double *solve, const double *bsl, double *xsl, doubl
             return NTD_ELAUNCH;                                                                                    \
         }                                                                                                          \
         if (depth == 4)                                                                                            \
-            sl::k_apply<K, 4><<<(unsigned)batch, 256, smem, st>>>(solve, bsl, xsl, xssl, nx, ny, nz, active);      \
+            sl::k_apply<K, 4><<<(unsigned)batch, 256, smem, st>>>(solve, bsl, xsl, xssl, zpl, nx, ny, nz, active);      \
         else                                                                                                       \
-            sl::k_apply<K, 2><<<(unsigned)batch, 256, smem, st>>>(solve, bsl, xsl, xssl, nx, ny, nz, active);      \
+            sl::k_apply<K, 2><<<(unsigned)batch, 256, smem, st>>>(solve, bsl, xsl, xssl, zpl, nx, ny, nz, active);      \
         return ntd::check_launch("ntd_apply");                                                                     \
     }

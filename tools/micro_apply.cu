@@ -24,19 +24,20 @@ int main(int argc, char **argv)
     const long nsl = (long)ny * nz * LR;
     double *sv, *bs, *xs, *xss;
     const long nrec = (long)ny * nz * sl::recd_of(K); cudaMalloc(&sv, 8 * nrec * B); cudaMalloc(&bs, 8 * nsl * B); cudaMalloc(&xs, 8 * nsl * B); cudaMalloc(&xss, 8 * nsl * B);
+    double *zp; cudaMalloc(&zp, 8 * ny * LR); cudaMemset(zp, 0, 8 * ny * LR);
     std::vector<double> hs(nrec * B);
-    for (long i = 0; i < nrec * B; i++) { long a = (i % sl::recd_of(K)) / LR; hs[i] = a == 0 ? 0.3 : (a < 3 ? -0.05 : (a < 7 ? -0.1 : 0.01)); }
+    for (long i = 0; i < nrec * B; i++) { long o = i % sl::recd_of(K); hs[i] = o < 2 * LR ? -0.05 : (o < sl::blk_of(K) ? 0.01 : -0.03); }
     cudaMemcpy(sv, hs.data(), 8 * nrec * B, cudaMemcpyHostToDevice);
     cudaMemset(bs, 0, 8 * nsl * B); cudaMemset(xs, 0, 8 * nsl * B); cudaMemset(xss, 0, 8 * nsl * B);
     size_t smem = (size_t)4 * 4 * sl::stage_of(K) * 8;
     cudaFuncSetAttribute(sl::k_apply<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sl::k_apply<3, 4><<<B, 256, smem>>>(sv, bs, xs, xss, nx, ny, nz, nullptr);
+    sl::k_apply<3, 4><<<B, 256, smem>>>(sv, bs, xs, xss, zp, nx, ny, nz, nullptr);
     cudaDeviceSynchronize();
     unsigned long long zero[64] = {0};
     cudaMemcpyToSymbol(g_ntd_timing, zero, sizeof(zero));
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    sl::k_apply<3, 4><<<B, 256, smem>>>(sv, bs, xs, xss, nx, ny, nz, nullptr);
+    sl::k_apply<3, 4><<<B, 256, smem>>>(sv, bs, xs, xss, zp, nx, ny, nz, nullptr);
     cudaEventRecord(e1);
     cudaDeviceSynchronize();
     float ms; cudaEventElapsedTime(&ms, e0, e1);
