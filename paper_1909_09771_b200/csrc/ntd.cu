@@ -41,8 +41,7 @@ extern "C" int64_t ntd_max_nx(void) { return 32 * MAX_K; }
 static int sl_depth(int K)
 {
     if (K > 11) return 0;
-    const size_t per_stage = (size_t)4 * sl::stage_of(K) * 8;
-    return per_stage * 4 <= 200 * 1024 ? 4 : (per_stage * 2 <= 200 * 1024 ? 2 : 0);
+    return sl::depth_of(K) >= 2 ? sl::depth_of(K) : 0;
 }
 
 static i64 sl_doubles(i64 nx, i64 ny, i64 nz)
@@ -124,7 +123,7 @@ extern "C" int ntd_apply(const double *pre, const double *solve, const double *b
         switch (K) {
 #define SLCASE(KK)                                                                                                \
     case KK:                                                                                                       \
-        rc = launch_apply_sl_k<KK>(solve, bsl, xsl, xssl, zpl, (int)nx, (int)ny, (int)nz, batch, active, st, depth);    \
+        rc = launch_apply_sl_k<KK>(solve, bsl, xsl, xssl, zpl, (int)nx, (int)ny, (int)nz, batch, active, st);    \
         break;
             SLCASE(1) SLCASE(2) SLCASE(3) SLCASE(4) SLCASE(5) SLCASE(6) SLCASE(8) SLCASE(11)
 #undef SLCASE

@@ -27,6 +27,7 @@
 
 namespace sl {
 
+
 // Solve record of one line (record-major, [system][line][RECD]):
 //   [ NL | NU | PREP (NPREP x 32) | L2' | U2' | L3' | U3' ]
 // NL = -(l1 m), NU = -(u1 m) are the chain coefficients, PREP the line's
@@ -52,6 +53,14 @@ __host__ __device__ constexpr int rs1_of(int K) { return blk_of(K) + lr_of(K); }
 __host__ __device__ constexpr int rs2_of(int K) { return blk_of(K) + 2 * lr_of(K); }
 __host__ __device__ constexpr int rx_of(int K) { return blk_of(K) + 3 * lr_of(K); }
 __host__ __device__ constexpr int stage_of(int K) { return blk_of(K) + 4 * lr_of(K); }
+// ring depth: as many stages as fit beside the static shared memory (<= 8)
+__host__ __device__ constexpr int static_smem_of(int K) { return 2 * 2 * 2 * (32 * K + 1) * 8 + 4 * 2 * 8 * 8; }
+__host__ __device__ constexpr int depth_of(int K)
+{
+    return (232448 - 1024 - static_smem_of(K)) / (4 * stage_of(K) * 8) > 8
+               ? 8
+               : (232448 - 1024 - static_smem_of(K)) / (4 * stage_of(K) * 8);
+}
 
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(void *bar)
@@ -320,38 +329,86 @@ __global__ void k_prep_sl(double *__restrict__ solve, i64 lines_total)
 // ---------------- producer: bulk copies of what each line step reads
 //   lower sweep:  block, in-plane coupling (L2' / U2' by half), C1 (+C2), b' (LOWER3)
 //   upper sweep:  block, in-plane coupling (U2' / L2'), xo (UPPER3)
-template <int K, int D>
-__device__ void produce_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q, const Ring<K, D> &R,
-                              unsigned &rec)
+// Record k of a plane (k < cnt: lower sweep, else upper sweep) is copied
+// into a ring stage (dst) or, with dst == nullptr, prefetched into L2.
+#ifndef NTD_L2_PF
+#define NTD_L2_PF 0
+#endif
+constexpr int L2_PF = NTD_L2_PF;
+#ifndef NTD_PRODUCER_FENCE
+#define NTD_PRODUCER_FENCE 1
+#endif
+constexpr bool PRODUCER_FENCE = NTD_PRODUCER_FENCE;
+#ifndef NTD_WAIT_AHEAD
+#define NTD_WAIT_AHEAD 1
+#endif
+constexpr bool WAIT_AHEAD = NTD_WAIT_AHEAD;  // test the barrier of record i+2, consume after the solve
+  // L2 prefetch distance in records (ahead of the ring copies)
+
+__device__ __forceinline__ void prefetch_bulk_l2(const double *p, unsigned bytes)
 {
-    const int lane = threadIdx.x & 31;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <int K>
+__device__ __forceinline__ void rec_copy(const SlArrays &S, const PlaneDesc &P, const Seq &Q, int k, double *dst,
+                                         unsigned long long *bar)
+{
     constexpr int LR = lr_of(K);
     constexpr unsigned lb = LR * 8u, bb = blk_of(K) * 8u;
     const bool lower3 = P.mode == M_LOWER3;
-    for (int ph = 0; ph < 2; ph++) {
-        const int cpl = (ph == 0) == (Q.w2 == 0) ? o_l2(K) : o_u2(K);
-        const unsigned nc = ph == 0 ? (P.two ? 2u : 1u) : 0u;
-        const bool extra = ph == 0 ? lower3 : !lower3;
-        const unsigned bytes = bb + lb + nc * lb + (extra ? lb : 0u);
-        for (int i = 0; i < Q.cnt; i++, rec++) {
-            if (lane == 0) {
-                const int st = rec % D;
-                if (rec >= (unsigned)D) mbar_wait_lazy(&R.empty[st], ((rec / D) + 1) & 1);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                unsigned long long *bar = &R.full[st];
-                const int q = ph == 0 ? Q.qlow(i) : Q.qup(i);
-                const i64 line = P.prec + q;
-                const double *src = S.solve + line * (i64)recd_of(K);
-                double *dst = R.stage(st);
-                mbar_expect_tx(bar, bytes);
-                tma_load_1d(dst, src, bb, bar);
-                tma_load_1d(dst + rs0_of(K), src + cpl, lb, bar);
-                if (nc) tma_load_1d(dst + rs1_of(K), src + P.c1, nc * lb, bar);
-                if (extra) tma_load_1d(dst + rx_of(K), (ph == 0 ? S.b : S.x) + line * (i64)LR, lb, bar);
-            }
+    const int ph = k < Q.cnt ? 0 : 1, i = ph ? k - Q.cnt : k;
+    const int cpl = (ph == 0) == (Q.w2 == 0) ? o_l2(K) : o_u2(K);
+    const unsigned nc = ph == 0 ? (P.two ? 2u : 1u) : 0u;
+    const bool extra = ph == 0 ? lower3 : !lower3;
+    const i64 line = P.prec + (ph == 0 ? Q.qlow(i) : Q.qup(i));
+    const double *src = S.solve + line * (i64)recd_of(K);
+    const double *xsrc = (ph == 0 ? S.b : S.x) + line * (i64)LR;
+    if (dst) {
+        mbar_expect_tx(bar, bb + lb + nc * lb + (extra ? lb : 0u));
+        tma_load_1d(dst, src, bb, bar);
+        tma_load_1d(dst + rs0_of(K), src + cpl, lb, bar);
+        if (nc) tma_load_1d(dst + rs1_of(K), src + P.c1, nc * lb, bar);
+        if (extra) tma_load_1d(dst + rx_of(K), xsrc, lb, bar);
+    } else {
+        prefetch_bulk_l2(src, bb);
+        prefetch_bulk_l2(src + cpl, lb);
+        if (nc) prefetch_bulk_l2(src + P.c1, nc * lb);
+        if (extra) prefetch_bulk_l2(xsrc, lb);
+    }
+}
+
+// Pn: the warp's next plane (L2 prefetch runs across the boundary), or nullptr
+template <int K, int D>
+__device__ void produce_plane(const SlArrays &S, const PlaneDesc &P, const PlaneDesc *Pn, const Seq &Q,
+                              const Ring<K, D> &R, unsigned &rec)
+{
+    const int lane = threadIdx.x & 31;
+    const int n = 2 * Q.cnt;
+    if (lane == 0) {
+        for (int k = 0; k < n; k++, rec++) {
+            const int j = k + L2_PF;
+            if (j < n)
+                rec_copy<K>(S, P, Q, j, nullptr, nullptr);
+            else if (Pn && j - n < n)
+                rec_copy<K>(S, *Pn, Q, j - n, nullptr, nullptr);
+            const int st = rec % D;
+            if (rec >= (unsigned)D) mbar_wait_lazy(&R.empty[st], ((rec / D) + 1) & 1);
+            if (PRODUCER_FENCE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            rec_copy<K>(S, P, Q, k, R.stage(st), &R.full[st]);
         }
     }
     __syncwarp();
+}
+
+__device__ __forceinline__ bool mbar_test(void *bar, unsigned parity)
+{
+    unsigned ok;
+    asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok)
+                 : "r"(smem_u32(bar)), "r"(parity)
+                 : "memory");
+    return ok != 0;
 }
 
 template <int K>
@@ -365,6 +422,93 @@ __device__ __forceinline__ void sub_mul(double (&r)[K], double &rt, const double
     rt -= ct * yt;
 }
 
+// Ring operands of one line step, loaded one step ahead (software pipeline):
+// ld_* only issues the shared-memory loads; fin_* (placed after the current
+// line's solve) forms the x-independent constants from them.
+template <int K>
+struct LineOps {
+    double aL[K], aU[K], cp[K], pt[K], c1[K], c2[K];  // chain coefs, in-plane coupling, constants, C1', C2'
+    double cpt, ptt, c1t, c2t, nlt, nut;
+    LinePrep P;
+};
+
+template <int K>
+__device__ __forceinline__ void ld_common(LineOps<K> &o, const double *sg, const LaneSl<K> &L, int lane)
+{
+    ld_rec(sg + (L.desc ? o_nu(K) : o_nl(K)), L, o.aL);
+    ld_rec(sg + (L.desc ? o_nl(K) : o_nu(K)), L, o.aU);
+    o.nlt = sg[o_nl(K) + L.tw];
+    o.nut = sg[o_nu(K) + L.tw];
+    ld_rec(sg + rs0_of(K), L, o.cp, o.cpt);
+    const double *pp = sg + o_prep(K);
+    o.P.p2 = pp[0 * 32 + lane];
+    o.P.p3 = pp[1 * 32 + lane];
+    o.P.e1 = pp[2 * 32 + lane];
+    o.P.e2 = pp[3 * 32 + lane];
+    o.P.e3 = pp[4 * 32 + lane];
+    o.P.q2 = pp[5 * 32 + lane];
+    o.P.q3 = pp[6 * 32 + lane];
+    o.P.f1 = pp[7 * 32 + lane];
+    o.P.f2 = pp[8 * 32 + lane];
+    o.P.f3 = pp[9 * 32 + lane];
+    o.P.bex = pp[10 * 32 + lane];
+}
+
+// p1, e0, q1, f0 (same expressions as line_prep)
+template <int K>
+__device__ __forceinline__ void fin_prep(LineOps<K> &o, int lane)
+{
+    const int s = lane & 15;
+    double A0 = 1.0, B0 = 1.0;
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        A0 *= o.aL[k];
+        B0 *= o.aU[k];
+    }
+    o.P.p1 = s >= 1 ? A0 : 0.0;
+    o.P.e0 = s >= 1 ? 1.0 : 0.0;
+    o.P.q1 = s <= 14 ? B0 : 0.0;
+    o.P.f0 = s <= 14 ? 1.0 : 0.0;
+}
+
+// lower sweep: pt = b' - C1' y1 (- C2' y2)   (LOWER3)   or   C1' y1   (UPPER3)
+template <int K, bool LOWER3, bool TWO>
+__device__ __forceinline__ void ld_lower(LineOps<K> &o, const double *sg, const LaneSl<K> &L, int lane)
+{
+    ld_common(o, sg, L, lane);
+    if (LOWER3) ld_rec(sg + rx_of(K), L, o.pt, o.ptt);
+    ld_rec(sg + rs1_of(K), L, o.c1, o.c1t);
+    if (TWO) ld_rec(sg + rs2_of(K), L, o.c2, o.c2t);
+}
+template <int K, bool LOWER3, bool TWO>
+__device__ __forceinline__ void fin_lower(LineOps<K> &o, int lane, const double (&v1)[K], double v1t,
+                                          const double (&v2)[K], double v2t)
+{
+    fin_prep(o, lane);
+    if (LOWER3) {
+#pragma unroll
+        for (int k = 0; k < K; k++) o.pt[k] -= o.c1[k] * v1[k];
+        o.ptt -= o.c1t * v1t;
+        if (TWO) {
+#pragma unroll
+            for (int k = 0; k < K; k++) o.pt[k] -= o.c2[k] * v2[k];
+            o.ptt -= o.c2t * v2t;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < K; k++) o.pt[k] = o.c1[k] * v1[k];
+        o.ptt = o.c1t * v1t;
+    }
+}
+
+// upper sweep: pt = xo (UPPER3)
+template <int K, bool LOWER3>
+__device__ __forceinline__ void ld_upper(LineOps<K> &o, const double *sg, const LaneSl<K> &L, int lane)
+{
+    ld_common(o, sg, L, lane);
+    if (!LOWER3) ld_rec(sg + rx_of(K), L, o.pt, o.ptt);
+}
+
 // ---------------- solver: one plane
 template <int K, int D, int MODE, bool TWO>
 __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q, int nx, int bar_id, double *ex,
@@ -374,7 +518,7 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
     const int lane = threadIdx.x & 31, w2 = Q.w2;
     const int ny = Q.ny, t2 = Q.t2, cnt = Q.cnt, t = (nx - 1) / 2;
     const i64 plr = (i64)ny * LR;  // plane stride in SL
-    const bool lower3 = P.mode == M_LOWER3;
+    constexpr bool lower3 = MODE == M_LOWER3;
     // Plane bases (line q of a plane at base + q*LR).  A missing level-3
     // neighbour (first/last plane) has an exactly-zero coupling; it reads the
     // zero plane instead of branching.
@@ -399,60 +543,87 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
 #pragma unroll
     for (int k = 0; k < K; k++) xprev[k] = 0.0;
     // ---------------- level-2 lower sweep (ntd_solve.py:147-171)
-    double n1[K], n1t = 0.0, n2[K], n2t = 0.0;
+    // Software-pipelined (PIPE): the ring operands of line i+1 and the
+    // x-independent part of its scan constants are loaded while line i
+    // solves, so the serial chain per line is cr = pt - cp' xprev and the
+    // scans.  The full barrier of record i+2 is tested at the top of step i
+    // and its result consumed after the solve (an mbarrier test queues behind
+    // the warp's outstanding memory traffic: never block on it per step).
+    constexpr bool PIPE = K <= 5;
+    double n1[K], n1t = 0.0, n2[K], n2t = 0.0;  // neighbour-plane values, loaded ahead
 #pragma unroll
     for (int k = 0; k < K; k++) n1[k] = n2[k] = 0.0;
+    auto ld_nbr = [&](int j) {
+        ld_rec(y1 + Q.qlow(j) * LR, L, n1, n1t);
+        if (TWO) ld_rec(y2 + Q.qlow(j) * LR, L, n2, n2t);
+    };
+    auto full = [&](unsigned r) { return &R.full[r % D]; };
+    auto par = [&](unsigned r) { return (r / D) & 1u; };
+    LineOps<K> cur;
     if (cnt > 0) {
-        ld_rec(y1 + Q.qlow(0) * LR, L, n1, n1t);
-        if (TWO) ld_rec(y2 + Q.qlow(0) * LR, L, n2, n2t);
+        ld_nbr(0);
+        if (PIPE) {
+            double v1[K], v1t = n1t, v2[K], v2t = n2t;
+#pragma unroll
+            for (int k = 0; k < K; k++) {
+                v1[k] = n1[k];
+                v2[k] = n2[k];
+            }
+            ld_nbr(cnt > 1 ? 1 : 0);
+            mbar_wait(full(rec), par(rec));
+            ld_lower<K, lower3, TWO>(cur, R.stage(rec % D), L, lane);
+            fin_lower<K, lower3, TWO>(cur, lane, v1, v1t, v2, v2t);
+            if (WAIT_AHEAD && cnt > 1) mbar_wait(full(rec + 1), par(rec + 1));
+        }
     }
+#pragma unroll 2  // ping-pong registers: no copies of in-flight loads
     for (int i = 0; i < cnt; i++, rec++) {
+        const int st = rec % D;
+        TSTAMP(q1);
         double v1[K], v1t = n1t, v2[K], v2t = n2t;
 #pragma unroll
         for (int k = 0; k < K; k++) {
             v1[k] = n1[k];
             v2[k] = n2[k];
         }
-        if (i + 1 < cnt) {
-            ld_rec(y1 + Q.qlow(i + 1) * LR, L, n1, n1t);
-            if (TWO) ld_rec(y2 + Q.qlow(i + 1) * LR, L, n2, n2t);
+        LineOps<K> nxo;
+        bool ok2 = true;
+        if (PIPE) {
+            ld_nbr(i + 2 < cnt ? i + 2 : cnt - 1);
+            if (WAIT_AHEAD)
+                ok2 = mbar_test(full(rec + 2), par(rec + 2));
+            else if (i + 1 < cnt)
+                mbar_wait(full(rec + 1), par(rec + 1));
+            ld_lower<K, lower3, TWO>(nxo, R.stage((rec + 1) % D), L, lane);  // unused past the sweep
+        } else {
+            ld_nbr(i + 1 < cnt ? i + 1 : cnt - 1);
+            mbar_wait(full(rec), par(rec));
+            ld_lower<K, lower3, TWO>(cur, R.stage(st), L, lane);
+            fin_lower<K, lower3, TWO>(cur, lane, v1, v1t, v2, v2t);
         }
-        const int st = rec % D;
-        TSTAMP(q1);
-        mbar_wait(&R.full[st], (rec / D) & 1);
         TSTAMP(q2);
         TACC(0, q1, q2);
-        const double *sg = R.stage(st);
-        double aL[K], aU[K], rhs[K], rhst;
-        ld_rec(sg + gL, L, aL);
-        ld_rec(sg + gU, L, aU);
-        const double nlt = sg[o_nl(K) + L.tw], nut = sg[o_nu(K) + L.tw];
-        if (lower3) {
-            ld_rec(sg + rx_of(K), L, rhs, rhst);
-            sub_mul(rhs, rhst, sg + rs1_of(K), L, v1, v1t);
-            if (TWO) sub_mul(rhs, rhst, sg + rs2_of(K), L, v2, v2t);
-        } else {
-            double c[K], ct;
-            ld_rec(sg + rs1_of(K), L, c, ct);
+        double rhs[K], rhst = cur.ptt - cur.cpt * xprevt;  // line 0: xprev = 0
 #pragma unroll
-            for (int k = 0; k < K; k++) rhs[k] = c[k] * v1[k];
-            rhst = ct * v1t;
-        }
-        sub_mul(rhs, rhst, sg + rs0_of(K), L, xprev, xprevt);  // line 0: xprev = 0
+        for (int k = 0; k < K; k++) rhs[k] = cur.pt[k] - cur.cp[k] * xprev[k];
         TSTAMP(q3);
         TACC(1, q2, q3);
         double x[K], xt;
-        const LinePrep PP = read_prep<K>(sg + o_prep(K), lane, aL, aU);
-        line_solve4<K>(PP, nx, t, aL, rhs, aU, rhst, nlt, nut, x, xt);
+        line_solve4<K>(cur.P, nx, t, cur.aL, rhs, cur.aU, rhst, cur.nlt, cur.nut, x, xt);
         TSTAMP(q4);
         TACC(2, q3, q4);
-        mbar_arrive(&R.empty[st]);
+        mbar_arrive(&R.empty[st]);  // every operand of stage st has been consumed
         st_rec(xlow + Q.qlow(i) * LR, L, x, xt);
-        TSTAMP(q5);
-        TACC(3, q4, q5);
 #pragma unroll
         for (int k = 0; k < K; k++) xprev[k] = x[k];
         xprevt = xt;
+        if (PIPE) {
+            fin_lower<K, lower3, TWO>(nxo, lane, v1, v1t, v2, v2t);
+            if (WAIT_AHEAD && i + 2 < cnt && !ok2) mbar_wait(full(rec + 2), par(rec + 2));
+            cur = nxo;
+        }
+        TSTAMP(q5);
+        TACC(3, q4, q5);
     }
     // ---------------- exchange the lines next to the twist
     const int stride = 32 * K + 1;
@@ -479,7 +650,17 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
     // ---------------- twist line (ntd_solve.py:172-177), direct loads after
     // the barrier (the neighbour plane's twist line was written by warp 0)
     double xn[K], xnt;
-    double yv[K], yvt = 0.0;
+    // lower-sweep value of the next upper-sweep line, one line ahead: line 0's
+    // is the last lower-sweep x
+    double ya[K], yat = xprevt;
+#pragma unroll
+    for (int k = 0; k < K; k++) ya[k] = xprev[k];
+    if (PIPE && cnt > 0) {  // first upper-sweep records: loads overlap the twist line
+        mbar_wait(full(rec), par(rec));
+        ld_upper<K, lower3>(cur, R.stage(rec % D), L, lane);
+        fin_prep(cur, lane);
+        if (WAIT_AHEAD && cnt > 1) mbar_wait(full(rec + 1), par(rec + 1));
+    }
     {
         const int q = t2;
         double aL[K], aU[K], rhs[K], rhst;
@@ -508,7 +689,6 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
         }
         if (t2 > 0) sub_mul(rhs, rhst, srec(o_l2(K), q), L, xa, xat);
         if (t2 < ny - 1) sub_mul(rhs, rhst, srec(o_u2(K), q), L, xd, xdt);
-        if (cnt > 0) ld_rec(xlow + Q.qup(0) * LR, L, yv, yvt);  // first upper line's lower value
         const LinePrep PP = line_prep<K>(lane & 15, aL, aU);
         line_solve4<K>(PP, nx, t, aL, rhs, aU, rhst, nlt, nut, xn, xnt);
         if (w2 == 0) {
@@ -524,40 +704,52 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
         }
     }
     // ---------------- level-2 upper sweep (ntd_solve.py:178-185)
-    for (int i = 0; i < cnt; i++, rec++) {
-        double y[K], yt = yvt;
-#pragma unroll
-        for (int k = 0; k < K; k++) y[k] = yv[k];
-        if (i + 1 < cnt) ld_rec(xlow + Q.qup(i + 1) * LR, L, yv, yvt);
+    auto ustep = [&](int i, double (&yb_)[K], double &ybt_) {
         const int st = rec % D;
-        mbar_wait(&R.full[st], (rec / D) & 1);
-        const double *sg = R.stage(st);
-        double aL[K], aU[K], cp[K], cpt;
-        ld_rec(sg + gL, L, aL);
-        ld_rec(sg + gU, L, aU);
-        const double nlt = sg[o_nl(K) + L.tw], nut = sg[o_nu(K) + L.tw];
-        ld_rec(sg + rs0_of(K), L, cp, cpt);
-        double xo[K], xot = 0.0;
-        if (!lower3) ld_rec(sg + rx_of(K), L, xo, xot);
+        double y[K], yt = ybt_;
+#pragma unroll
+        for (int k = 0; k < K; k++) y[k] = yb_[k];
+        ld_rec(xlow + Q.qup(i + 1 < cnt ? i + 1 : i) * LR, L, yb_, ybt_);  // line i+1 (unconditional)
+        LineOps<K> nxo;
+        bool ok2 = true;
+        if (PIPE) {
+            if (WAIT_AHEAD)
+                ok2 = mbar_test(full(rec + 2), par(rec + 2));
+            else if (i + 1 < cnt)
+                mbar_wait(full(rec + 1), par(rec + 1));
+            ld_upper<K, lower3>(nxo, R.stage((rec + 1) % D), L, lane);  // unused past the sweep
+        } else {
+            mbar_wait(full(rec), par(rec));
+            ld_upper<K, lower3>(cur, R.stage(st), L, lane);
+            fin_prep(cur, lane);
+        }
         double bs[K];
 #pragma unroll
-        for (int k = 0; k < K; k++) bs[k] = cp[k] * xn[k];
+        for (int k = 0; k < K; k++) bs[k] = cur.cp[k] * xn[k];
         double xs[K], xst;
-        const LinePrep PP = read_prep<K>(sg + o_prep(K), lane, aL, aU);
-        line_solve4<K>(PP, nx, t, aL, bs, aU, cpt * xnt, nlt, nut, xs, xst);
-        mbar_arrive(&R.empty[st]);
+        line_solve4<K>(cur.P, nx, t, cur.aL, bs, cur.aU, cur.cpt * xnt, cur.nlt, cur.nut, xs, xst);
 #pragma unroll
         for (int k = 0; k < K; k++) xn[k] = y[k] - xs[k];
         xnt = yt - xst;
-        if (!lower3) {
-            double nv[K];
+        double nv[K], nvt = xnt;
 #pragma unroll
-            for (int k = 0; k < K; k++) nv[k] = xo[k] - xn[k];
-            st_rec(xpl + Q.qup(i) * LR, L, nv, xot - xnt);
-        } else {
-            st_rec(xpl + Q.qup(i) * LR, L, xn, xnt);
+        for (int k = 0; k < K; k++) nv[k] = xn[k];
+        if (!lower3) {
+#pragma unroll
+            for (int k = 0; k < K; k++) nv[k] = cur.pt[k] - xn[k];
+            nvt = cur.ptt - xnt;
         }
-    }
+        mbar_arrive(&R.empty[st]);
+        st_rec(xpl + Q.qup(i) * LR, L, nv, nvt);
+        if (PIPE) {
+            fin_prep(nxo, lane);
+            if (WAIT_AHEAD && i + 2 < cnt && !ok2) mbar_wait(full(rec + 2), par(rec + 2));
+            cur = nxo;
+        }
+        rec++;
+    };
+#pragma unroll 2  // ping-pong registers: no copies of in-flight loads
+    for (int i = 0; i < cnt; i++) ustep(i, ya, yat);
 }
 
 template <int K, int D>
@@ -603,62 +795,66 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
     double *myex = ex[pair];
     int parity = 0;
     const int t3 = (nz - 1) / 2;
-    // level-3 lower sweep (ntd_solve.py:198-221)
+    // The warp pair's plane schedule: level-3 lower sweep (ntd_solve.py:198-221),
+    // the twist plane for pair 0 (222-232), level-3 upper sweep (233-253).
     const int nlow = pair == 0 ? t3 : nz - 1 - t3;
-    for (int i = 0; i < nlow; i++) {
-        const int p = pair == 0 ? i : nz - 1 - i;
+    const int ntw = pair == 0 ? 1 : 0;
+    auto desc = [&](int idx) {
         PlaneDesc P;
-        P.prec = (i64)p * ny;
-        P.mode = M_LOWER3;
         P.two = false;
-        P.hasM = pair == 0 && p > 0;
-        P.hasP = pair == 1 && p < nz - 1;
-        P.nbrUp = false;
-        P.up = pair == 1;
-        P.c1 = P.up ? o_u3(K) : o_l3(K);
-        if (producer) {
-            produce_plane<K, D>(S, P, Q, R, rec);
+        P.hasM = P.hasP = P.nbrUp = P.up = false;
+        if (idx < nlow) {
+            const int p = pair == 0 ? idx : nz - 1 - idx;
+            P.prec = (i64)p * ny;
+            P.mode = M_LOWER3;
+            P.hasM = pair == 0 && p > 0;
+            P.hasP = pair == 1 && p < nz - 1;
+            P.up = pair == 1;
+            P.c1 = P.up ? o_u3(K) : o_l3(K);
+        } else if (idx < nlow + ntw) {
+            P.prec = (i64)t3 * ny;
+            P.mode = M_LOWER3;
+            P.two = true;
+            P.hasM = t3 > 0;
+            P.hasP = t3 < nz - 1;
+            P.c1 = o_l3(K);  // L3 then U3 (contiguous)
         } else {
-            solve_plane<K, D, M_LOWER3, false>(S, P, Q, nx, bar, myex, parity, R, L, rec);
+            const int u = idx - nlow - ntw;
+            const int p = pair == 0 ? t3 - 1 - u : t3 + 1 + u;
+            P.prec = (i64)p * ny;
+            P.mode = M_UPPER3;
+            P.nbrUp = pair == 0;
+            P.c1 = P.nbrUp ? o_u3(K) : o_l3(K);
         }
+        return P;
+    };
+    const int nplanes = 2 * nlow + ntw;
+    auto produce = [&](int idx) {
+        const PlaneDesc P = desc(idx), Pn = desc(idx + 1);
+        produce_plane<K, D>(S, P, idx + 1 < nplanes ? &Pn : nullptr, Q, R, rec);
+    };
+    for (int i = 0; i < nlow; i++) {
+        if (producer)
+            produce(i);
+        else
+            solve_plane<K, D, M_LOWER3, false>(S, desc(i), Q, nx, bar, myex, parity, R, L, rec);
     }
     __syncthreads();
-    // twist plane (ntd_solve.py:222-232): pair 0, both level-3 neighbours
     if (pair == 0) {
-        PlaneDesc P;
-        P.prec = (i64)t3 * ny;
-        P.mode = M_LOWER3;
-        P.two = true;
-        P.hasM = t3 > 0;
-        P.hasP = t3 < nz - 1;
-        P.nbrUp = false;
-        P.up = false;
-        P.c1 = o_l3(K);  // L3 then U3 (contiguous)
         if (producer) {
             fence_proxy_async();
-            produce_plane<K, D>(S, P, Q, R, rec);
+            produce(nlow);
         } else {
-            solve_plane<K, D, M_LOWER3, true>(S, P, Q, nx, bar, myex, parity, R, L, rec);
+            solve_plane<K, D, M_LOWER3, true>(S, desc(nlow), Q, nx, bar, myex, parity, R, L, rec);
         }
     }
     __syncthreads();
     if (producer) fence_proxy_async();  // x (read as xo) was written by generic stores
-    // level-3 upper sweep (ntd_solve.py:233-253)
-    for (int i = 0; i < nlow; i++) {
-        const int p = pair == 0 ? t3 - 1 - i : t3 + 1 + i;
-        PlaneDesc P;
-        P.prec = (i64)p * ny;
-        P.mode = M_UPPER3;
-        P.two = false;
-        P.hasM = P.hasP = false;
-        P.nbrUp = pair == 0;
-        P.up = false;
-        P.c1 = P.nbrUp ? o_u3(K) : o_l3(K);
-        if (producer) {
-            produce_plane<K, D>(S, P, Q, R, rec);
-        } else {
-            solve_plane<K, D, M_UPPER3, false>(S, P, Q, nx, bar, myex, parity, R, L, rec);
-        }
+    for (int i = nlow + ntw; i < nplanes; i++) {
+        if (producer)
+            produce(i);
+        else
+            solve_plane<K, D, M_UPPER3, false>(S, desc(i), Q, nx, bar, myex, parity, R, L, rec);
     }
 }
 
@@ -668,7 +864,7 @@ template <int K>
 int launch_prep_sl_k(double *solve, i64 lines_total, cudaStream_t st);
 template <int K>
 int launch_apply_sl_k(const double *solve, const double *bsl, double *xsl, double *xssl, const double *zpl, int nx,
-                      int ny, int nz, i64 batch, const int32_t *active, cudaStream_t st, int depth);
+                      int ny, int nz, i64 batch, const int32_t *active, cudaStream_t st);
 
 #define NTD_INSTANTIATE_SL(K)                                                                                     \
     template <>                                                                                                    \
@@ -680,19 +876,16 @@ int launch_apply_sl_k(const double *solve, const double *bsl, double *xsl, doubl
     }                                                                                                              \
     template <>                                                                                                    \
     int launch_apply_sl_k<K>(const double *solve, const double *bsl, double *xsl, double *xssl, const double *zpl,   \
-                             int nx, int ny, int nz, i64 batch, const int32_t *active, cudaStream_t st, int depth)  \
+                             int nx, int ny, int nz, i64 batch, const int32_t *active, cudaStream_t st)            \
     {                                                                                                              \
-        size_t smem = (size_t)4 * depth * sl::stage_of(K) * 8;                                                     \
-        cudaError_t e = depth == 4                                                                                 \
-            ? cudaFuncSetAttribute(sl::k_apply<K, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)      \
-            : cudaFuncSetAttribute(sl::k_apply<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+        constexpr int D = sl::depth_of(K);                                                                         \
+        const size_t smem = (size_t)4 * D * sl::stage_of(K) * 8;                                                   \
+        cudaError_t e = cudaFuncSetAttribute(sl::k_apply<K, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                             (int)smem);                                                           \
         if (e != cudaSuccess) {                                                                                    \
             ntd::set_error("ntd_apply smem", e);                                                                   \
             return NTD_ELAUNCH;                                                                                    \
         }                                                                                                          \
-        if (depth == 4)                                                                                            \
-            sl::k_apply<K, 4><<<(unsigned)batch, 256, smem, st>>>(solve, bsl, xsl, xssl, zpl, nx, ny, nz, active);      \
-        else                                                                                                       \
-            sl::k_apply<K, 2><<<(unsigned)batch, 256, smem, st>>>(solve, bsl, xsl, xssl, zpl, nx, ny, nz, active);      \
+        sl::k_apply<K, D><<<(unsigned)batch, 256, smem, st>>>(solve, bsl, xsl, xssl, zpl, nx, ny, nz, active);     \
         return ntd::check_launch("ntd_apply");                                                                     \
     }
