@@ -232,6 +232,8 @@ def run_ntd(args):
     # ---- device-timed steps (inputs resident)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     _lib.reset_launch_count()
+    for grp in solver.groups:
+        grp.precond.ntd_events = []
     with ClockSampler(local) as clk:
         barrier()
         ev[0].record()
@@ -242,6 +244,10 @@ def run_ntd(args):
         ev[1].record()
         barrier()
     launches = _lib.launch_count()
+    for grp in solver.groups:
+        evs_keep = grp.precond.ntd_events
+        grp.precond.ntd_events = None
+        grp.precond.ntd_events_timed = evs_keep
     t_dev = ev[0].elapsed_time(ev[1]) / 1e3
     # ---- e2e through the public API with host buffers
     ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -256,31 +262,33 @@ def run_ntd(args):
     ev2[1].record()
     barrier()
     t_e2e = ev2[0].elapsed_time(ev2[1]) / 1e3
-    # ---- dominant kernel: batched NTD apply, CUDA events on its stream
-    v = torch.rand_like(b_dev)
+    # ---- dominant kernel: the NTD apply launches of the timed region
+    # (CUDA events recorded on each group's stream around every apply)
+    evs = [e for grp in solver.groups for e in grp.precond.ntd_events_timed]
+    torch.cuda.synchronize()
+    t_apply_sum = float(np.sum([a.elapsed_time(b) for a, b in evs])) / 1e3
+    t_apply = t_apply_sum / max(1, len(evs))
+    # algorithmic bytes of the timed applies: each system is preconditioned
+    # once per PCG iteration it takes (masked systems do no work)
+    apply_gbs = NTD_APPLY_BYTES_PER_UNKNOWN * work_local / t_apply_sum / 1e9
+    g0 = solver.groups[0]
+    Bg = g0.hi - g0.lo  # systems per NTD launch
+    # standalone context timings for one group's launch (ILU0 apply, spmv)
+    P = g0.precond
+    v = torch.rand((Bg, n), dtype=torch.float64, device="cuda")
     xa = torch.empty_like(v)
-    wk = torch.empty(3 * B * n, dtype=torch.float64, device="cuda")
     R = 5
     for _ in range(2):
-        D.ntd_apply(solver.precond.pre, v, nx, ny, nz, B, x=xa, work=wk, solve=solver.precond.solve)
-    e3 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    e3[0].record()
-    for _ in range(R):
-        D.ntd_apply(solver.precond.pre, v, nx, ny, nz, B, x=xa, work=wk, solve=solver.precond.solve)
-    e3[1].record()
-    torch.cuda.synchronize()
-    t_apply = e3[0].elapsed_time(e3[1]) / 1e3 / R
-    # ILU0 apply and spmv for context
+        D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, Bg, z=xa, skew=P.skew, work=P.skew_work)
     e4 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     e4[0].record()
     for _ in range(R):
-        D.ilu0_apply(solver.precond.ilu, solver.precond.split, v, nx, ny, nz, B, z=xa, skew=solver.precond.skew,
-                     work=solver.precond.skew_work)
+        D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, Bg, z=xa, skew=P.skew, work=P.skew_work)
     e4[1].record()
     e5 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     e5[0].record()
     for _ in range(R):
-        _lib.call("ntd_spmv", _lib.ptr(a_dev), _lib.ptr(v), _lib.ptr(xa), nx, ny, nz, B, None, _lib.stream())
+        _lib.call("ntd_spmv", _lib.ptr(g0.a), _lib.ptr(v), _lib.ptr(xa), nx, ny, nz, Bg, None, _lib.stream())
     e5[1].record()
     torch.cuda.synchronize()
     t_ilu = e4[0].elapsed_time(e4[1]) / 1e3 / R
@@ -289,13 +297,14 @@ def run_ntd(args):
     # ---- reductions over ranks (NCCL: max of timings, sum of work, one all_gather of stats)
     from paper_1909_09771_b200 import dist as pdist
     dev = torch.device("cuda", local)
-    times = pdist.reduce_max([t_dev, t_e2e, t_apply, t_ilu, t_spmv, setup_s], dev)
+    times = pdist.reduce_max([t_dev, t_e2e, t_apply, t_ilu, t_spmv, setup_s, -apply_gbs], dev)
     work = pdist.reduce_sum([work_local, work_e2e, launches], dev)
     stats = pdist.gather_stats([[s, it, int(cv), rr] for s, it, cv, rr in
                                 zip(mine, res.iterations, res.converged, res.final_relres)], n_total, dev)
     stats = stats.cpu().numpy()
     if rank == 0:
-        t_dev, t_e2e, t_apply, t_ilu, t_spmv, setup_s = times
+        t_dev, t_e2e, t_apply, t_ilu, t_spmv, setup_s, apply_gbs = times
+        apply_gbs = -apply_gbs  # min over ranks
         value = work[0] / t_dev / 1e6
         e2e = work[1] / t_e2e / 1e6
         iters = [int(v) for v in stats[:, 1]]
@@ -303,8 +312,7 @@ def run_ntd(args):
         ref_match = None
         if cfg == 4:
             ref_match = sum(abs(it - CFG4_REF_ITERS[s]) <= 1 for s, it in zip(sys_ids, iters))
-        apply_bytes = NTD_APPLY_BYTES_PER_UNKNOWN * n * B  # per launch on this rank
-        achieved = apply_bytes / t_apply / 1e9
+        achieved = apply_gbs
         peak = _measured_peak()
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -313,15 +321,18 @@ def run_ntd(args):
             "data": "synthetic (seeded BASELINE config recipe, SURVEY.md 8(d))",
             "config": {"workload": f"cfg{cfg}", "systems": n_total, "grid": f"{nx}x{ny}x{nz}",
                        "precond": "ntd+ilu0", "tol": args.tol, "parallelism": f"batch-shard x{world}",
+                       "stream_groups": len(solver.groups), "systems_per_ntd_launch": Bg,
                        "l2": "inputs larger than L2 (each batch vector %.0f MB)" % (8 * n * B / 1e6)},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n * B * world,
                     "d2h_bytes_per_step": 8 * n * B * world},
-            "roofline": {"kernel": "ntd_apply (batched, rank 0 shard)", "bound": "hbm",
+            "roofline": {"kernel": "ntd_apply entry (to_sl + sl::k_apply + from_sl), timed-region launches, rank 0",
+                         "bound": "hbm",
                          "achieved": achieved, "peak": peak[0], "unit": "GB/s", "frac": achieved / peak[0],
-                         "peak_source": peak[1], "traffic": _traffic(cfg, B),
+                         "peak_source": peak[1], "traffic": _traffic(cfg, Bg),
                          "traffic_unit": "bytes per launch (ncu dram read+write)",
                          "bytes_per_unknown": NTD_APPLY_BYTES_PER_UNKNOWN, "apply_ms": 1e3 * t_apply,
-                         "apply_munknowns_per_s": n * B / t_apply / 1e6},
+                         "apply_munknowns_per_s": n * Bg / t_apply / 1e6,
+                         "launches_timed": len(evs)},
             "kernels_ms": {"ntd_apply": 1e3 * t_apply, "ilu0_apply": 1e3 * t_ilu, "spmv": 1e3 * t_spmv},
             "setup_seconds": setup_s,
             "iterations": {"min": min(iters), "max": max(iters), "mean": float(np.mean(iters)),

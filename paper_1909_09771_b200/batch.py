@@ -7,6 +7,7 @@ no batch API: it runs one process per system.  ``build_precond`` mirrors the
 reference CLI's string-keyed factory (bench_cli.py:113-142).
 """
 
+import os
 from dataclasses import dataclass
 from time import perf_counter
 
@@ -82,10 +83,41 @@ class BatchResult:
     solve_seconds: float
 
 
-class BatchSolver:
-    """B independent systems (B, 7, N) on one grid shape, ntd+ilu0 PCG."""
+def default_groups(batch):
+    """Stream groups for a batch: the NTD apply and the ILU0 sweeps are
+    latency-bound (one CTA per system / half), so while one group sweeps, the
+    bandwidth-bound stencil/CG kernels of the other run on the idle SMs."""
+    env = os.environ.get("NTD_STREAM_GROUPS")
+    if env:
+        return max(1, min(int(env), batch))
+    return max(1, min(4, batch // 4))
 
-    def __init__(self, a_dev, nx, ny, nz, kind="ntd+ilu0", max_iters=200):
+
+class _Group:
+    """One slice [lo, hi) of the batch: its own factors, PCG state and stream."""
+
+    def __init__(self, a, lo, hi, nx, ny, nz, max_iters, x_view, stream):
+        self.lo, self.hi = lo, hi
+        self.a = a[lo:hi]
+        self.stream = stream
+        self.pcg = D.PcgDevice(self.a, nx, ny, nz, hi - lo, max_iters, x=x_view)
+        self.precond = None
+        self.flags_host = [torch.zeros((hi - lo, _lib.NTD_FL["N"]), dtype=torch.int32).pin_memory()
+                           for _ in range(2)]
+        self.events = [torch.cuda.Event() for _ in range(2)]
+
+
+class BatchSolver:
+    """B independent systems (B, 7, N) on one grid shape, ntd+ilu0 PCG.
+
+    The batch is split into `groups` slices, each enqueued on its own CUDA
+    stream, so the latency-bound sweeps of one slice overlap the
+    bandwidth-bound kernels of another.  The host never blocks inside the
+    iteration loop: convergence flags are copied asynchronously and checked
+    one iteration late (converged systems are masked on the device, so the
+    extra enqueued iteration does no work for them)."""
+
+    def __init__(self, a_dev, nx, ny, nz, kind="ntd+ilu0", max_iters=200, groups=None):
         if kind not in ("ntd+ilu0", "none"):
             raise ValueError("BatchSolver supports 'ntd+ilu0' and 'none'")
         self.a = as_device(a_dev)
@@ -96,9 +128,21 @@ class BatchSolver:
             raise ValueError("a_dev must have shape (B, 7, nx*ny*nz)")
         self.kind = kind
         self.max_iters = max_iters
-        self.precond = None
         self.setup_seconds = 0.0
-        self.pcg = D.PcgDevice(self.a, nx, ny, nz, self.batch, max_iters)
+        G = default_groups(self.batch) if groups is None else max(1, min(int(groups), self.batch))
+        self.x = torch.empty((self.batch, self.n), dtype=torch.float64, device=self.a.device)
+        self.history = torch.zeros((self.batch, max(1, max_iters)), dtype=torch.float64, device=self.a.device)
+        bounds = [self.batch * g // G for g in range(G + 1)]
+        self.groups = []
+        for g in range(G):
+            lo, hi = bounds[g], bounds[g + 1]
+            st = torch.cuda.current_stream() if G == 1 else torch.cuda.Stream()
+            self.groups.append(_Group(self.a, lo, hi, nx, ny, nz, max_iters, self.x[lo:hi], st))
+
+    @property
+    def precond(self):
+        """The first group's preconditioner (all of it when groups == 1)."""
+        return self.groups[0].precond
 
     def setup(self):
         """Both factorisations for all systems (CombinedPrecond.__init__,
@@ -107,37 +151,88 @@ class BatchSolver:
             return self
         torch.cuda.synchronize()
         t0 = perf_counter()
-        g = (self.nx, self.ny, self.nz, self.batch)
-        pre, st = D.ntd_factor(self.a, *g)
-        bad = [(s, *map(int, st[s])) for s in range(self.batch) if int(st[s, 0])]
-        if bad:
-            s, code, plane, row = bad[0]
-            raise FactorizationError(f"system {s}: " + D.ntd_factor_message(code, plane, row))
         if not D.check_grid_pattern(self.a, self.nx, self.ny, self.nz):
             raise ValueError("band entries coupling across a grid line/plane boundary must be zero")
-        split = self.n // 2
-        f, st2 = D.ilu0_factor(self.a, *g, split)
-        bad = [s for s in range(self.batch) if int(st2[s, 0])]
-        if bad:
-            raise FactorizationError(f"system {bad[0]}: zero or non-finite pivot at row {int(st2[bad[0], 2])}")
-        self.precond = D.CombinedDevice(self.a, *g, pre=pre, ilu=f, split=split)
+        for grp in self.groups:
+            B = grp.hi - grp.lo
+            g = (self.nx, self.ny, self.nz, B)
+            pre, st = D.ntd_factor(grp.a, *g)
+            bad = [(s, *map(int, st[s])) for s in range(B) if int(st[s, 0])]
+            if bad:
+                s, code, plane, row = bad[0]
+                raise FactorizationError(f"system {grp.lo + s}: " + D.ntd_factor_message(code, plane, row))
+            split = self.n // 2
+            f, st2 = D.ilu0_factor(grp.a, *g, split)
+            bad = [s for s in range(B) if int(st2[s, 0])]
+            if bad:
+                raise FactorizationError(f"system {grp.lo + bad[0]}: zero or non-finite pivot at row "
+                                         f"{int(st2[bad[0], 2])}")
+            grp.precond = D.CombinedDevice(grp.a, *g, pre=pre, ilu=f, split=split)
         torch.cuda.synchronize()
         self.setup_seconds = perf_counter() - t0
         return self
 
     def solve(self, b_dev, tol=1e-8):
         b = as_device(b_dev).reshape(self.batch, self.n)
-        torch.cuda.synchronize()
+        cur = torch.cuda.current_stream()
         t0 = perf_counter()
-        papply = None if self.precond is None else self.precond.apply
-        self.pcg.solve(b, tol, papply, None)
-        fl, st = self.pcg.read_flags()
+        for grp in self.groups:
+            grp.stream.wait_stream(cur)  # b may have been produced on the caller's stream
+        self._run(b, tol)
+        for grp in self.groups:
+            cur.wait_stream(grp.stream)
+        fl = torch.cat([grp.pcg.flags for grp in self.groups]).cpu()
+        st = torch.cat([grp.pcg.state for grp in self.groups]).cpu()
+        for grp in self.groups:
+            self.history[grp.lo:grp.hi] = grp.pcg.history
         dt = perf_counter() - t0
-        fl = fl.clone()
-        st = st.clone()
         return BatchResult(
-            x=self.pcg.x, iterations=[int(v) for v in fl[:, _lib.NTD_FL["ITERS"]]],
+            x=self.x, iterations=[int(v) for v in fl[:, _lib.NTD_FL["ITERS"]]],
             converged=[int(v) == _lib.PCG_CONVERGED for v in fl[:, _lib.NTD_FL["STATUS"]]],
             final_relres=[float(v) for v in st[:, _lib.NTD_ST["RELRES"]]],
             status=[int(v) for v in fl[:, _lib.NTD_FL["STATUS"]]],
-            history=self.pcg.history, setup_seconds=self.setup_seconds, solve_seconds=dt)
+            history=self.history, setup_seconds=self.setup_seconds, solve_seconds=dt)
+
+    def _flags_async(self, slot):
+        for grp in self.groups:
+            with torch.cuda.stream(grp.stream):
+                grp.flags_host[slot].copy_(grp.pcg.flags, non_blocking=True)
+                grp.events[slot].record(grp.stream)
+
+    def _any_active(self, slot):
+        act = _lib.NTD_FL["ACTIVE"]
+        alive = False
+        for grp in self.groups:
+            grp.events[slot].synchronize()
+            alive = alive or bool(grp.flags_host[slot][:, act].any())
+        return alive
+
+    def _run(self, b, tol):
+        """PCG (precond_pcg.py:84-119) on every group, enqueued round-robin.
+        Iteration it's update is enqueued before the host looks at the flags
+        of iteration it-1, so the GPU always has queued work."""
+        groups = self.groups
+        for grp in groups:
+            with torch.cuda.stream(grp.stream):
+                grp.pcg.init(b[grp.lo:grp.hi], tol)
+        self._flags_async(0)
+        for grp in groups:
+            with torch.cuda.stream(grp.stream):
+                z = grp.pcg.r if grp.precond is None else grp.precond.apply(grp.pcg.r, grp.pcg.z, grp.pcg.active)
+                grp.pcg.start(z)
+        if not self._any_active(0):
+            return
+        for it in range(1, self.max_iters + 1):
+            for grp in groups:
+                with torch.cuda.stream(grp.stream):
+                    grp.pcg.step_update()
+            self._flags_async(it % 2)
+            if it >= 2 and not self._any_active((it - 1) % 2):
+                break  # everything had converged at it-1; iteration it was fully masked
+            if it == self.max_iters:
+                break
+            for grp in groups:
+                with torch.cuda.stream(grp.stream):
+                    z = grp.pcg.r if grp.precond is None else grp.precond.apply(grp.pcg.r, grp.pcg.z,
+                                                                                  grp.pcg.active)
+                    grp.pcg.direction(z)

@@ -142,6 +142,7 @@ class CombinedDevice:
         self.xn = torch.empty(shape, dtype=torch.float64, device=_dev())
         self.work = torch.empty(_lib.load().ntd_apply_work_doubles(nx, ny, nz, batch), dtype=torch.float64,
                                 device=_dev())
+        self.ntd_events = None  # list: (start, end) CUDA events around every NTD apply (bench timing)
 
     def apply(self, r, z, active=None):
         """z = M^{-1} r:  w = ilu(r); t = r - A w; z = ntd(t) + w;
@@ -152,7 +153,13 @@ class CombinedDevice:
                                          device=_dev())
         ilu0_apply(self.ilu, self.split, r, *g, z=self.w, active=active, skew=self.skew, work=self.skew_work)
         residual(self.a, r, self.w, *g, t=self.t, active=active)
+        if self.ntd_events is not None:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
         ntd_apply(self.pre, self.t, *g, x=self.xn, work=self.work, active=active, solve=self.solve)
+        if self.ntd_events is not None:
+            ev[1].record()
+            self.ntd_events.append(ev)
         residual(self.a, r, self.w, *g, t=self.t, v=self.xn, z_out=z, active=active)
         if self.skew is not None:
             ilu0_apply(self.ilu, self.split, self.t, *g, z=None, acc=z, active=active, skew=self.skew,
@@ -169,7 +176,7 @@ class PcgDevice:
     device; one small device->host read of the flags per iteration decides
     whether to continue.  Converged systems are masked out of every kernel."""
 
-    def __init__(self, a_dev, nx, ny, nz, batch, max_iters):
+    def __init__(self, a_dev, nx, ny, nz, batch, max_iters, x=None):
         lib = _lib.load()
         self.a, self.nx, self.ny, self.nz, self.batch = a_dev, nx, ny, nz, batch
         n = nx * ny * nz
@@ -177,7 +184,7 @@ class PcgDevice:
         self.max_iters = max_iters
         dev = _dev()
         shape = (batch, n)
-        self.x = torch.empty(shape, dtype=torch.float64, device=dev)
+        self.x = torch.empty(shape, dtype=torch.float64, device=dev) if x is None else x
         self.r = torch.empty(shape, dtype=torch.float64, device=dev)
         self.z = torch.empty(shape, dtype=torch.float64, device=dev)
         self.p = torch.empty(shape, dtype=torch.float64, device=dev)

@@ -20,7 +20,7 @@ a = torch.from_numpy(np.stack([i[0] for i in ins])).cuda()
 xt = torch.from_numpy(np.stack([i[1] for i in ins])).cuda()
 b = torch.empty_like(xt)
 _lib.call("ntd_spmv", _lib.ptr(a), _lib.ptr(xt), _lib.ptr(b), nx, ny, nz, B, None, _lib.stream())
-s = BatchSolver(a, nx, ny, nz).setup()
+s = BatchSolver(a, nx, ny, nz, groups=1).setup()
 v = torch.rand_like(b)
 x = torch.empty_like(b)
 for _ in range(2):
