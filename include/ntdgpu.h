@@ -62,6 +62,21 @@ int ntd_residual(const double *a, const double *r, const double *w,
                  int64_t ny, int64_t nz, int64_t batch, const int32_t *active,
                  void *stream);
 
+/* Symmetric packed operator for the PCG-side stencil kernels.  a4 (B,4,N)
+ * receives the bands 0,+1,+nx,+nxy of a; sym_ok[s] (int32, set to 1 by the
+ * caller) is cleared when any mirrored pair A[r][r-d] / A[r-d][r] of system s
+ * differs bitwise.  For systems with sym_ok == 1 the *_sym entry points below
+ * read A[r][r-d] as A[r-d][r] and are bitwise equal to their 7-band forms
+ * (same summation order, banded_core.py:105-117) while moving 32 instead of
+ * 56 operator bytes per row.  The BASELINE operators (harmonic-mean faces,
+ * problem_gen.py:98) are bitwise symmetric. */
+int ntd_sym_pack(const double *a, double *a4, int32_t *sym_ok, int64_t nx,
+                 int64_t ny, int64_t nz, int64_t batch, void *stream);
+int ntd_residual_sym(const double *a4, const double *r, const double *w,
+                     const double *v, double *z_out, double *t, int64_t nx,
+                     int64_t ny, int64_t nz, int64_t batch,
+                     const int32_t *active, void *stream);
+
 /* out[s] = x_s . y_s (banded_core.py:133-136 dot / 146-147 norm2 when x==y,
  * fixed-order tree reduction).  work: >= ntd_dot_work_doubles(batch).  If
  * sqrt_out != 0 the square root is stored (norm2). */
@@ -103,6 +118,18 @@ int ntd_pcg_update_residual(const double *a, const double *b, double *x,
                             double *history, int64_t max_iters, int64_t nx,
                             int64_t ny, int64_t nz, int64_t batch, double *work,
                             void *stream);
+/* The same two steps on the symmetric packed operator (see ntd_sym_pack). */
+int ntd_pcg_spmv_alpha_sym(const double *a4, const double *p, double *ap,
+                           double *state, int32_t *flags, int32_t *active,
+                           int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+                           double *work, void *stream);
+int ntd_pcg_update_residual_sym(const double *a4, const double *b, double *x,
+                                double *r, const double *p, const double *ap,
+                                double *state, int32_t *flags,
+                                int32_t *active, double *history,
+                                int64_t max_iters, int64_t nx, int64_t ny,
+                                int64_t nz, int64_t batch, double *work,
+                                void *stream);
 /* rz_new = r.z; beta = rz_new/rz; p = beta p + z (precond_pcg.py:116-119) */
 int ntd_pcg_direction(const double *r, const double *z, double *p,
                       double *state, const int32_t *active, int64_t n,

@@ -27,6 +27,8 @@ _SIGS = {
     "ntd_max_nx": (_I, []),
     "ntd_spmv": (_INT, [_P, _P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_residual": (_INT, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
+    "ntd_sym_pack": (_INT, [_P, _P, _P, _I, _I, _I, _I, _P]),
+    "ntd_residual_sym": (_INT, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_dot_work_doubles": (_I, [_I]),
     "ntd_dot": (_INT, [_P, _P, _P, _INT, _I, _I, _P, _P, _P]),
     "ntd_pcg_init": (_INT, [_P, _P, _P, _P, _P, _P, ctypes.c_double, _I, _I, _P, _P]),
@@ -34,6 +36,9 @@ _SIGS = {
     "ntd_pcg_spmv_alpha": (_INT, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_pcg_update_residual": (_INT, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I,
                                        _I, _P, _P]),
+    "ntd_pcg_spmv_alpha_sym": (_INT, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
+    "ntd_pcg_update_residual_sym": (_INT, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I,
+                                           _I, _P, _P]),
     "ntd_pcg_direction": (_INT, [_P, _P, _P, _P, _P, _I, _I, _P, _P]),
     "ntd_factor_work_doubles": (_I, [_I, _I, _I, _I]),
     "ntd_factor": (_INT, [_P, _P, _P, _P, _I, _I, _I, _I, _P]),
@@ -57,7 +62,8 @@ KERNELS_PER_CALL = {
     "ntd_spmv": 1, "ntd_residual": 1, "ntd_dot": 2, "ntd_pcg_init": 3, "ntd_pcg_start": 3,
     "ntd_pcg_spmv_alpha": 2, "ntd_pcg_update_residual": 3, "ntd_pcg_direction": 3, "ntd_factor": 1,
     "ntd_apply": 3, "ntd_solve_bands": 1, "ntd_ilu0_factor": 2, "ntd_ilu0_apply": 1, "ntd_ilu0_skew_build": 1,
-    "ntd_ilu0_skew_apply": 3,
+    "ntd_ilu0_skew_apply": 3, "ntd_sym_pack": 1, "ntd_residual_sym": 1, "ntd_pcg_spmv_alpha_sym": 2,
+    "ntd_pcg_update_residual_sym": 3,
 }
 _launches = [0]
 

@@ -100,7 +100,7 @@ class _Group:
         self.lo, self.hi = lo, hi
         self.a = a[lo:hi]
         self.stream = stream
-        self.pcg = D.PcgDevice(self.a, nx, ny, nz, hi - lo, max_iters, x=x_view)
+        self.pcg = D.PcgDevice(self.a, nx, ny, nz, hi - lo, max_iters, x=x_view, a4=None)
         self.precond = None
         self.flags_host = [torch.zeros((hi - lo, _lib.NTD_FL["N"]), dtype=torch.int32).pin_memory()
                            for _ in range(2)]
@@ -167,7 +167,9 @@ class BatchSolver:
             if bad:
                 raise FactorizationError(f"system {grp.lo + bad[0]}: zero or non-finite pivot at row "
                                          f"{int(st2[bad[0], 2])}")
-            grp.precond = D.CombinedDevice(grp.a, *g, pre=pre, ilu=f, split=split)
+            a4 = D.sym_pack(grp.a, *g)  # symmetric 4-band operator for the stencil kernels
+            grp.pcg.a4 = a4
+            grp.precond = D.CombinedDevice(grp.a, *g, pre=pre, ilu=f, split=split, a4=a4)
         torch.cuda.synchronize()
         self.setup_seconds = perf_counter() - t0
         return self

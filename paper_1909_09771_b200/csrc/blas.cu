@@ -46,6 +46,31 @@ __device__ __forceinline__ double spmv_row(const double *__restrict__ a, const d
     return s;
 }
 
+// The same row from the symmetric packed operator (4 bands: 0, +1, +nx, +nxy):
+// A[r][r-d] is read as A[r-d][r].  ntd_sym_pack only produces this layout when
+// every mirrored pair is bitwise equal, so the result is bitwise spmv_row's.
+__device__ __forceinline__ double spmv_row4(const double *__restrict__ a, const double *__restrict__ x,
+                                            i64 r, i64 n, i64 nx, i64 nxy)
+{
+    double s = mul_rn(a[r], x[r]);
+    if (r >= 1) s = add_rn(s, mul_rn(a[n + r - 1], x[r - 1]));
+    if (r >= nx) s = add_rn(s, mul_rn(a[2 * n + r - nx], x[r - nx]));
+    if (r >= nxy) s = add_rn(s, mul_rn(a[3 * n + r - nxy], x[r - nxy]));
+    if (r + 1 < n) s = add_rn(s, mul_rn(a[n + r], x[r + 1]));
+    if (r + nx < n) s = add_rn(s, mul_rn(a[2 * n + r], x[r + nx]));
+    if (r + nxy < n) s = add_rn(s, mul_rn(a[3 * n + r], x[r + nxy]));
+    return s;
+}
+template <int NB>
+__device__ __forceinline__ double row_of(const double *__restrict__ a, const double *__restrict__ x, i64 r, i64 n,
+                                         i64 nx, i64 nxy)
+{
+    if constexpr (NB == 4)
+        return spmv_row4(a, x, r, n, nx, nxy);
+    else
+        return spmv_row(a, x, r, n, nx, nxy);
+}
+
 // Block-level fixed-order tree reduction (deterministic).
 __device__ __forceinline__ double block_sum(double v, double *sh)
 {
@@ -95,6 +120,7 @@ extern "C" int ntd_spmv(const double *a, const double *x, double *y, int64_t nx,
 // ------------------------------------------------------------ residual
 // t = r - A(w [+ v]); optionally z_out = w + v.  numpy: `z = ntd(t); z += w`
 // gives z = v + w (elementwise add, commutative in IEEE) and `r - spmv(a, z)`.
+template <int NB>
 __global__ void __launch_bounds__(256) k_residual(const double *__restrict__ a, const double *__restrict__ r,
                                                   const double *__restrict__ w, const double *__restrict__ v,
                                                   double *__restrict__ z_out, double *__restrict__ t, i64 n,
@@ -102,13 +128,13 @@ __global__ void __launch_bounds__(256) k_residual(const double *__restrict__ a, 
 {
     i64 s = blockIdx.y;
     if (active && !active[s]) return;
-    const double *as = a + s * 7 * n;
+    const double *as = a + s * NB * n;
     const double *ws = w + s * n;
     const double *rs = r + s * n;
     double *ts = t + s * n;
     if (!v) {
         for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
-            ts[i] = sub_rn(rs[i], spmv_row(as, ws, i, n, nx, nxy));
+            ts[i] = sub_rn(rs[i], row_of<NB>(as, ws, i, n, nx, nxy));
         return;
     }
     const double *vs = v + s * n;
@@ -116,30 +142,83 @@ __global__ void __launch_bounds__(256) k_residual(const double *__restrict__ a, 
     for (i64 r0 = blockIdx.x * (i64)blockDim.x + threadIdx.x; r0 < n; r0 += (i64)gridDim.x * blockDim.x) {
         // spmv of z = v + w, z formed on the fly at the 7 taps (bitwise).
 #define ZV(idx) add_rn(vs[idx], ws[idx])
+        // band values: 7-band layout, or the mirrored upper band (NB == 4)
+        const double *d0 = as + (NB == 4 ? 0 : 3 * n);
+        const double *lm1 = NB == 4 ? as + n - 1 : as + 2 * n, *lmx = NB == 4 ? as + 2 * n - nx : as + n;
+        const double *lmz = NB == 4 ? as + 3 * n - nxy : as;
+        const double *up1 = as + (NB == 4 ? n : 4 * n), *upx = as + (NB == 4 ? 2 * n : 5 * n);
+        const double *upz = as + (NB == 4 ? 3 * n : 6 * n);
         double zc = ZV(r0);
-        double sacc = mul_rn(as[3 * n + r0], zc);
-        if (r0 >= 1) sacc = add_rn(sacc, mul_rn(as[2 * n + r0], ZV(r0 - 1)));
-        if (r0 >= nx) sacc = add_rn(sacc, mul_rn(as[n + r0], ZV(r0 - nx)));
-        if (r0 >= nxy) sacc = add_rn(sacc, mul_rn(as[r0], ZV(r0 - nxy)));
-        if (r0 + 1 < n) sacc = add_rn(sacc, mul_rn(as[4 * n + r0], ZV(r0 + 1)));
-        if (r0 + nx < n) sacc = add_rn(sacc, mul_rn(as[5 * n + r0], ZV(r0 + nx)));
-        if (r0 + nxy < n) sacc = add_rn(sacc, mul_rn(as[6 * n + r0], ZV(r0 + nxy)));
+        double sacc = mul_rn(d0[r0], zc);
+        if (r0 >= 1) sacc = add_rn(sacc, mul_rn(lm1[r0], ZV(r0 - 1)));
+        if (r0 >= nx) sacc = add_rn(sacc, mul_rn(lmx[r0], ZV(r0 - nx)));
+        if (r0 >= nxy) sacc = add_rn(sacc, mul_rn(lmz[r0], ZV(r0 - nxy)));
+        if (r0 + 1 < n) sacc = add_rn(sacc, mul_rn(up1[r0], ZV(r0 + 1)));
+        if (r0 + nx < n) sacc = add_rn(sacc, mul_rn(upx[r0], ZV(r0 + nx)));
+        if (r0 + nxy < n) sacc = add_rn(sacc, mul_rn(upz[r0], ZV(r0 + nxy)));
 #undef ZV
         ts[r0] = sub_rn(rs[r0], sacc);
         zs[r0] = zc;
     }
 }
 
-extern "C" int ntd_residual(const double *a, const double *r, const double *w, const double *v,
-                            double *z_out, double *t, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
-                            const int32_t *active, void *stream)
+template <int NB>
+static int residual_nb(const double *a, const double *r, const double *w, const double *v, double *z_out,
+                       double *t, int64_t nx, int64_t ny, int64_t nz, int64_t batch, const int32_t *active,
+                       void *stream)
 {
     if (!a || !r || !w || !t || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
     if ((v == nullptr) != (z_out == nullptr)) return NTD_EINVAL;
     i64 n = nx * ny * nz;
     dim3 grid(grid_rows(n), (unsigned)batch);
-    k_residual<<<grid, 256, 0, (cudaStream_t)stream>>>(a, r, w, v, z_out, t, n, nx, nx * ny, active);
+    k_residual<NB><<<grid, 256, 0, (cudaStream_t)stream>>>(a, r, w, v, z_out, t, n, nx, nx * ny, active);
     NTD_CHECK_LAUNCH("ntd_residual");
+}
+extern "C" int ntd_residual(const double *a, const double *r, const double *w, const double *v,
+                            double *z_out, double *t, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+                            const int32_t *active, void *stream)
+{
+    return residual_nb<7>(a, r, w, v, z_out, t, nx, ny, nz, batch, active, stream);
+}
+extern "C" int ntd_residual_sym(const double *a4, const double *r, const double *w, const double *v,
+                                double *z_out, double *t, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+                                const int32_t *active, void *stream)
+{
+    return residual_nb<4>(a4, r, w, v, z_out, t, nx, ny, nz, batch, active, stream);
+}
+
+// ------------------------------------------------------------ symmetric pack
+// a4[s] = (A_0, A_+1, A_+nx, A_+nxy); sym_ok[s] is cleared when any mirrored
+// pair (A[r][r-d], A[r-d][r]) differs in its bits (signed zeros included), in
+// which case the caller keeps the 7-band operator.
+__global__ void k_sym_pack(const double *__restrict__ a, double *__restrict__ a4, int32_t *__restrict__ ok, i64 n,
+                           i64 nx, i64 nxy)
+{
+    const i64 s = blockIdx.y;
+    const double *as = a + s * 7 * n;
+    double *o = a4 + s * 4 * n;
+    bool good = true;
+    for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < n; r += (i64)gridDim.x * blockDim.x) {
+        o[r] = as[3 * n + r];
+        o[n + r] = as[4 * n + r];
+        o[2 * n + r] = as[5 * n + r];
+        o[3 * n + r] = as[6 * n + r];
+        auto same = [](double p, double q) { return __double_as_longlong(p) == __double_as_longlong(q); };
+        if (r >= 1 && !same(as[2 * n + r], as[4 * n + r - 1])) good = false;
+        if (r >= nx && !same(as[n + r], as[5 * n + r - nx])) good = false;
+        if (r >= nxy && !same(as[r], as[6 * n + r - nxy])) good = false;
+    }
+    if (!good) ok[s] = 0;
+}
+
+extern "C" int ntd_sym_pack(const double *a, double *a4, int32_t *sym_ok, int64_t nx, int64_t ny, int64_t nz,
+                            int64_t batch, void *stream)
+{
+    if (!a || !a4 || !sym_ok || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
+    i64 n = nx * ny * nz;
+    dim3 grid(grid_rows(n), (unsigned)batch);
+    k_sym_pack<<<grid, 256, 0, (cudaStream_t)stream>>>(a, a4, sym_ok, n, nx, nx * ny);
+    NTD_CHECK_LAUNCH("ntd_sym_pack");
 }
 
 // ----------------------------------------------------------------- dot
@@ -281,6 +360,7 @@ extern "C" int ntd_pcg_start(const double *r, const double *z, double *p, double
 }
 
 // ap = A p and partial p.ap in one pass
+template <int NB>
 __global__ void __launch_bounds__(RED_THREADS) k_spmv_dot(const double *__restrict__ a, const double *__restrict__ p,
                                                           double *__restrict__ ap, double *__restrict__ part, i64 n,
                                                           i64 nx, i64 nxy, const int32_t *__restrict__ active)
@@ -288,11 +368,11 @@ __global__ void __launch_bounds__(RED_THREADS) k_spmv_dot(const double *__restri
     __shared__ double sh[RED_THREADS];
     i64 s = blockIdx.y;
     if (active && !active[s]) return;
-    const double *as = a + s * 7 * n, *ps = p + s * n;
+    const double *as = a + s * NB * n, *ps = p + s * n;
     double *aps = ap + s * n;
     double acc = 0.0;
     for (i64 i = blockIdx.x * (i64)RED_THREADS + threadIdx.x; i < n; i += (i64)RED_BLOCKS * RED_THREADS) {
-        double y = spmv_row(as, ps, i, n, nx, nxy);
+        double y = row_of<NB>(as, ps, i, n, nx, nxy);
         aps[i] = y;
         acc = add_rn(acc, mul_rn(ps[i], y));
     }
@@ -320,19 +400,32 @@ __global__ void k_alpha(const double *__restrict__ part, double *__restrict__ st
     }
 }
 
-extern "C" int ntd_pcg_spmv_alpha(const double *a, const double *p, double *ap, double *state, int32_t *flags,
-                                  int32_t *active, int64_t nx, int64_t ny, int64_t nz, int64_t batch, double *work,
-                                  void *stream)
+template <int NB>
+static int spmv_alpha_nb(const double *a, const double *p, double *ap, double *state, int32_t *flags,
+                         int32_t *active, int64_t nx, int64_t ny, int64_t nz, int64_t batch, double *work,
+                         void *stream)
 {
     if (!a || !p || !ap || !state || !flags || !active || !work || batch < 1) return NTD_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     i64 n = nx * ny * nz;
     dim3 grid(RED_BLOCKS, (unsigned)batch);
-    k_spmv_dot<<<grid, RED_THREADS, 0, st>>>(a, p, ap, work, n, nx, nx * ny, active);
+    k_spmv_dot<NB><<<grid, RED_THREADS, 0, st>>>(a, p, ap, work, n, nx, nx * ny, active);
     int rc = ntd::check_launch("spmv_dot");
     if (rc) return rc;
     k_alpha<<<(unsigned)batch, RED_THREADS, 0, st>>>(work, state, flags, active);
     NTD_CHECK_LAUNCH("ntd_pcg_spmv_alpha");
+}
+extern "C" int ntd_pcg_spmv_alpha(const double *a, const double *p, double *ap, double *state, int32_t *flags,
+                                  int32_t *active, int64_t nx, int64_t ny, int64_t nz, int64_t batch, double *work,
+                                  void *stream)
+{
+    return spmv_alpha_nb<7>(a, p, ap, state, flags, active, nx, ny, nz, batch, work, stream);
+}
+extern "C" int ntd_pcg_spmv_alpha_sym(const double *a4, const double *p, double *ap, double *state,
+                                      int32_t *flags, int32_t *active, int64_t nx, int64_t ny, int64_t nz,
+                                      int64_t batch, double *work, void *stream)
+{
+    return spmv_alpha_nb<4>(a4, p, ap, state, flags, active, nx, ny, nz, batch, work, stream);
 }
 
 // x = alpha*p + x ; r = (-alpha)*ap + r  (axpy, banded_core.py:139-143: two roundings)
@@ -352,6 +445,7 @@ __global__ void k_update_xr(double *__restrict__ x, double *__restrict__ r, cons
 }
 
 // ||(-1)*A x + b||^2 partials (precond_pcg.py:106: axpy(-1.0, spmv(a, x), b))
+template <int NB>
 __global__ void __launch_bounds__(RED_THREADS) k_true_res(const double *__restrict__ a, const double *__restrict__ b,
                                                           const double *__restrict__ x, double *__restrict__ part,
                                                           i64 n, i64 nx, i64 nxy, const int32_t *__restrict__ active)
@@ -359,10 +453,10 @@ __global__ void __launch_bounds__(RED_THREADS) k_true_res(const double *__restri
     __shared__ double sh[RED_THREADS];
     i64 s = blockIdx.y;
     if (!active[s]) return;
-    const double *as = a + s * 7 * n, *xs = x + s * n, *bs = b + s * n;
+    const double *as = a + s * NB * n, *xs = x + s * n, *bs = b + s * n;
     double acc = 0.0;
     for (i64 i = blockIdx.x * (i64)RED_THREADS + threadIdx.x; i < n; i += (i64)RED_BLOCKS * RED_THREADS) {
-        double res = add_rn(-spmv_row(as, xs, i, n, nx, nxy), bs[i]);
+        double res = add_rn(-row_of<NB>(as, xs, i, n, nx, nxy), bs[i]);
         acc = add_rn(acc, mul_rn(res, res));
     }
     double bsum = block_sum(acc, sh);
@@ -395,10 +489,11 @@ __global__ void k_relres(const double *__restrict__ part, double *__restrict__ s
     }
 }
 
-extern "C" int ntd_pcg_update_residual(const double *a, const double *b, double *x, double *r, const double *p,
-                                       const double *ap, double *state, int32_t *flags, int32_t *active,
-                                       double *history, int64_t max_iters, int64_t nx, int64_t ny, int64_t nz,
-                                       int64_t batch, double *work, void *stream)
+template <int NB>
+static int update_residual_nb(const double *a, const double *b, double *x, double *r, const double *p,
+                              const double *ap, double *state, int32_t *flags, int32_t *active, double *history,
+                              int64_t max_iters, int64_t nx, int64_t ny, int64_t nz, int64_t batch, double *work,
+                              void *stream)
 {
     if (!a || !b || !x || !r || !p || !ap || !state || !flags || !active || !history || !work) return NTD_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
@@ -408,11 +503,27 @@ extern "C" int ntd_pcg_update_residual(const double *a, const double *b, double 
     int rc = ntd::check_launch("update_xr");
     if (rc) return rc;
     dim3 g2(RED_BLOCKS, (unsigned)batch);
-    k_true_res<<<g2, RED_THREADS, 0, st>>>(a, b, x, work, n, nx, nx * ny, active);
+    k_true_res<NB><<<g2, RED_THREADS, 0, st>>>(a, b, x, work, n, nx, nx * ny, active);
     rc = ntd::check_launch("true_res");
     if (rc) return rc;
     k_relres<<<(unsigned)batch, RED_THREADS, 0, st>>>(work, state, flags, active, history, max_iters);
     NTD_CHECK_LAUNCH("ntd_pcg_update_residual");
+}
+extern "C" int ntd_pcg_update_residual(const double *a, const double *b, double *x, double *r, const double *p,
+                                       const double *ap, double *state, int32_t *flags, int32_t *active,
+                                       double *history, int64_t max_iters, int64_t nx, int64_t ny, int64_t nz,
+                                       int64_t batch, double *work, void *stream)
+{
+    return update_residual_nb<7>(a, b, x, r, p, ap, state, flags, active, history, max_iters, nx, ny, nz, batch,
+                                 work, stream);
+}
+extern "C" int ntd_pcg_update_residual_sym(const double *a4, const double *b, double *x, double *r,
+                                           const double *p, const double *ap, double *state, int32_t *flags,
+                                           int32_t *active, double *history, int64_t max_iters, int64_t nx,
+                                           int64_t ny, int64_t nz, int64_t batch, double *work, void *stream)
+{
+    return update_residual_nb<4>(a4, b, x, r, p, ap, state, flags, active, history, max_iters, nx, ny, nz, batch,
+                                 work, stream);
 }
 
 // beta = rz_new / rz ; rz = rz_new  (precond_pcg.py:116-118)

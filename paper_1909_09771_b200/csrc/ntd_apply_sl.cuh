@@ -350,6 +350,29 @@ __device__ __forceinline__ void prefetch_bulk_l2(const double *p, unsigned bytes
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// Producer-side wait.  try_wait suspends the warp in hardware until the phase
+// completes (or the hint expires), so a waiting producer takes no issue slots
+// from the solver warp of its SM sub-partition.
+#ifndef NTD_PRODUCER_TRYWAIT
+#define NTD_PRODUCER_TRYWAIT 1
+#endif
+__device__ __forceinline__ void mbar_wait_producer(void *bar, unsigned parity)
+{
+    if constexpr (NTD_PRODUCER_TRYWAIT) {
+        unsigned ok = 0;
+        const unsigned a = smem_u32(bar);
+        while (!ok) {
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+                : "=r"(ok)
+                : "r"(a), "r"(parity), "r"(1000000u)
+                : "memory");
+        }
+    } else {
+        mbar_wait_lazy(bar, parity);
+    }
+}
+
 template <int K>
 __device__ __forceinline__ void rec_copy(const SlArrays &S, const PlaneDesc &P, const Seq &Q, int k, double *dst,
                                          unsigned long long *bar)
@@ -387,13 +410,15 @@ __device__ void produce_plane(const SlArrays &S, const PlaneDesc &P, const Plane
     const int n = 2 * Q.cnt;
     if (lane == 0) {
         for (int k = 0; k < n; k++, rec++) {
-            const int j = k + L2_PF;
-            if (j < n)
-                rec_copy<K>(S, P, Q, j, nullptr, nullptr);
-            else if (Pn && j - n < n)
-                rec_copy<K>(S, *Pn, Q, j - n, nullptr, nullptr);
+            if constexpr (L2_PF > 0) {
+                const int j = k + L2_PF;
+                if (j < n)
+                    rec_copy<K>(S, P, Q, j, nullptr, nullptr);
+                else if (Pn && j - n < n)
+                    rec_copy<K>(S, *Pn, Q, j - n, nullptr, nullptr);
+            }
             const int st = rec % D;
-            if (rec >= (unsigned)D) mbar_wait_lazy(&R.empty[st], ((rec / D) + 1) & 1);
+            if (rec >= (unsigned)D) mbar_wait_producer(&R.empty[st], ((rec / D) + 1) & 1);
             if (PRODUCER_FENCE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             rec_copy<K>(S, P, Q, k, R.stage(st), &R.full[st]);
         }
@@ -509,6 +534,15 @@ __device__ __forceinline__ void ld_upper(LineOps<K> &o, const double *sg, const 
     if (!LOWER3) ld_rec(sg + rx_of(K), L, o.pt, o.ptt);
 }
 
+#ifndef NTD_L1PF
+#define NTD_L1PF 0
+#endif
+constexpr int L1PF = NTD_L1PF;
+__device__ __forceinline__ void prefetch_l1(const double *p)
+{
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 // ---------------- solver: one plane
 template <int K, int D, int MODE, bool TWO>
 __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q, int nx, int bar_id, double *ex,
@@ -557,6 +591,17 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
         ld_rec(y1 + Q.qlow(j) * LR, L, n1, n1t);
         if (TWO) ld_rec(y2 + Q.qlow(j) * LR, L, n2, n2t);
     };
+    // L1 prefetch of the x-dependent lines NTD_L1PF steps ahead of their load
+    // (these operands are final long before use; an L1 hit keeps the copy of
+    // the in-flight load at the top of a step from stalling on L2 latency)
+    auto pf_nbr = [&](int j) {
+        if constexpr (L1PF > 0) {
+            if (j < cnt) {
+                prefetch_l1(y1 + Q.qlow(j) * LR + L.base);
+                if (TWO) prefetch_l1(y2 + Q.qlow(j) * LR + L.base);
+            }
+        }
+    };
     auto full = [&](unsigned r) { return &R.full[r % D]; };
     auto par = [&](unsigned r) { return (r / D) & 1u; };
     LineOps<K> cur;
@@ -589,6 +634,7 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
         LineOps<K> nxo;
         bool ok2 = true;
         if (PIPE) {
+            pf_nbr(i + 2 + L1PF);
             ld_nbr(i + 2 < cnt ? i + 2 : cnt - 1);
             if (WAIT_AHEAD)
                 ok2 = mbar_test(full(rec + 2), par(rec + 2));
@@ -709,6 +755,9 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
         double y[K], yt = ybt_;
 #pragma unroll
         for (int k = 0; k < K; k++) y[k] = yb_[k];
+        if constexpr (L1PF > 0) {
+            if (i + 1 + L1PF < cnt) prefetch_l1(xlow + Q.qup(i + 1 + L1PF) * LR + L.base);
+        }
         ld_rec(xlow + Q.qup(i + 1 < cnt ? i + 1 : i) * LR, L, yb_, ybt_);  // line i+1 (unconditional)
         LineOps<K> nxo;
         bool ok2 = true;

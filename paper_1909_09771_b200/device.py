@@ -113,11 +113,24 @@ def ilu0_apply(f_dev, split, r_dev, nx, ny, nz, batch, z=None, acc=None, active=
     return z
 
 
-def residual(a_dev, r_dev, w_dev, nx, ny, nz, batch, t=None, v=None, z_out=None, active=None):
-    """t = r - A w, or (v given) z_out = v + w and t = r - A z_out."""
+def sym_pack(a_dev, nx, ny, nz, batch):
+    """(B,4,N) symmetric packed operator (bands 0,+1,+nx,+nxy) when every
+    system's A is bitwise symmetric, else None (the 7-band kernels are used).
+    One pass over A plus one small device->host read (setup time)."""
+    n = nx * ny * nz
+    a4 = torch.empty((batch, 4, n), dtype=torch.float64, device=a_dev.device)
+    ok = torch.ones(batch, dtype=torch.int32, device=a_dev.device)
+    _lib.call("ntd_sym_pack", _lib.ptr(a_dev), _lib.ptr(a4), _lib.ptr(ok), nx, ny, nz, batch, _lib.stream())
+    return a4 if bool(ok.all().item()) else None
+
+
+def residual(a_dev, r_dev, w_dev, nx, ny, nz, batch, t=None, v=None, z_out=None, active=None, a4=None):
+    """t = r - A w, or (v given) z_out = v + w and t = r - A z_out.  With a4
+    (sym_pack) the symmetric 4-band kernel is used (bitwise the same)."""
     if t is None:
         t = torch.empty_like(r_dev)
-    _lib.call("ntd_residual", _lib.ptr(a_dev), _lib.ptr(r_dev), _lib.ptr(w_dev), _lib.ptr(v), _lib.ptr(z_out),
+    name, op = ("ntd_residual", a_dev) if a4 is None else ("ntd_residual_sym", a4)
+    _lib.call(name, _lib.ptr(op), _lib.ptr(r_dev), _lib.ptr(w_dev), _lib.ptr(v), _lib.ptr(z_out),
               _lib.ptr(t), nx, ny, nz, batch, _lib.ptr(active), _lib.stream())
     return t
 
@@ -126,8 +139,10 @@ class CombinedDevice:
     """Symmetric ILU0 -> NTD -> ILU0 preconditioner on B systems
     (precond_pcg.py:28-65), all buffers preallocated on the device."""
 
-    def __init__(self, a_dev, nx, ny, nz, batch, pre=None, ilu=None, split=None, solve=None, skew=None):
+    def __init__(self, a_dev, nx, ny, nz, batch, pre=None, ilu=None, split=None, solve=None, skew=None,
+                 a4="auto"):
         self.a, self.nx, self.ny, self.nz, self.batch = a_dev, nx, ny, nz, batch
+        self.a4 = sym_pack(a_dev, nx, ny, nz, batch) if isinstance(a4, str) else a4
         n = nx * ny * nz
         self.n = n
         self.pre = pre
@@ -152,7 +167,7 @@ class CombinedDevice:
             self.skew_work = torch.empty(_lib.load().ntd_ilu0_skew_work_doubles(*g), dtype=torch.float64,
                                          device=_dev())
         ilu0_apply(self.ilu, self.split, r, *g, z=self.w, active=active, skew=self.skew, work=self.skew_work)
-        residual(self.a, r, self.w, *g, t=self.t, active=active)
+        residual(self.a, r, self.w, *g, t=self.t, active=active, a4=self.a4)
         if self.ntd_events is not None:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record()
@@ -160,7 +175,7 @@ class CombinedDevice:
         if self.ntd_events is not None:
             ev[1].record()
             self.ntd_events.append(ev)
-        residual(self.a, r, self.w, *g, t=self.t, v=self.xn, z_out=z, active=active)
+        residual(self.a, r, self.w, *g, t=self.t, v=self.xn, z_out=z, active=active, a4=self.a4)
         if self.skew is not None:
             ilu0_apply(self.ilu, self.split, self.t, *g, z=None, acc=z, active=active, skew=self.skew,
                        work=self.skew_work)
@@ -176,9 +191,10 @@ class PcgDevice:
     device; one small device->host read of the flags per iteration decides
     whether to continue.  Converged systems are masked out of every kernel."""
 
-    def __init__(self, a_dev, nx, ny, nz, batch, max_iters, x=None):
+    def __init__(self, a_dev, nx, ny, nz, batch, max_iters, x=None, a4="auto"):
         lib = _lib.load()
         self.a, self.nx, self.ny, self.nz, self.batch = a_dev, nx, ny, nz, batch
+        self.a4 = sym_pack(a_dev, nx, ny, nz, batch) if isinstance(a4, str) else a4
         n = nx * ny * nz
         self.n = n
         self.max_iters = max_iters
@@ -212,10 +228,14 @@ class PcgDevice:
 
     def step_update(self):
         """ap = A p; alpha; x, r update; true residual; convergence flags."""
-        _lib.call("ntd_pcg_spmv_alpha", _lib.ptr(self.a), _lib.ptr(self.p), _lib.ptr(self.ap),
+        sym = self.a4 is not None
+        op = self.a4 if sym else self.a
+        _lib.call("ntd_pcg_spmv_alpha_sym" if sym else "ntd_pcg_spmv_alpha", _lib.ptr(op), _lib.ptr(self.p),
+                  _lib.ptr(self.ap),
                   _lib.ptr(self.state), _lib.ptr(self.flags), _lib.ptr(self.active), *self._g(),
                   _lib.ptr(self.work), _lib.stream())
-        _lib.call("ntd_pcg_update_residual", _lib.ptr(self.a), _lib.ptr(self.b), _lib.ptr(self.x),
+        _lib.call("ntd_pcg_update_residual_sym" if sym else "ntd_pcg_update_residual", _lib.ptr(op),
+                  _lib.ptr(self.b), _lib.ptr(self.x),
                   _lib.ptr(self.r), _lib.ptr(self.p), _lib.ptr(self.ap), _lib.ptr(self.state),
                   _lib.ptr(self.flags), _lib.ptr(self.active), _lib.ptr(self.history), self.max_iters,
                   *self._g(), _lib.ptr(self.work), _lib.stream())

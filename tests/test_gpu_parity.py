@@ -127,3 +127,33 @@ def test_baseline_configs_1_2(ntd):
         xs, st = ntd.pcg(a, b, cp, tol=1e-8, max_iters=200)
         assert st.converged and st.final_relres < 1e-8
         assert abs(st.iterations - rec["pcg_iters"]) <= 1, (cfg, st.iterations, rec["pcg_iters"])
+
+
+def test_symmetric_packed_stencil_bitwise(ntd, golden):
+    """The 4-band symmetric operator (ntd_sym_pack) gives bitwise the same
+    residuals and CG iterates as the reference-order 7-band kernels; a
+    non-symmetric operator is refused (stays on the 7-band path)."""
+    import torch
+    from paper_1909_09771_b200 import device as D
+    for name in names(golden):
+        nx, ny, nz = grid_of(name)
+        n = nx * ny * nz
+        A = torch.from_numpy(np.ascontiguousarray(golden[name + "/A"])).cuda().reshape(1, 7, n)
+        a4 = D.sym_pack(A, nx, ny, nz, 1)
+        assert a4 is not None, name
+        gen = torch.Generator().manual_seed(7)
+        r, w, v = ((torch.rand((1, n), generator=gen, dtype=torch.float64) * 2 - 1).cuda() for _ in range(3))
+        assert torch.equal(D.residual(A, r, w, nx, ny, nz, 1), D.residual(A, r, w, nx, ny, nz, 1, a4=a4)), name
+        z7, z4 = torch.empty_like(r), torch.empty_like(r)
+        t7 = D.residual(A, r, w, nx, ny, nz, 1, v=v, z_out=z7)
+        t4 = D.residual(A, r, w, nx, ny, nz, 1, v=v, z_out=z4, a4=a4)
+        assert torch.equal(t7, t4) and torch.equal(z7, z4), name
+        xs = []
+        for op in (None, a4):
+            cg = D.PcgDevice(A, nx, ny, nz, 1, 30, a4=op)
+            it = cg.solve(r, 1e-10)
+            xs.append((it, cg.x.clone()))
+        assert xs[0][0] == xs[1][0] and torch.equal(xs[0][1], xs[1][1]), name
+    B = A.clone()
+    B[0, 2, 1] += 1e-3  # A[1][0] != A[0][1]
+    assert D.sym_pack(B, nx, ny, nz, 1) is None
