@@ -488,6 +488,202 @@ __global__ void __launch_bounds__(128) k_ntd_apply(const double *__restrict__ pr
 }
 
 // =============================================================== factor
+// Setup-side line and plane solves in the reference's exact operation order.
+//
+// The factorisation feeds nested solves back into the bands (correct_line:
+// T_m^-1 u; correct_from: the nested plane solve of the neighbour), and on
+// strongly heterogeneous fields (BASELINE config 5, kappa jumps of 1e6)
+// rounding differences there are amplified to ~1e-10 in the bands.  So the
+// setup does not use the warp-scan line solve of the apply: it restates
+// _chain_scaled / _chain_unit (ntd_solve.py:20-104) with the reference's
+// lane composition (CHAIN_LANES = 4, ntd_solve.py:17: `lanes` chunks of
+// m // lanes composed into prefix maps, stitched sequentially, remainder
+// walked sequentially), every operation exactly rounded in the reference's
+// order.  The resulting factor is bitwise equal to the reference's.
+constexpr int REF_LANES = 4;
+
+// One chain of a line (both chains of a line run concurrently, one per
+// half-warp h).  Chain position e = 0..m-1 is cell lo + e*step.
+//   SCALED: x_e = (rhs_e - off_e x_{e-1}) dr_e, x_{-1} = x0 (_chain_scaled)
+//   UNIT:   x_e = x_e - dr_e off_e x_{e-1}     (_chain_unit, in place)
+// aw/cw: smem prefix maps (m each); car: smem carries (REF_LANES + 1).
+template <bool SCALED>
+__device__ __forceinline__ void chain_ref_compose(double *x, const double *dr, const double *off, const double *rhs,
+                                                  int lo, int step, int m, double *aw, double *cw, int sl)
+{
+    // sl: lane within the half-warp; lanes 0..REF_LANES-1 compose one chunk each
+    if (m < 2 * REF_LANES || sl >= REF_LANES) return;
+    const int chunk = m / REF_LANES, base = sl * chunk;
+    int p = lo + base * step;
+    double a = SCALED ? mul_rn(-off[p], dr[p]) : mul_rn(-dr[p], off[p]);
+    double aa = a, cc = SCALED ? mul_rn(rhs[p], dr[p]) : x[p];
+    aw[base] = aa;
+    cw[base] = cc;
+    for (int t = 1; t < chunk; t++) {
+        p += step;
+        a = SCALED ? mul_rn(-off[p], dr[p]) : mul_rn(-dr[p], off[p]);
+        aa = mul_rn(a, aa);
+        cc = add_rn(mul_rn(a, cc), SCALED ? mul_rn(rhs[p], dr[p]) : x[p]);
+        aw[base + t] = aa;
+        cw[base + t] = cc;
+    }
+}
+
+template <bool SCALED>
+__device__ __forceinline__ void chain_ref_finish(double *x, const double *dr, const double *off, const double *rhs,
+                                                 int lo, int step, int m, double x0, const double *aw,
+                                                 const double *cw, double *car, int sl)
+{
+    // Both half-warps run this concurrently (their chains may take different
+    // branches), so every path passes exactly two __syncwarp().
+    if (m < 2 * REF_LANES) {  // scalar chain (also m <= 0: nothing)
+        if (sl == 0) {
+            double xp = x0;
+            int p = lo;
+            for (int it = 0; it < m; it++, p += step) {
+                xp = SCALED ? mul_rn(sub_rn(rhs[p], mul_rn(off[p], xp)), dr[p])
+                            : sub_rn(x[p], mul_rn(mul_rn(dr[p], off[p]), xp));
+                x[p] = xp;
+            }
+        }
+        __syncwarp();
+        __syncwarp();
+        return;
+    }
+    const int chunk = m / REF_LANES;
+    if (sl == 0) {  // carries into each chunk, stitched in order
+        double carry = x0;
+        for (int l = 0; l < REF_LANES; l++) {
+            car[l] = carry;
+            const int e = l * chunk + chunk - 1;
+            carry = add_rn(mul_rn(aw[e], carry), cw[e]);
+        }
+        car[REF_LANES] = carry;
+    }
+    __syncwarp();
+    for (int e = sl; e < REF_LANES * chunk; e += 16) x[lo + e * step] = add_rn(mul_rn(aw[e], car[e / chunk]), cw[e]);
+    if (sl == 0) {  // remainder, sequential from the last carry
+        double xp = car[REF_LANES];
+        int p = lo + REF_LANES * chunk * step;
+        for (int it = REF_LANES * chunk; it < m; it++, p += step) {
+            xp = SCALED ? mul_rn(sub_rn(rhs[p], mul_rn(off[p], xp)), dr[p])
+                        : sub_rn(x[p], mul_rn(mul_rn(dr[p], off[p]), xp));
+            x[p] = xp;
+        }
+    }
+    __syncwarp();
+}
+
+// _line_solve (ntd_solve.py:134-137) of one line of n cells by one warp:
+// x = T^-1 b with T's factor (mr, l1, u1).  All arrays line-local (index 0 =
+// first cell); x and b may live in global memory.  lsm: >= 2n doubles of smem
+// (prefix maps), car: 2 x (REF_LANES + 1) doubles of smem.
+static __device__ void line_solve_ref(double *x, const double *b, const double *mr, const double *l1, const double *u1,
+                               int n, double *lsm, double *car)
+{
+    const int lane = threadIdx.x & 31, h = lane >> 4, sl = lane & 15;
+    const int t = (n - 1) / 2;
+    // half 0: ascending chain over cells 0..t-1; half 1: descending n-1..t+1
+    const int m = h == 0 ? t : n - 1 - t;
+    const int lo = h == 0 ? 0 : n - 1, step = h == 0 ? 1 : -1;
+    double *aw = lsm + (h == 0 ? 0 : 2 * t), *cw = aw + m;
+    double *ch = car + h * (REF_LANES + 1);
+    // _line_lower (ntd_solve.py:107-121)
+    chain_ref_compose<true>(x, mr, h == 0 ? l1 : u1, b, lo, step, m, aw, cw, sl);
+    __syncwarp();
+    chain_ref_finish<true>(x, mr, h == 0 ? l1 : u1, b, lo, step, m, 0.0, aw, cw, ch, sl);
+    if (lane == 0) {
+        double acc = b[t];
+        if (t > 0) acc = sub_rn(acc, mul_rn(l1[t], x[t - 1]));
+        if (t < n - 1) acc = sub_rn(acc, mul_rn(u1[t], x[t + 1]));
+        x[t] = mul_rn(acc, mr[t]);
+    }
+    __syncwarp();
+    // _line_upper (ntd_solve.py:124-131): outward from the twist
+    const double xt = x[t];
+    const int lo2 = h == 0 ? t - 1 : t + 1, step2 = -step;
+    chain_ref_compose<false>(x, mr, h == 0 ? u1 : l1, nullptr, lo2, step2, m, aw, cw, sl);
+    __syncwarp();
+    chain_ref_finish<false>(x, mr, h == 0 ? u1 : l1, nullptr, lo2, step2, m, xt, aw, cw, ch, sl);
+}
+
+// _plane_solve (ntd_solve.py:140-185) of factored plane (F at offset pb) in
+// the reference's order, by a warp pair (w2 = 0: lines 0..t2, w2 = 1: lines
+// t2+1..ny-1; the two level-2 halves only meet at the twist line).
+// rhs: plane-local right-hand side (read only); X: solution; B, XS, BS:
+// plane-local scratch (B receives the consumed copy of rhs).
+static __device__ void plane_solve_ref(const FactorPtrs &F, i64 pb, const double *rhs, double *X, double *B, double *XS,
+                                double *BS, int nx, int ny, int w2, int bar_id, double *lsm, double *car)
+{
+    const int lane = threadIdx.x & 31;
+    const int t2 = (ny - 1) / 2;
+    const double *mr = F.mr + pb, *l1 = F.l1 + pb, *u1 = F.u1 + pb, *l2 = F.l2 + pb, *u2 = F.u2 + pb;
+    const i64 q0 = w2 == 0 ? 0 : (i64)(t2 + 1) * nx, q1 = w2 == 0 ? (i64)(t2 + 1) * nx : (i64)ny * nx;
+    for (i64 k = q0 + lane; k < q1; k += 32) B[k] = rhs[k];
+    __syncwarp();
+    auto lsolve = [&](double *xx, const double *bb, i64 off) {
+        line_solve_ref(xx + off, bb + off, mr + off, l1 + off, u1 + off, nx, lsm, car);
+    };
+    // level-2 lower sweep, ends inward (ntd_solve.py:147-171)
+    if (w2 == 0) {
+        for (int q = 0; q < t2; q++) {
+            const i64 s = (i64)q * nx;
+            if (q > 0) {
+                for (int c = lane; c < nx; c += 32) B[s + c] = sub_rn(B[s + c], mul_rn(l2[s + c], X[s + c - nx]));
+                __syncwarp();
+            }
+            lsolve(X, B, s);
+        }
+    } else {
+        for (int q = ny - 1; q > t2; q--) {
+            const i64 s = (i64)q * nx;
+            if (q < ny - 1) {
+                for (int c = lane; c < nx; c += 32) B[s + c] = sub_rn(B[s + c], mul_rn(u2[s + c], X[s + c + nx]));
+                __syncwarp();
+            }
+            lsolve(X, B, s);
+        }
+    }
+    __threadfence_block();
+    named_bar(bar_id, 64);
+    // twist line (ntd_solve.py:172-177)
+    if (w2 == 0) {
+        const i64 s = (i64)t2 * nx;
+        for (int c = lane; c < nx; c += 32) {
+            double v = B[s + c];
+            if (t2 > 0) v = sub_rn(v, mul_rn(l2[s + c], X[s + c - nx]));
+            if (t2 < ny - 1) v = sub_rn(v, mul_rn(u2[s + c], X[s + c + nx]));
+            B[s + c] = v;
+        }
+        __syncwarp();
+        lsolve(X, B, s);
+    }
+    __threadfence_block();
+    named_bar(bar_id, 64);
+    // level-2 upper sweep, twist outward (ntd_solve.py:178-185)
+    if (w2 == 0) {
+        for (int q = t2 - 1; q >= 0; q--) {
+            const i64 s = (i64)q * nx;
+            for (int c = lane; c < nx; c += 32) BS[s + c] = mul_rn(u2[s + c], X[s + c + nx]);
+            __syncwarp();
+            lsolve(XS, BS, s);
+            for (int c = lane; c < nx; c += 32) X[s + c] = sub_rn(X[s + c], XS[s + c]);
+            __syncwarp();
+        }
+    } else {
+        for (int q = t2 + 1; q < ny; q++) {
+            const i64 s = (i64)q * nx;
+            for (int c = lane; c < nx; c += 32) BS[s + c] = mul_rn(l2[s + c], X[s + c - nx]);
+            __syncwarp();
+            lsolve(XS, BS, s);
+            for (int c = lane; c < nx; c += 32) X[s + c] = sub_rn(X[s + c], XS[s + c]);
+            __syncwarp();
+        }
+    }
+    __threadfence_block();
+    named_bar(bar_id, 64);
+}
+
 // Per-pair global scratch (plane-local, nxy each).
 enum { S_PC0 = 0, S_PC1 = 5, S_W = 10, S_YL, S_BETA, S_QD, S_TDW, S_XW, S_BW, S_PER_PAIR };
 
@@ -582,19 +778,15 @@ static __device__ int line_factor_warp(const double *__restrict__ td, const doub
 // plane's factor outputs, TDW/XW/BW scratch.  Returns -1 or bad plane-local row.
 template <int K>
 __device__ i64 correct_line_warp(int q, int m, const double *P_l2, const double *P_u2, double *TDW, double *L1G,
-                                 double *U1G, const double *MRG, double *XW, double *BW, int nx)
+                                 double *U1G, const double *MRG, double *XW, double *BW, int nx, double *lsm,
+                                 double *car)
 {
     const int lane = threadIdx.x & 31;
-    const LineGeom<K> g(nx, lane);
     const i64 sq = (i64)q * nx, sm = (i64)m * nx;
     const double *src = m < q ? P_u2 : P_l2;
     for (int c = lane; c < nx; c += 32) BW[sm + c] = src[sm + c];
     __syncwarp();
-    double mr[K], oL[K], oU[K], mrt, l1t, u1t, rhs[K], rhst, xw[K], xwt;
-    load_line_factors(g, MRG, L1G, U1G, sm, mr, oL, oU, mrt, l1t, u1t);
-    load_slots(g, BW, sm, rhs, rhst);
-    line_solve(g, mr, oL, oU, rhs, rhst, mrt, l1t, u1t, xw, xwt);
-    store_slots(g, XW, sm, xw, xwt);
+    line_solve_ref(XW + sm, BW + sm, MRG + sm, L1G + sm, U1G + sm, nx, lsm, car);
     __syncwarp();
     // beta = w/u where u != 0 (first non-finite -> error)
     int badk = 0x7fffffff;
@@ -636,7 +828,7 @@ struct FactorCtx {
 template <int K>
 __device__ void factor_plane_pair(const FactorCtx &c, i64 pb, const double *P[5], const PairScratch &S, int w2,
                                   int bar_id, volatile int *ecode, i64 *eplane, i64 *erow, int plane,
-                                  double *lsm, volatile i64 *wbad)
+                                  double *lsm, volatile i64 *wbad, double *car)
 {
     const int lane = threadIdx.x & 31;
     const int nx = c.nx, ny = c.ny, t2 = (ny - 1) / 2;
@@ -660,7 +852,8 @@ __device__ void factor_plane_pair(const FactorCtx &c, i64 pb, const double *P[5]
         int q = w2 == 0 ? i : ny - 1 - i;
         init_line(q);
         if (i > 0) {
-            i64 st = correct_line_warp<K>(q, w2 == 0 ? q - 1 : q + 1, P[3], P[4], TDW, L1G, U1G, MRG, XW, BW, nx);
+            i64 st = correct_line_warp<K>(q, w2 == 0 ? q - 1 : q + 1, P[3], P[4], TDW, L1G, U1G, MRG, XW, BW, nx,
+                                          lsm, car);
             if (st >= 0) {
                 mcode = 2;
                 mrow = st;
@@ -695,11 +888,11 @@ __device__ void factor_plane_pair(const FactorCtx &c, i64 pb, const double *P[5]
         i64 st = -1;
         int code = 0;
         if (t2 > 0) {
-            st = correct_line_warp<K>(q, q - 1, P[3], P[4], TDW, L1G, U1G, MRG, XW, BW, nx);
+            st = correct_line_warp<K>(q, q - 1, P[3], P[4], TDW, L1G, U1G, MRG, XW, BW, nx, lsm, car);
             if (st >= 0) code = 2;
         }
         if (!code && t2 < ny - 1) {
-            st = correct_line_warp<K>(q, q + 1, P[3], P[4], TDW, L1G, U1G, MRG, XW, BW, nx);
+            st = correct_line_warp<K>(q, q + 1, P[3], P[4], TDW, L1G, U1G, MRG, XW, BW, nx, lsm, car);
             if (st >= 0) code = 2;
         }
         if (!code) {
@@ -720,7 +913,8 @@ __device__ void factor_plane_pair(const FactorCtx &c, i64 pb, const double *P[5]
 template <int K>
 __device__ void correct_from_pair(const FactorCtx &c, int p, int m, double *P[5], const double *Q[5],
                                   const PairScratch &S, int w2, int bar_id, double *ex, int &parity,
-                                  volatile int *ecode, i64 *eplane, i64 *erow, volatile int *flag)
+                                  volatile int *ecode, i64 *eplane, i64 *erow, volatile int *flag, double *lsm,
+                                  double *car)
 {
     const i64 nxy = c.nxy, n = c.n;
     const int nx = c.nx;
@@ -729,15 +923,9 @@ __device__ void correct_from_pair(const FactorCtx &c, int p, int m, double *P[5]
     const double *useg = (m < p ? c.a + 6 * n : c.a) + (i64)m * nxy;  // u3 | l3 = copies of A's +-nxy
     const double *rowscale = (m < p ? c.a : c.a + 6 * n) + (i64)p * nxy;
     double *W = S.at(S_W), *BETA = S.at(S_BETA), *QD = S.at(S_QD);
-    PlaneIO io;
-    io.b = nullptr;
-    io.x = io.xs = nullptr;
-    io.hasM = io.hasP = io.nbrUp = false;
-    io.useg = useg;
-    io.ylow = S.at(S_YL);
-    io.out = W;
-    plane_solve<K, M_SETUP>(F, io, (i64)m * nxy, c.nx, c.ny, w2, bar_id, ex, parity);
-    named_bar(bar_id, 64);
+    // _apply_factored_plane (ntd_factor.py:336-348): w = nested solve of plane
+    // m on a copy of u (BETA / QD serve as the solve's scratch planes)
+    plane_solve_ref(F, (i64)m * nxy, useg, W, S.at(S_YL), BETA, QD, c.nx, c.ny, w2, bar_id, lsm, car);
     // beta (_beta_from :242-249), qw (_plane_band_action :266-274), qd shift (:393-399)
     int fb = 0, fq = 0;
     for (i64 k = tid; k < nxy; k += 64) {
@@ -796,7 +984,8 @@ static __device__ void load_plane_bands(const FactorCtx &c, int p, double *P[5],
 // factor_one (ntd_factor.py:406-419)
 template <int K>
 __device__ void factor_one_pair(const FactorCtx &c, int p, double *P[5], const PairScratch &S, int w2, int bar_id,
-                                volatile int *ecode, i64 *eplane, i64 *erow, double *lsm, volatile i64 *wbad)
+                                volatile int *ecode, i64 *eplane, i64 *erow, double *lsm, volatile i64 *wbad,
+                                double *car)
 {
     const int tid = threadIdx.x & 63;
     const i64 pb = (i64)p * c.nxy, n = c.n;
@@ -806,7 +995,7 @@ __device__ void factor_one_pair(const FactorCtx &c, int p, double *P[5], const P
     }
     named_bar(bar_id, 64);
     const double *Pc[5] = {P[0], P[1], P[2], P[3], P[4]};
-    factor_plane_pair<K>(c, pb, Pc, S, w2, bar_id, ecode, eplane, erow, p, lsm, wbad);
+    factor_plane_pair<K>(c, pb, Pc, S, w2, bar_id, ecode, eplane, erow, p, lsm, wbad, car);
 }
 
 template <int K>
@@ -820,6 +1009,7 @@ __global__ void __launch_bounds__(128) k_ntd_factor(const double *__restrict__ a
     __shared__ i64 wbad_s[2][4];
     __shared__ int flag_s[2][2];
     __shared__ int last_p[2];
+    __shared__ double car_s[4][2 * (REF_LANES + 1)];  // chain carries, per warp
     const i64 sys = blockIdx.x;
     const i64 nxy = (i64)nx * ny, n = nxy * nz;
     FactorCtx c;
@@ -832,6 +1022,7 @@ __global__ void __launch_bounds__(128) k_ntd_factor(const double *__restrict__ a
     c.nz = nz;
     const int warp = threadIdx.x >> 5, pair = warp >> 1, w2 = warp & 1, bar = 1 + pair;
     double *lsm = lsm_all + warp * 3 * nx;
+    double *car = car_s[warp];
     if (threadIdx.x < 2) {
         ecode_s[threadIdx.x] = 0;
         eplane_s[threadIdx.x] = -1;
@@ -877,10 +1068,11 @@ __global__ void __launch_bounds__(128) k_ntd_factor(const double *__restrict__ a
                 named_bar(bar, 64);
                 const double *Q[5] = {Pprev[0], Pprev[1], Pprev[2], Pprev[3], Pprev[4]};
                 correct_from_pair<K>(c, p, prev_p, Pcur, Q, MS, w2, bar, ex[pair], parity, ecode, &eplane_s[pair],
-                                     &erow_s[pair], flag_s[pair]);
+                                     &erow_s[pair], flag_s[pair], lsm, car);
                 if (*ecode) break;
             }
-            factor_one_pair<K>(c, p, Pcur, MS, w2, bar, ecode, &eplane_s[pair], &erow_s[pair], lsm, wbad_s[pair]);
+            factor_one_pair<K>(c, p, Pcur, MS, w2, bar, ecode, &eplane_s[pair], &erow_s[pair], lsm, wbad_s[pair],
+                               car);
             if (*ecode) break;
             double **tmp = Pcur;
             Pcur = Pprev;
@@ -901,7 +1093,7 @@ __global__ void __launch_bounds__(128) k_ntd_factor(const double *__restrict__ a
             named_bar(bar, 64);
             const double *Q[5] = {Pprev[0], Pprev[1], Pprev[2], Pprev[3], Pprev[4]};
             correct_from_pair<K>(c, t3, pa, Pt, Q, MS, w2, bar, ex[0], parity, ecode, &eplane_s[0], &erow_s[0],
-                                 flag_s[0]);
+                                 flag_s[0], lsm, car);
         }
         if (!*ecode && pd >= 0) {
             // pair 1's last corrected bands: its "Pprev" after the final swap
@@ -912,10 +1104,10 @@ __global__ void __launch_bounds__(128) k_ntd_factor(const double *__restrict__ a
             named_bar(bar, 64);
             const double *Q[5] = {Q1[0], Q1[1], Q1[2], Q1[3], Q1[4]};
             correct_from_pair<K>(c, t3, pd, Pt, Q, MS, w2, bar, ex[0], parity, ecode, &eplane_s[0], &erow_s[0],
-                                 flag_s[0]);
+                                 flag_s[0], lsm, car);
         }
         if (!*ecode)
-            factor_one_pair<K>(c, t3, Pt, MS, w2, bar, ecode, &eplane_s[0], &erow_s[0], lsm, wbad_s[0]);
+            factor_one_pair<K>(c, t3, Pt, MS, w2, bar, ecode, &eplane_s[0], &erow_s[0], lsm, wbad_s[0], car);
     }
     __syncthreads();
     if (threadIdx.x == 0) {

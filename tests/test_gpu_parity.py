@@ -52,9 +52,10 @@ def test_factor_bands_match_reference(ntd, golden):
         pre = ntd.factor_level3(a)
         want = golden[name + "/pre"]
         got = pre.host()
-        # l2,u2,l3,u3 are copies / elementwise corrections: compare per band
+        # the setup's nested solves follow the reference's chain order
+        # (CHAIN_LANES = 4): every band is bitwise the reference's
         for i in range(7):
-            assert rel(got[i], want[i]) <= APPLY_TOL, (name, i, rel(got[i], want[i]))
+            assert np.array_equal(got[i], want[i]), (name, i, rel(got[i], want[i]))
 
 
 def test_ntd_apply_matches_reference(ntd, golden):
