@@ -332,6 +332,8 @@ def run_ntd(args):
                          "traffic_unit": "bytes per launch (ncu dram read+write)",
                          "bytes_per_unknown": NTD_APPLY_BYTES_PER_UNKNOWN, "apply_ms": 1e3 * t_apply,
                          "apply_munknowns_per_s": n * Bg / t_apply / 1e6,
+                         "concurrent_launches": len(solver.groups),
+                         "aggregate_gbs": NTD_APPLY_BYTES_PER_UNKNOWN * work[0] / t_dev / 1e9,
                          "launches_timed": len(evs)},
             "kernels_ms": {"ntd_apply": 1e3 * t_apply, "ilu0_apply": 1e3 * t_ilu, "spmv": 1e3 * t_spmv},
             "setup_seconds": setup_s,

@@ -156,23 +156,27 @@ class BatchSolver:
         t0 = perf_counter()
         if not D.check_grid_pattern(self.a, self.nx, self.ny, self.nz):
             raise ValueError("band entries coupling across a grid line/plane boundary must be zero")
+        # both factorisations and the symmetric pack for the whole batch, one
+        # launch each (the setup kernels are latency-bound per system, so one
+        # launch of B CTAs costs what one group would); the stream groups
+        # then work on views of these tensors
+        g = (self.nx, self.ny, self.nz, self.batch)
+        pre, st = D.ntd_factor(self.a, *g)
+        bad = [(s, *map(int, st[s])) for s in range(self.batch) if int(st[s, 0])]
+        if bad:
+            s, code, plane, row = bad[0]
+            raise FactorizationError(f"system {s}: " + D.ntd_factor_message(code, plane, row))
+        split = self.n // 2
+        f, st2 = D.ilu0_factor(self.a, *g, split)
+        bad = [s for s in range(self.batch) if int(st2[s, 0])]
+        if bad:
+            raise FactorizationError(f"system {bad[0]}: zero or non-finite pivot at row {int(st2[bad[0], 2])}")
+        a4 = D.sym_pack(self.a, *g)  # symmetric 4-band operator for the stencil kernels
         for grp in self.groups:
-            B = grp.hi - grp.lo
-            g = (self.nx, self.ny, self.nz, B)
-            pre, st = D.ntd_factor(grp.a, *g)
-            bad = [(s, *map(int, st[s])) for s in range(B) if int(st[s, 0])]
-            if bad:
-                s, code, plane, row = bad[0]
-                raise FactorizationError(f"system {grp.lo + s}: " + D.ntd_factor_message(code, plane, row))
-            split = self.n // 2
-            f, st2 = D.ilu0_factor(grp.a, *g, split)
-            bad = [s for s in range(B) if int(st2[s, 0])]
-            if bad:
-                raise FactorizationError(f"system {grp.lo + bad[0]}: zero or non-finite pivot at row "
-                                         f"{int(st2[bad[0], 2])}")
-            a4 = D.sym_pack(grp.a, *g)  # symmetric 4-band operator for the stencil kernels
-            grp.pcg.a4 = a4
-            grp.precond = D.CombinedDevice(grp.a, *g, pre=pre, ilu=f, split=split, a4=a4)
+            lo, hi = grp.lo, grp.hi
+            grp.pcg.a4 = None if a4 is None else a4[lo:hi]
+            grp.precond = D.CombinedDevice(grp.a, self.nx, self.ny, self.nz, hi - lo, pre=pre[lo:hi], ilu=f[lo:hi],
+                                           split=split, a4=grp.pcg.a4)
         torch.cuda.synchronize()
         self.setup_seconds = perf_counter() - t0
         return self

@@ -25,7 +25,7 @@ v = torch.rand_like(b)
 x = torch.empty_like(b)
 for _ in range(2):
     D.ntd_apply(s.precond.pre, v, nx, ny, nz, B, x=x, solve=s.precond.solve)
-    D.ilu0_apply(s.precond.ilu, s.precond.split, v, nx, ny, nz, B, z=x)
-    D.residual(a, v, x, nx, ny, nz, B)
+    D.ilu0_apply(s.precond.ilu, s.precond.split, v, nx, ny, nz, B, z=x, skew=s.precond.skew)
+    D.residual(a, v, x, nx, ny, nz, B, a4=s.precond.a4)
 torch.cuda.synchronize()
 print("ok")
