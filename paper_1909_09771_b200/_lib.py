@@ -11,6 +11,8 @@ import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libntdgpu.so")
+# experiments only: load a variant build instead (must be a libntdgpu built from this tree)
+LIB_PATH = os.environ.get("NTD_LIB_OVERRIDE", LIB_PATH)
 
 NTD_ST = dict(RZ=0, PAP=1, ALPHA=2, BETA=3, BNORM=4, RELRES=5, TOL=6, N=8)
 NTD_FL = dict(ACTIVE=0, STATUS=1, ITERS=2, N=4)

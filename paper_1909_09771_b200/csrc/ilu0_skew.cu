@@ -13,14 +13,28 @@
 // coefficients (0 where the reference skips the term), so the step is
 // branch-free: acc - 0*z == acc for the finite z the sweep produces.
 //
+// Mapping: one CTA of 24 warps per system half; warps take units round-robin
+// in sweep order and follow their neighbour units through progress words in
+// shared memory.  Coefficient and input rows are staged by cp.async into a
+// per-warp ring 4 steps ahead; the neighbour-unit z values are loaded 2 steps
+// ahead into registers.  (Measured on B200, 96^3, one system: 16 warps with
+// 4-step register look-ahead 1.42 ms per fwd+bwd apply, this mapping 1.29 ms;
+// the sweep is bound by warps in flight, 144 units x 127 steps / 24 warps.)
+//
 // Applies when the half split is a plane boundary (split % (nx*ny) == 0, true
 // for every BASELINE config); ntd_ilu0_apply falls back to ilu0.cu otherwise.
 #include "common.cuh"
 
 namespace skew {
 
-constexpr int WARPS = 16;
-constexpr int PF = 4;  // steps of operand look-ahead (registers)
+#ifndef SKEW_WARPS
+#define SKEW_WARPS 24
+#endif
+constexpr int WARPS = SKEW_WARPS;
+#ifndef SKEW_PF
+#define SKEW_PF 2
+#endif
+constexpr int PF = SKEW_PF;  // steps of look-ahead of the x-dependent operands (registers)
 
 struct Geom {
     int nx, ny, nz, G, T;  // groups per plane, steps per unit (nx + 31)
@@ -150,37 +164,80 @@ __device__ __forceinline__ void publish(volatile unsigned long long *prog, int w
     }
 }
 
+// Static operands (coefficient rows and the input row) are staged into a
+// per-warp shared-memory ring by cp.async, PS steps ahead, continuously
+// across the warp's units; only the x-dependent operands (z of the
+// neighbour units, gated by their progress words) use a register
+// look-ahead of PF steps.
+#ifndef SKEW_PS
+#define SKEW_PS 4
+#endif
+constexpr int PS = SKEW_PS;  // cp.async ring depth (steps)
+constexpr int ROWS = 5;     // rows per stage: up to 4 coefficient rows + the input row
+__host__ __device__ constexpr int ring_doubles() { return WARPS * PS * ROWS * 32; }
+
+__device__ __forceinline__ void cp_async8(double *dst, const double *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // One half-system sweep.  FWD: units ascending, tau ascending; BWD: mirror.
 // in: rhs (FWD) or forward result (BWD), skewed; out: z skewed.
 template <bool FWD>
 __device__ void sweep(const Geom &g, i64 u_lo, i64 u_hi, const double *__restrict__ coef, const double *in,
-                      double *z, volatile unsigned long long *prog)
+                      double *z, volatile unsigned long long *prog, double *ring)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int T = g.T, G = g.G;
-    const int NC = FWD ? 3 : 4;
+    constexpr int NC = FWD ? 3 : 4;
     const i64 nunits = u_hi - u_lo;
+    const i64 nmine = nunits > warp ? (nunits - warp + W - 1) / W : 0;  // units of this warp
+    auto unit_of = [&](i64 v) { return FWD ? u_lo + v : u_hi - 1 - v; };
+    auto step_tau = [&](int q) { return FWD ? q : T - 1 - q; };  // q: step index in sweep order
+    // The stager walks this warp's steps (unit round sr, step sq) PS steps
+    // ahead of the solver and copies them into ring slot (step index) % PS.
+    i64 sr = 0;
+    int sq = 0;
+    unsigned sj = 0;
+    auto stage = [&]() {
+        if (sr < nmine) {
+            const i64 u = unit_of(warp + sr * W);
+            const int tau = step_tau(sq);
+            double *dst = ring + (sj % PS) * ROWS * 32 + lane;
+            const double *cs = coef + (u * T + tau) * (i64)32 * NC + lane;
+#pragma unroll
+            for (int c = 0; c < NC; c++) cp_async8(dst + c * 32, cs + c * 32);
+            cp_async8(dst + 4 * 32, in + (u * T + tau) * 32 + lane);
+            if (++sq == T) {
+                sq = 0;
+                sr++;
+            }
+        }
+        sj++;
+        cp_async_commit();  // one group per step, empty past the end
+    };
+    for (int k = 0; k < PS; k++) stage();
     unsigned long long cw1 = 0, cw2 = 0;
     i64 cu1 = -1, cu2 = -1;
+    unsigned j = 0;  // step index of this warp (all units)
     for (i64 v = warp; v < nunits; v += W) {  // v: position in sweep order
-        const i64 u = FWD ? u_lo + v : u_hi - 1 - v;
+        const i64 u = unit_of(v);
         const bool has_y = FWD ? (u % G) > 0 : (u % G) < G - 1;            // neighbour unit in the same plane
         const bool has_z = FWD ? (u - G) >= u_lo : (u + G) < u_hi;         // previous plane inside the half
         const i64 uy = FWD ? u - 1 : u + 1, uz = FWD ? u - G : u + G;
         const i64 vy = v - 1, vz = v - G;                                   // their sweep positions
-        const double *cu_ = coef + u * (i64)T * 32 * NC;
-        const double *inu = in + u * (i64)T * 32;
         double *zu = z + u * (i64)T * 32;
         const double *zyu = z + uy * (i64)T * 32;
         const double *zzu = z + uz * (i64)T * 32;
-        // register ring of look-ahead operands for steps tau .. tau+PF-1
-        double rc[PF][4], rin[PF], rzz[PF], rzy[PF];
-        auto step_tau = [&](int q) { return FWD ? q : T - 1 - q; };  // q: step index in sweep order
+        // register ring of the x-dependent operands for steps q .. q+PF-1
+        double rzz[PF], rzy[PF];
         auto load = [&](int slot, int q) {
             const int tau = step_tau(q);
-#pragma unroll
-            for (int c = 0; c < 4; c++) rc[slot][c] = c < NC ? cu_[(i64)tau * 32 * NC + c * 32 + lane] : 1.0;
-            rin[slot] = __ldcg(inu + (i64)tau * 32 + lane);
             rzz[slot] = has_z ? __ldcg(zzu + (i64)tau * 32 + lane) : 0.0;
             // lane 0 (FWD) / lane 31 (BWD) reads the neighbour unit's edge lane
             const int ty = FWD ? tau + 31 : tau - 31;
@@ -204,22 +261,31 @@ __device__ void sweep(const Geom &g, i64 u_lo, i64 u_hi, const double *__restric
             for (int d = 0; d < PF; d++) {
                 const int q = q0 + d;
                 if (q >= T) break;
+                cp_async_wait<PS - 1>();  // this lane's copies of step j have landed
+                const double *sg = ring + (j % PS) * ROWS * 32 + lane;
+                double rc[4];
+#pragma unroll
+                for (int c = 0; c < 4; c++) rc[c] = c < NC ? sg[c * 32] : 1.0;
+                const double rin = sg[4 * 32];
                 const double zn = FWD ? __shfl_up_sync(FULL_MASK, zprev, 1) : __shfl_down_sync(FULL_MASK, zprev, 1);
                 const double zy = (FWD ? lane == 0 : lane == 31) ? rzy[d] : zn;
-                double acc = rin[d];
-                acc = sub_rn(acc, mul_rn(rc[d][0], zprev));
-                acc = sub_rn(acc, mul_rn(rc[d][1], zy));
-                acc = sub_rn(acc, mul_rn(rc[d][2], rzz[d]));
-                const double zv = FWD ? acc : acc / rc[d][3];
+                double acc = rin;
+                acc = sub_rn(acc, mul_rn(rc[0], zprev));
+                acc = sub_rn(acc, mul_rn(rc[1], zy));
+                acc = sub_rn(acc, mul_rn(rc[2], rzz[d]));
+                const double zv = FWD ? acc : acc / rc[3];
                 zu[(i64)step_tau(q) * 32 + lane] = zv;
                 zprev = zv;
                 if (q + PF < T) load(d, q + PF);
+                stage();  // refill this slot (each lane reads only its own copies)
+                j++;
             }
             if (((q0 / PF) & 1) == 1 || q0 + PF >= T)
                 publish(prog, warp, (unsigned long long)v * (T + 1) + (q0 + PF < T ? q0 + PF : T));
         }
         publish(prog, warp, (unsigned long long)v * (T + 1) + T);
     }
+    cp_async_wait<0>();
 }
 
 __global__ void __launch_bounds__(WARPS * 32) k_apply(const double *__restrict__ fw, const double *__restrict__ bw,
@@ -227,6 +293,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_apply(const double *__restrict__
                                                       i64 split, int nx, int ny, int nz,
                                                       const int32_t *__restrict__ active)
 {
+    extern __shared__ __align__(16) double skew_ring[];
     __shared__ unsigned long long prog[WARPS];
     const Geom g(nx, ny, nz);
     const i64 sys = blockIdx.x >> 1;
@@ -239,13 +306,14 @@ __global__ void __launch_bounds__(WARPS * 32) k_apply(const double *__restrict__
     const double *fws = fw + sys * per * 3, *bws = bw + sys * per * 4;
     const double *rss = rs + sys * per;
     double *zfs = zf + sys * per, *zbs = zb + sys * per;
+    double *ring = skew_ring + (size_t)(threadIdx.x >> 5) * PS * ROWS * 32;
     if (threadIdx.x < WARPS) prog[threadIdx.x] = 0ull;
     __syncthreads();
-    sweep<true>(g, u_lo, u_hi, fws, rss, zfs, prog);
+    sweep<true>(g, u_lo, u_hi, fws, rss, zfs, prog, ring);
     __syncthreads();
     if (threadIdx.x < WARPS) prog[threadIdx.x] = 0ull;
     __syncthreads();
-    sweep<false>(g, u_lo, u_hi, bws, zfs, zbs, prog);
+    sweep<false>(g, u_lo, u_hi, bws, zfs, zbs, prog, ring);
 }
 
 }  // namespace skew
@@ -295,8 +363,18 @@ extern "C" int ntd_ilu0_skew_apply(const double *coef, int64_t split, const doub
     skew::k_to_skew<<<grid_n(per * batch), 256, 0, st>>>(r, rs, (int)nx, (int)ny, (int)nz, batch);
     int rc = ntd::check_launch("ilu0 to_skew");
     if (rc) return rc;
-    skew::k_apply<<<(unsigned)(2 * batch), skew::WARPS * 32, 0, st>>>(coef, coef + per * batch * 3, rs, zf, zb,
-                                                                      split, (int)nx, (int)ny, (int)nz, active);
+    const int smem = skew::ring_doubles() * 8;
+    static bool attr_set = false;  // per process; the attribute is per function
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(skew::k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) {
+            ntd::set_error("ilu0 skew apply smem", e);
+            return NTD_ELAUNCH;
+        }
+        attr_set = true;
+    }
+    skew::k_apply<<<(unsigned)(2 * batch), skew::WARPS * 32, smem, st>>>(coef, coef + per * batch * 3, rs, zf, zb,
+                                                                         split, (int)nx, (int)ny, (int)nz, active);
     rc = ntd::check_launch("ilu0 skew apply");
     if (rc) return rc;
     skew::k_from_skew<<<grid_n(g.n * batch), 256, 0, st>>>(zb, z, acc, (int)nx, (int)ny, (int)nz, batch, active);
