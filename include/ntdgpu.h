@@ -182,7 +182,9 @@ int ntd_ilu0_apply(const double *f, int64_t split, const double *r, double *z,
  * per-step rows).  Available when split is a multiple of nx*ny:
  * ntd_ilu0_skew_doubles returns 0 otherwise.  coef is built once from the
  * factor f by ntd_ilu0_skew_build; work >= ntd_ilu0_skew_work_doubles.
- * z and/or acc receive the result (acc += z). */
+ * r, z and acc are in the natural (B,N) layout: one kernel gathers r,
+ * sweeps in the skewed layout (scratch in work) and writes z and/or
+ * acc += z (precond_pcg.py:64) directly. */
 int64_t ntd_ilu0_skew_doubles(int64_t nx, int64_t ny, int64_t nz, int64_t batch,
                               int64_t split);
 int ntd_ilu0_skew_build(const double *f, double *coef, int64_t split,

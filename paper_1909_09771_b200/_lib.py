@@ -64,7 +64,7 @@ KERNELS_PER_CALL = {
     "ntd_spmv": 1, "ntd_residual": 1, "ntd_dot": 2, "ntd_pcg_init": 3, "ntd_pcg_start": 3,
     "ntd_pcg_spmv_alpha": 2, "ntd_pcg_update_residual": 3, "ntd_pcg_direction": 3, "ntd_factor": 1,
     "ntd_apply": 3, "ntd_solve_bands": 1, "ntd_ilu0_factor": 2, "ntd_ilu0_apply": 1, "ntd_ilu0_skew_build": 1,
-    "ntd_ilu0_skew_apply": 3, "ntd_sym_pack": 1, "ntd_residual_sym": 1, "ntd_pcg_spmv_alpha_sym": 2,
+    "ntd_ilu0_skew_apply": 1, "ntd_sym_pack": 1, "ntd_residual_sym": 1, "ntd_pcg_spmv_alpha_sym": 2,
     "ntd_pcg_update_residual_sym": 3,
 }
 _launches = [0]

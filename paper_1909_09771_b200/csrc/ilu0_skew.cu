@@ -102,38 +102,21 @@ __global__ void k_build(const double *__restrict__ f, double *__restrict__ fw, d
     }
 }
 
-// natural (B,N) -> skewed (B, units*T*32)
-__global__ void k_to_skew(const double *__restrict__ r, double *__restrict__ rs, int nx, int ny, int nz, i64 batch)
+// natural row of slot (tau, lane) of a unit: base + tau when valid
+struct UnitRow {
+    i64 base;  // nxy*k + nx*(32*grp + lane) - lane
+    bool jv;   // the lane's line exists (32*grp + lane < ny)
+};
+__device__ __forceinline__ UnitRow unit_row(const Geom &g, i64 u, int lane)
 {
-    const Geom g(nx, ny, nz);
-    const i64 per = g.skew_size();
-    for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < per * batch; e += (i64)gridDim.x * blockDim.x) {
-        const i64 s = e / per, el = e - s * per;
-        const i64 u = el / (g.T * 32);
-        const int rem = (int)(el - u * g.T * 32);
-        const i64 row = slot_row(g, u, rem >> 5, rem & 31);
-        rs[e] = row >= 0 ? r[s * g.n + row] : 0.0;
-    }
+    const i64 k = u / g.G;
+    const int grp = (int)(u - k * g.G);
+    const int j = grp * 32 + lane;
+    return UnitRow{g.nxy * k + (i64)g.nx * j - lane, j < g.ny};
 }
-
-// skewed -> natural z (and acc += z, precond_pcg.py:64)
-__global__ void k_from_skew(const double *__restrict__ zs, double *__restrict__ z, double *__restrict__ acc, int nx,
-                            int ny, int nz, i64 batch, const int32_t *__restrict__ active)
+__device__ __forceinline__ bool slot_valid(const Geom &g, const UnitRow &ur, int tau, int lane)
 {
-    const Geom g(nx, ny, nz);
-    const i64 per = g.skew_size();
-    for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < g.n * batch; e += (i64)gridDim.x * blockDim.x) {
-        const i64 s = e / g.n, row = e - s * g.n;
-        if (active && !active[s]) continue;
-        const i64 k = row / g.nxy;
-        const i64 rr = row - k * g.nxy;
-        const int j = (int)(rr / nx), i = (int)(rr - (i64)j * nx);
-        const i64 u = k * g.G + j / 32;
-        const int lane = j & 31, tau = i + lane;
-        const double v = zs[s * per + (u * g.T + tau) * 32 + lane];
-        if (z) z[e] = v;
-        if (acc) acc[e] = add_rn(acc[e], v);
-    }
+    return ur.jv && tau >= lane && tau - lane < g.nx;
 }
 
 // progress word: unit * (T+1) + steps completed
@@ -164,7 +147,9 @@ __device__ __forceinline__ void publish(volatile unsigned long long *prog, int w
     }
 }
 
-// Static operands (coefficient rows and the input row) are staged into a
+// Static operands (coefficient rows, the input row -- gathered from the
+// natural layout in the forward sweep, so no separate conversion pass -- and
+// the accumulator being updated) are staged into a
 // per-warp shared-memory ring by cp.async, PS steps ahead, continuously
 // across the warp's units; only the x-dependent operands (z of the
 // neighbour units, gated by their progress words) use a register
@@ -173,7 +158,7 @@ __device__ __forceinline__ void publish(volatile unsigned long long *prog, int w
 #define SKEW_PS 4
 #endif
 constexpr int PS = SKEW_PS;  // cp.async ring depth (steps)
-constexpr int ROWS = 5;     // rows per stage: up to 4 coefficient rows + the input row
+constexpr int ROWS = 6;     // rows per stage: up to 4 coefficient rows, the input row, acc
 __host__ __device__ constexpr int ring_doubles() { return WARPS * PS * ROWS * 32; }
 
 __device__ __forceinline__ void cp_async8(double *dst, const double *src)
@@ -187,10 +172,14 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // One half-system sweep.  FWD: units ascending, tau ascending; BWD: mirror.
-// in: rhs (FWD) or forward result (BWD), skewed; out: z skewed.
+// FWD: in = rhs in the NATURAL layout (gathered by the stager, 0 on empty
+//      slots), z = forward result, skewed.
+// BWD: in = forward result, skewed; z = result, skewed (read back by the
+//      neighbour units) and also written to the natural-layout outputs:
+//      zout[row] = value and/or acc_out[row] += value (precond_pcg.py:64).
 template <bool FWD>
 __device__ void sweep(const Geom &g, i64 u_lo, i64 u_hi, const double *__restrict__ coef, const double *in,
-                      double *z, volatile unsigned long long *prog, double *ring)
+                      double *z, volatile unsigned long long *prog, double *ring, double *zout, double *acc_out)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int T = g.T, G = g.G;
@@ -204,18 +193,35 @@ __device__ void sweep(const Geom &g, i64 u_lo, i64 u_hi, const double *__restric
     i64 sr = 0;
     int sq = 0;
     unsigned sj = 0;
+    i64 su = nmine > 0 ? unit_of(warp) : 0;
+    UnitRow sur = unit_row(g, su, lane);
     auto stage = [&]() {
         if (sr < nmine) {
-            const i64 u = unit_of(warp + sr * W);
+            const i64 u = su;
             const int tau = step_tau(sq);
             double *dst = ring + (sj % PS) * ROWS * 32 + lane;
             const double *cs = coef + (u * T + tau) * (i64)32 * NC + lane;
 #pragma unroll
             for (int c = 0; c < NC; c++) cp_async8(dst + c * 32, cs + c * 32);
-            cp_async8(dst + 4 * 32, in + (u * T + tau) * 32 + lane);
+            if (FWD || acc_out) {
+                const bool ok = slot_valid(g, sur, tau, lane);  // empty slots have no natural row
+                const i64 row = sur.base + tau;
+                if (FWD) {
+                    if (ok)
+                        cp_async8(dst + 4 * 32, in + row);
+                    else
+                        dst[4 * 32] = 0.0;
+                } else if (ok) {
+                    cp_async8(dst + 5 * 32, acc_out + row);
+                }
+            }
+            if (!FWD) cp_async8(dst + 4 * 32, in + (u * T + tau) * 32 + lane);
             if (++sq == T) {
                 sq = 0;
-                sr++;
+                if (++sr < nmine) {
+                    su = unit_of(warp + sr * W);
+                    sur = unit_row(g, su, lane);
+                }
             }
         }
         sj++;
@@ -232,6 +238,7 @@ __device__ void sweep(const Geom &g, i64 u_lo, i64 u_hi, const double *__restric
         const i64 uy = FWD ? u - 1 : u + 1, uz = FWD ? u - G : u + G;
         const i64 vy = v - 1, vz = v - G;                                   // their sweep positions
         double *zu = z + u * (i64)T * 32;
+        const UnitRow ur = unit_row(g, u, lane);
         const double *zyu = z + uy * (i64)T * 32;
         const double *zzu = z + uz * (i64)T * 32;
         // register ring of the x-dependent operands for steps q .. q+PF-1
@@ -275,6 +282,11 @@ __device__ void sweep(const Geom &g, i64 u_lo, i64 u_hi, const double *__restric
                 acc = sub_rn(acc, mul_rn(rc[2], rzz[d]));
                 const double zv = FWD ? acc : acc / rc[3];
                 zu[(i64)step_tau(q) * 32 + lane] = zv;
+                if (!FWD && slot_valid(g, ur, step_tau(q), lane)) {
+                    const i64 row = ur.base + step_tau(q);
+                    if (zout) zout[row] = zv;
+                    if (acc_out) acc_out[row] = add_rn(sg[5 * 32], zv);
+                }
                 zprev = zv;
                 if (q + PF < T) load(d, q + PF);
                 stage();  // refill this slot (each lane reads only its own copies)
@@ -288,9 +300,10 @@ __device__ void sweep(const Geom &g, i64 u_lo, i64 u_hi, const double *__restric
     cp_async_wait<0>();
 }
 
+// r: rhs (B, N) natural; z / acc: natural outputs (either may be null)
 __global__ void __launch_bounds__(WARPS * 32) k_apply(const double *__restrict__ fw, const double *__restrict__ bw,
-                                                      const double *__restrict__ rs, double *zf, double *zb,
-                                                      i64 split, int nx, int ny, int nz,
+                                                      const double *__restrict__ r, double *zf, double *zb,
+                                                      double *z, double *acc, i64 split, int nx, int ny, int nz,
                                                       const int32_t *__restrict__ active)
 {
     extern __shared__ __align__(16) double skew_ring[];
@@ -304,16 +317,17 @@ __global__ void __launch_bounds__(WARPS * 32) k_apply(const double *__restrict__
     if (u_lo >= u_hi) return;
     const i64 per = g.skew_size();
     const double *fws = fw + sys * per * 3, *bws = bw + sys * per * 4;
-    const double *rss = rs + sys * per;
+    const double *rn = r + sys * g.n;
+    double *zn = z ? z + sys * g.n : nullptr, *an = acc ? acc + sys * g.n : nullptr;
     double *zfs = zf + sys * per, *zbs = zb + sys * per;
     double *ring = skew_ring + (size_t)(threadIdx.x >> 5) * PS * ROWS * 32;
     if (threadIdx.x < WARPS) prog[threadIdx.x] = 0ull;
     __syncthreads();
-    sweep<true>(g, u_lo, u_hi, fws, rss, zfs, prog, ring);
+    sweep<true>(g, u_lo, u_hi, fws, rn, zfs, prog, ring, nullptr, nullptr);
     __syncthreads();
     if (threadIdx.x < WARPS) prog[threadIdx.x] = 0ull;
     __syncthreads();
-    sweep<false>(g, u_lo, u_hi, bws, zfs, zbs, prog, ring);
+    sweep<false>(g, u_lo, u_hi, bws, zfs, zbs, prog, ring, zn, an);
 }
 
 }  // namespace skew
@@ -347,7 +361,7 @@ extern "C" int ntd_ilu0_skew_build(const double *f, double *coef, int64_t split,
 extern "C" int64_t ntd_ilu0_skew_work_doubles(int64_t nx, int64_t ny, int64_t nz, int64_t batch)
 {
     const skew::Geom g((int)nx, (int)ny, (int)nz);
-    return g.skew_size() * batch * 3;  // rhs, forward, backward (skewed)
+    return g.skew_size() * batch * 2;  // forward, backward (skewed)
 }
 
 extern "C" int ntd_ilu0_skew_apply(const double *coef, int64_t split, const double *r, double *z, double *acc,
@@ -359,10 +373,7 @@ extern "C" int ntd_ilu0_skew_apply(const double *coef, int64_t split, const doub
     if (split % g.nxy != 0) return NTD_ENOTSUP;
     cudaStream_t st = (cudaStream_t)stream;
     const i64 per = g.skew_size();
-    double *rs = work, *zf = work + per * batch, *zb = work + 2 * per * batch;
-    skew::k_to_skew<<<grid_n(per * batch), 256, 0, st>>>(r, rs, (int)nx, (int)ny, (int)nz, batch);
-    int rc = ntd::check_launch("ilu0 to_skew");
-    if (rc) return rc;
+    double *zf = work, *zb = work + per * batch;
     const int smem = skew::ring_doubles() * 8;
     static bool attr_set = false;  // per process; the attribute is per function
     if (!attr_set) {
@@ -373,10 +384,8 @@ extern "C" int ntd_ilu0_skew_apply(const double *coef, int64_t split, const doub
         }
         attr_set = true;
     }
-    skew::k_apply<<<(unsigned)(2 * batch), skew::WARPS * 32, smem, st>>>(coef, coef + per * batch * 3, rs, zf, zb,
-                                                                         split, (int)nx, (int)ny, (int)nz, active);
-    rc = ntd::check_launch("ilu0 skew apply");
-    if (rc) return rc;
-    skew::k_from_skew<<<grid_n(g.n * batch), 256, 0, st>>>(zb, z, acc, (int)nx, (int)ny, (int)nz, batch, active);
-    NTD_CHECK_LAUNCH("ilu0 from_skew");
+    skew::k_apply<<<(unsigned)(2 * batch), skew::WARPS * 32, smem, st>>>(coef, coef + per * batch * 3, r, zf, zb, z,
+                                                                         acc, split, (int)nx, (int)ny, (int)nz,
+                                                                         active);
+    NTD_CHECK_LAUNCH("ilu0 skew apply");
 }
