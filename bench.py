@@ -293,6 +293,7 @@ def run_ntd(args):
     torch.cuda.synchronize()
     t_ilu = e4[0].elapsed_time(e4[1]) / 1e3 / R
     t_spmv = e5[0].elapsed_time(e5[1]) / 1e3 / R
+    stencil = stencil_roofline(solver, B, n, nx, ny, nz)
 
     # ---- reductions over ranks (NCCL: max of timings, sum of work, one all_gather of stats)
     from paper_1909_09771_b200 import dist as pdist
@@ -336,6 +337,7 @@ def run_ntd(args):
                          "aggregate_gbs": NTD_APPLY_BYTES_PER_UNKNOWN * work[0] / t_dev / 1e9,
                          "launches_timed": len(evs)},
             "kernels_ms": {"ntd_apply": 1e3 * t_apply, "ilu0_apply": 1e3 * t_ilu, "spmv": 1e3 * t_spmv},
+            "stencil_roofline": stencil,
             "setup_seconds": setup_s,
             "iterations": {"min": min(iters), "max": max(iters), "mean": float(np.mean(iters)),
                            "within_1_of_reference": ref_match, "systems": len(iters)},
@@ -349,6 +351,56 @@ def run_ntd(args):
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def stencil_roofline(solver, B, n, nx, ny, nz):
+    """The bandwidth-bound stencil / CG kernels on the whole shard in one
+    launch each (CUDA events, median of 5): algorithmic bytes per unknown
+    (SURVEY.md 8(d), A as its 4 symmetric bands) / time, against the HBM
+    peak.  north_star asks >= 70% for these."""
+    import torch
+    from paper_1909_09771_b200 import _lib
+    from paper_1909_09771_b200 import device as D
+    a4 = D.sym_pack(solver.a, nx, ny, nz, B)
+    if a4 is None:
+        return None
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    r, w, v = (torch.rand((B, n), dtype=torch.float64, device="cuda", generator=gen) for _ in range(3))
+    t, z = torch.empty_like(r), torch.empty_like(r)
+    cg = D.PcgDevice(solver.a, nx, ny, nz, B, 2, a4=a4)
+    cg.init(r, 1e-30)
+    cg.p.copy_(w)
+    cg.state[:, _lib.NTD_ST["RZ"]] = 1.0
+    peak = _measured_peak()[0]
+
+    def timed(fn):
+        fn()
+        ts = []
+        for _ in range(5):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            e[0].record()
+            fn()
+            e[1].record()
+            torch.cuda.synchronize()
+            ts.append(e[0].elapsed_time(e[1]) / 1e3)
+        return float(np.median(ts))
+
+    cases = {
+        # t = r - A w: A (32) + r, w (16) + t (8)
+        "residual": (56, lambda: D.residual(solver.a, r, w, nx, ny, nz, B, t=t, a4=a4)),
+        # z = v + w, t = r - A z: A (32) + r, v, w (24) + z, t (16)
+        "residual_sum": (72, lambda: D.residual(solver.a, r, w, nx, ny, nz, B, t=t, v=v, z_out=z, a4=a4)),
+        # ap = A p, p.ap: A (32) + p (8) + ap (8)
+        "spmv_dot": (48, lambda: _lib.call("ntd_pcg_spmv_alpha_sym", _lib.ptr(a4), _lib.ptr(cg.p), _lib.ptr(cg.ap),
+                                           _lib.ptr(cg.state), _lib.ptr(cg.flags), _lib.ptr(cg.active), nx, ny, nz,
+                                           B, _lib.ptr(cg.work), _lib.stream())),
+    }
+    out = {}
+    for name, (bpu, fn) in cases.items():
+        dt = timed(fn)
+        gbs = bpu * n * B / dt / 1e9
+        out[name] = {"bytes_per_unknown": bpu, "ms": 1e3 * dt, "achieved_gbs": gbs, "frac": gbs / peak}
+    return out
 
 
 def _traffic(cfg, systems):

@@ -163,6 +163,28 @@ int ntd_apply(const double *pre, const double *solve, const double *b,
               double *x, double *work, int64_t nx, int64_t ny, int64_t nz,
               int64_t batch, const int32_t *active, void *stream);
 
+/* Fused combined-preconditioner stages around the NTD apply (the middle of
+ * precond_pcg.py:57-65), working on the apply's slot-layout buffers in
+ * `work` (>= ntd_apply_work_doubles; zero-filled once by the caller) so the
+ * apply needs no layout conversions.  a: the 7-band operator (bands == 7) or
+ * the ntd_sym_pack operator (bands == 4).  Available when ntd_solve_doubles
+ * is non-zero (NTD_ENOTSUP otherwise).
+ *   ntd_residual_to_slot:   b' = (r - A w) * m_recip into the apply's input
+ *   ntd_apply_slot:         the NTD apply of b' (ntd_solve.py:303-322)
+ *   ntd_residual_from_slot: z_out = x + w, t = r - A z_out (x: the apply's
+ *                           result), bitwise equal to ntd_residual(v = x). */
+int ntd_residual_to_slot(const double *a, int64_t bands, const double *pre,
+                         const double *r, const double *w, double *work,
+                         int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+                         const int32_t *active, void *stream);
+int ntd_apply_slot(const double *solve, double *work, int64_t nx, int64_t ny,
+                   int64_t nz, int64_t batch, const int32_t *active,
+                   void *stream);
+int ntd_residual_from_slot(const double *a, int64_t bands, const double *work,
+                           const double *r, const double *w, double *z_out,
+                           double *t, int64_t nx, int64_t ny, int64_t nz,
+                           int64_t batch, const int32_t *active, void *stream);
+
 /* -------- Block ILU0 (ilu0.py) ------------------------------------------
  * Factor of blkdiag(A[:split,:split], A[split:,split:]) on the 7-band
  * pattern, build_block_ilu0 (ilu0.py:34-92,126-156); bitwise equal to the

@@ -3,8 +3,11 @@
 // compile in parallel.  K = ceil(nx/32) cells per lane per chain.
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "ntd_kernels.cuh"
 #include "ntd_apply_sl.cuh"
+#include "stencil.cuh"
 
 // instantiated K values (ntd_k<K>.cu); a line of nx cells uses the
 // smallest instantiated K >= ceil(nx/32).
@@ -134,6 +137,141 @@ extern "C" int ntd_apply(const double *pre, const double *solve, const double *b
         return ntd::check_launch("ntd_apply from_sl");
     }
     NTD_DISPATCH(launch_apply_k, pre, b, x, work, (int)nx, (int)ny, (int)nz, batch, active, st);
+}
+
+// ------------------------------------------------------------------ fused
+// The combined preconditioner's two residuals (precond_pcg.py:58-63) read /
+// write the NTD apply's slot-layout buffers directly, so the apply needs no
+// layout conversion passes:
+//   t' = (r - A w) m  -> b' of the apply (k_to_sl's b m, same rounding)
+//   z = x + w, t = r - A z with x read from the apply's slot-layout result
+// Both keep the reference summation order (bitwise equal to ntd_residual on
+// the natural-layout vectors).
+template <int NB>
+__global__ void __launch_bounds__(256) k_residual_to_sl(const double *__restrict__ a, const double *__restrict__ pre,
+                                                        const double *__restrict__ r, const double *__restrict__ w,
+                                                        double *__restrict__ bsl, i64 n, int nx, i64 nxy, int K,
+                                                        const int32_t *__restrict__ active)
+{
+    const i64 s = blockIdx.y;
+    if (active && !active[s]) return;
+    const int LR = sl::lr_of(K);
+    const i64 lines = n / nx;
+    const double *as = a + s * NB * n, *ws = w + s * n, *rs = r + s * n, *ms = pre + s * 7 * n + 6 * n;
+    double *bs = bsl + s * lines * LR;
+    for (i64 r0 = blockIdx.x * (i64)blockDim.x + threadIdx.x; r0 < n; r0 += (i64)gridDim.x * blockDim.x) {
+        const double t = sub_rn(rs[r0], row_of<NB>(as, ws, r0, n, nx, nxy));
+        const unsigned line = (unsigned)r0 / (unsigned)nx;
+        const int i = (int)(r0 - (i64)line * nx);
+        bs[(i64)line * LR + sl::sl_index(i, nx, K)] = t * ms[r0];
+    }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(256) k_residual_from_sl(const double *__restrict__ a, const double *__restrict__ r,
+                                                          const double *__restrict__ w, const double *__restrict__ xsl,
+                                                          double *__restrict__ z_out, double *__restrict__ t, i64 n,
+                                                          int nx, i64 nxy, int ny, int K,
+                                                          const int32_t *__restrict__ active)
+{
+    const i64 s = blockIdx.y;
+    if (active && !active[s]) return;
+    const int LR = sl::lr_of(K);
+    const i64 lines = n / nx, plr = (i64)ny * LR;
+    const double *as = a + s * NB * n, *ws = w + s * n, *rs = r + s * n, *xs = xsl + s * lines * LR;
+    double *zs = z_out + s * n, *ts = t + s * n;
+    const double *d0 = as + (NB == 4 ? 0 : 3 * n);
+    const double *lm1 = NB == 4 ? as + n - 1 : as + 2 * n, *lmx = NB == 4 ? as + 2 * n - nx : as + n;
+    const double *lmz = NB == 4 ? as + 3 * n - nxy : as;
+    const double *up1 = as + (NB == 4 ? n : 4 * n), *upx = as + (NB == 4 ? 2 * n : 5 * n);
+    const double *upz = as + (NB == 4 ? 3 * n : 6 * n);
+    for (i64 r0 = blockIdx.x * (i64)blockDim.x + threadIdx.x; r0 < n; r0 += (i64)gridDim.x * blockDim.x) {
+        const unsigned line = (unsigned)r0 / (unsigned)nx;
+        const int i = (int)(r0 - (i64)line * nx);
+        const i64 lb = (i64)line * LR;
+        const int sc = sl::sl_index(i, nx, K);
+        // x at the 7 taps (cell i-1 / i+1 wrap to the neighbouring line, where
+        // the band value is an exact zero: same operands as the natural layout)
+        const i64 pm1 = i > 0 ? lb + sl::sl_index(i - 1, nx, K) : lb - LR + sl::sl_index(nx - 1, nx, K);
+        const i64 pp1 = i < nx - 1 ? lb + sl::sl_index(i + 1, nx, K) : lb + LR + sl::sl_index(0, nx, K);
+#define ZV(idx, pos) add_rn(xs[pos], ws[idx])
+        const double zc = ZV(r0, lb + sc);
+        double sacc = mul_rn(d0[r0], zc);
+        if (r0 >= 1) sacc = add_rn(sacc, mul_rn(lm1[r0], ZV(r0 - 1, pm1)));
+        if (r0 >= nx) sacc = add_rn(sacc, mul_rn(lmx[r0], ZV(r0 - nx, lb - LR + sc)));
+        if (r0 >= nxy) sacc = add_rn(sacc, mul_rn(lmz[r0], ZV(r0 - nxy, lb - plr + sc)));
+        if (r0 + 1 < n) sacc = add_rn(sacc, mul_rn(up1[r0], ZV(r0 + 1, pp1)));
+        if (r0 + nx < n) sacc = add_rn(sacc, mul_rn(upx[r0], ZV(r0 + nx, lb + LR + sc)));
+        if (r0 + nxy < n) sacc = add_rn(sacc, mul_rn(upz[r0], ZV(r0 + nxy, lb + plr + sc)));
+#undef ZV
+        ts[r0] = sub_rn(rs[r0], sacc);
+        zs[r0] = zc;
+    }
+}
+
+static bool slot_path(i64 nx, const double *work, const double *solve, int *K_out)
+{
+    const int K = pick_k(nx);
+    const bool aligned = ((uintptr_t)work % 16 == 0) && (!solve || (uintptr_t)solve % 16 == 0);
+    *K_out = K;
+    return K > 0 && sl_depth(K) && aligned && solve;
+}
+
+extern "C" int ntd_residual_to_slot(const double *a, int64_t bands, const double *pre, const double *r,
+                                    const double *w, double *work, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+                                    const int32_t *active, void *stream)
+{
+    if (!a || !pre || !r || !w || !work || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
+    if (bands != 4 && bands != 7) return NTD_EINVAL;
+    const int K = pick_k(nx);
+    if (K <= 0 || !sl_depth(K) || nx * ny * nz >= (1ll << 31)) return NTD_ENOTSUP;
+    const i64 n = nx * ny * nz;
+    dim3 grid((unsigned)std::min<i64>((n + 255) / 256, 148 * 8), (unsigned)batch);
+    if (bands == 4)
+        k_residual_to_sl<4><<<grid, 256, 0, (cudaStream_t)stream>>>(a, pre, r, w, work, n, (int)nx, nx * ny, K, active);
+    else
+        k_residual_to_sl<7><<<grid, 256, 0, (cudaStream_t)stream>>>(a, pre, r, w, work, n, (int)nx, nx * ny, K, active);
+    return ntd::check_launch("ntd_residual_to_slot");
+}
+
+extern "C" int ntd_apply_slot(const double *solve, double *work, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+                              const int32_t *active, void *stream)
+{
+    if (!solve || !work || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
+    int K;
+    if (!slot_path(nx, work, solve, &K)) return NTD_ENOTSUP;
+    cudaStream_t st = (cudaStream_t)stream;
+    const i64 s = sl_doubles(nx, ny, nz) * batch;
+    double *bsl = work, *xsl = work + s, *xssl = work + 2 * s, *zpl = work + 3 * s;
+    const i64 zn = ny * (i64)sl::lr_of(K);
+    if (cudaMemsetAsync(zpl, 0, sizeof(double) * zn, st) != cudaSuccess) return ntd::check_launch("memset");
+    switch (K) {
+#define SLCASE(KK) \
+    case KK: return launch_apply_sl_k<KK>(solve, bsl, xsl, xssl, zpl, (int)nx, (int)ny, (int)nz, batch, active, st);
+        SLCASE(1) SLCASE(2) SLCASE(3) SLCASE(4) SLCASE(5) SLCASE(6) SLCASE(8) SLCASE(11)
+#undef SLCASE
+    default: return NTD_ENOTSUP;
+    }
+}
+
+extern "C" int ntd_residual_from_slot(const double *a, int64_t bands, const double *work, const double *r,
+                                      const double *w, double *z_out, double *t, int64_t nx, int64_t ny, int64_t nz,
+                                      int64_t batch, const int32_t *active, void *stream)
+{
+    if (!a || !work || !r || !w || !z_out || !t || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
+    if (bands != 4 && bands != 7) return NTD_EINVAL;
+    const int K = pick_k(nx);
+    if (K <= 0 || !sl_depth(K) || nx * ny * nz >= (1ll << 31)) return NTD_ENOTSUP;
+    const i64 n = nx * ny * nz, s = sl_doubles(nx, ny, nz) * batch;
+    const double *xsl = work + s;
+    dim3 grid((unsigned)std::min<i64>((n + 255) / 256, 148 * 8), (unsigned)batch);
+    if (bands == 4)
+        k_residual_from_sl<4><<<grid, 256, 0, (cudaStream_t)stream>>>(a, r, w, xsl, z_out, t, n, (int)nx, nx * ny,
+                                                                      (int)ny, K, active);
+    else
+        k_residual_from_sl<7><<<grid, 256, 0, (cudaStream_t)stream>>>(a, r, w, xsl, z_out, t, n, (int)nx, nx * ny,
+                                                                      (int)ny, K, active);
+    return ntd::check_launch("ntd_residual_from_slot");
 }
 
 extern "C" int64_t ntd_factor_work_doubles(int64_t nx, int64_t ny, int64_t nz, int64_t batch)

@@ -155,8 +155,11 @@ class CombinedDevice:
         self.w = torch.empty(shape, dtype=torch.float64, device=_dev())
         self.t = torch.empty(shape, dtype=torch.float64, device=_dev())
         self.xn = torch.empty(shape, dtype=torch.float64, device=_dev())
-        self.work = torch.empty(_lib.load().ntd_apply_work_doubles(nx, ny, nz, batch), dtype=torch.float64,
+        # zero-filled: the slot-layout padding of the NTD input is never written
+        self.work = torch.zeros(_lib.load().ntd_apply_work_doubles(nx, ny, nz, batch), dtype=torch.float64,
                                 device=_dev())
+        # fused residual <-> NTD apply stages on the slot layout when available
+        self.fused = self.solve is not None and n < 2 ** 31
         self.ntd_events = None  # list: (start, end) CUDA events around every NTD apply (bench timing)
 
     def apply(self, r, z, active=None):
@@ -167,15 +170,28 @@ class CombinedDevice:
             self.skew_work = torch.empty(_lib.load().ntd_ilu0_skew_work_doubles(*g), dtype=torch.float64,
                                          device=_dev())
         ilu0_apply(self.ilu, self.split, r, *g, z=self.w, active=active, skew=self.skew, work=self.skew_work)
-        residual(self.a, r, self.w, *g, t=self.t, active=active, a4=self.a4)
+        op, nb = (self.a, 7) if self.a4 is None else (self.a4, 4)
+        if self.fused:
+            _lib.call("ntd_residual_to_slot", _lib.ptr(op), nb, _lib.ptr(self.pre), _lib.ptr(r), _lib.ptr(self.w),
+                      _lib.ptr(self.work), *g, _lib.ptr(active), _lib.stream())
+        else:
+            residual(self.a, r, self.w, *g, t=self.t, active=active, a4=self.a4)
         if self.ntd_events is not None:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record()
-        ntd_apply(self.pre, self.t, *g, x=self.xn, work=self.work, active=active, solve=self.solve)
+        if self.fused:
+            _lib.call("ntd_apply_slot", _lib.ptr(self.solve), _lib.ptr(self.work), *g, _lib.ptr(active),
+                      _lib.stream())
+        else:
+            ntd_apply(self.pre, self.t, *g, x=self.xn, work=self.work, active=active, solve=self.solve)
         if self.ntd_events is not None:
             ev[1].record()
             self.ntd_events.append(ev)
-        residual(self.a, r, self.w, *g, t=self.t, v=self.xn, z_out=z, active=active, a4=self.a4)
+        if self.fused:
+            _lib.call("ntd_residual_from_slot", _lib.ptr(op), nb, _lib.ptr(self.work), _lib.ptr(r),
+                      _lib.ptr(self.w), _lib.ptr(z), _lib.ptr(self.t), *g, _lib.ptr(active), _lib.stream())
+        else:
+            residual(self.a, r, self.w, *g, t=self.t, v=self.xn, z_out=z, active=active, a4=self.a4)
         if self.skew is not None:
             ilu0_apply(self.ilu, self.split, self.t, *g, z=None, acc=z, active=active, skew=self.skew,
                        work=self.skew_work)

@@ -158,3 +158,31 @@ def test_symmetric_packed_stencil_bitwise(ntd, golden):
     B = A.clone()
     B[0, 2, 1] += 1e-3  # A[1][0] != A[0][1]
     assert D.sym_pack(B, nx, ny, nz, 1) is None
+
+
+def test_fused_slot_stages_bitwise(ntd, golden):
+    """The combined apply with the residuals fused into the NTD apply's slot
+    layout (ntd_residual_to_slot / ntd_apply_slot / ntd_residual_from_slot)
+    is bitwise the unfused sequence (natural-layout residuals + ntd_apply),
+    with the 7-band and the symmetric 4-band operator."""
+    import torch
+    from paper_1909_09771_b200 import device as D
+    for name in names(golden):
+        nx, ny, nz = grid_of(name)
+        n = nx * ny * nz
+        a = ntd.BandedMatrix(nx, ny, nz, golden[name + "/A"])
+        A = a.device_data().reshape(1, 7, n)
+        if n < 2:
+            continue
+        pre = ntd.factor_level3(a).bands.reshape(1, 7, n)
+        g = ntd.build_block_ilu0(a)
+        f = g.device_data.reshape(1, 7, n)
+        r = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, (1, n))).cuda()
+        for a4 in ("auto", None):
+            cd = D.CombinedDevice(A, nx, ny, nz, 1, pre=pre, ilu=f, split=g.split, a4=a4)
+            if not cd.fused:
+                continue
+            z1 = cd.apply(r, torch.empty_like(r)).clone()
+            cd.fused = False
+            z2 = cd.apply(r, torch.empty_like(r)).clone()
+            assert torch.equal(z1, z2), (name, a4)
