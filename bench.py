@@ -326,7 +326,7 @@ def run_ntd(args):
                        "l2": "inputs larger than L2 (each batch vector %.0f MB)" % (8 * n * B / 1e6)},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n * B * world,
                     "d2h_bytes_per_step": 8 * n * B * world},
-            "roofline": {"kernel": "ntd_apply entry (to_sl + sl::k_apply + from_sl), timed-region launches, rank 0",
+            "roofline": {"kernel": "NTD apply sweep sl::k_apply (ntd_apply_slot), timed-region launches, rank 0",
                          "bound": "hbm",
                          "achieved": achieved, "peak": peak[0], "unit": "GB/s", "frac": achieved / peak[0],
                          "peak_source": peak[1], "traffic": _traffic(cfg, Bg),

@@ -761,7 +761,19 @@ static double sdot(const double *x, const double *y, i64 n)
     return s;
 }
 
-/* precond_pcg.py:68-122 (pcg).  kind: 0 none, 1 ntd+ilu0 (pre, ilu given).
+/* preconditioner of kind 1 (ntd+ilu0, precond_pcg.py:57-65) or 2 (ntd alone,
+ * bench_cli.py:113-121: ntd_apply with the factor), else the identity */
+static void precond(const combined *c, int kind, const double *r, double *z, i64 n)
+{
+    if (kind == 1)
+        combined_apply(c, r, z);
+    else if (kind == 2)
+        orc_ntd_apply(c->pre, r, z, c->nx, c->ny, c->nz, c->lanes, c->nthreads);
+    else
+        memcpy(z, r, sizeof(double) * n);
+}
+
+/* precond_pcg.py:68-122 (pcg).  kind: 0 none, 1 ntd+ilu0, 2 ntd (pre, ilu given).
  * history must hold max_iters doubles.  Returns iterations; *conv set;
  * returns -1 on breakdown (DivergenceError). */
 i64 orc_pcg(const double *a, const double *pre, const double *ilu, i64 nx,
@@ -778,7 +790,7 @@ i64 orc_pcg(const double *a, const double *pre, const double *ilu, i64 nx,
     double bnorm = sqrt(sdot(b, b, n));
     if (bnorm == 0.0) { free(ws); *conv = 1; return 0; }
     memcpy(r, b, sizeof(double) * n);
-    if (kind) combined_apply(&c, r, z); else memcpy(z, r, sizeof(double) * n);
+    precond(&c, kind, r, z, n);
     memcpy(p, z, sizeof(double) * n);
     double rz = sdot(r, z, n);
     i64 it = 0;
@@ -795,7 +807,7 @@ i64 orc_pcg(const double *a, const double *pre, const double *ilu, i64 nx,
         history[it - 1] = relres;
         if (!isfinite(relres)) { it = -2; break; }
         if (relres < tol) { *conv = 1; break; }
-        if (kind) combined_apply(&c, r, z); else memcpy(z, r, sizeof(double) * n);
+        precond(&c, kind, r, z, n);
         double rz_new = sdot(r, z, n);
         double beta = rz_new / rz;
         for (i64 i = 0; i < n; i++) p[i] = beta * p[i] + z[i];

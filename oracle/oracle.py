@@ -150,7 +150,8 @@ def combined_apply(data, pre, f, split, r, nx, ny, nz, lanes=4, nthreads=1):
 
 def pcg(data, b, nx, ny, nz, kind="ntd+ilu0", tol=1e-7, max_iters=200,
         lanes=4, nthreads=1, pre=None, ilu=None):
-    """precond_pcg.py:68-122 with the combined (ntd+ilu0) or no preconditioner.
+    """precond_pcg.py:68-122 with the combined (ntd+ilu0), the ntd-only
+    (bench_cli.py:113-121) or no preconditioner.
     Returns (x, iterations, converged, history).  Factorizations are built
     here unless passed in (pre, (f, split))."""
     data, b = _f64(data), _f64(b)
@@ -162,6 +163,11 @@ def pcg(data, b, nx, ny, nz, kind="ntd+ilu0", tol=1e-7, max_iters=200,
             ilu = build_block_ilu0(data, nx, ny, nz, nthreads=nthreads)
         f, split = ilu
         k = 1
+    elif kind == "ntd":
+        if pre is None:
+            pre = factor_level3(data, nx, ny, nz, lanes, nthreads)
+        f, split = np.zeros(1), 0
+        k = 2
     elif kind == "none":
         pre = np.zeros(1)
         f, split = np.zeros(1), 0
