@@ -181,8 +181,14 @@ class BatchSolver:
         self.setup_seconds = perf_counter() - t0
         return self
 
-    def solve(self, b_dev, tol=1e-8):
+    def solve(self, b_dev, tol=1e-8, x_out=None):
+        """Solve all systems.  x_out: optional device (B, N) tensor that
+        receives the solutions (default: the solver's own buffer), so a caller
+        can copy one solve's x to the host while the next solve runs."""
         b = as_device(b_dev).reshape(self.batch, self.n)
+        x = self.x if x_out is None else x_out.reshape(self.batch, self.n)
+        for grp in self.groups:
+            grp.pcg.x = x[grp.lo:grp.hi]
         cur = torch.cuda.current_stream()
         t0 = perf_counter()
         for grp in self.groups:
@@ -196,7 +202,7 @@ class BatchSolver:
             self.history[grp.lo:grp.hi] = grp.pcg.history
         dt = perf_counter() - t0
         return BatchResult(
-            x=self.x, iterations=[int(v) for v in fl[:, _lib.NTD_FL["ITERS"]]],
+            x=x, iterations=[int(v) for v in fl[:, _lib.NTD_FL["ITERS"]]],
             converged=[int(v) == _lib.PCG_CONVERGED for v in fl[:, _lib.NTD_FL["STATUS"]]],
             final_relres=[float(v) for v in st[:, _lib.NTD_ST["RELRES"]]],
             status=[int(v) for v in fl[:, _lib.NTD_FL["STATUS"]]],
