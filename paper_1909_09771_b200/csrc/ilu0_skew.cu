@@ -23,6 +23,8 @@
 //
 // Applies when the half split is a plane boundary (split % (nx*ny) == 0, true
 // for every BASELINE config); ntd_ilu0_apply falls back to ilu0.cu otherwise.
+#include <stdio.h>
+
 #include "common.cuh"
 
 namespace skew {
@@ -119,17 +121,48 @@ __device__ __forceinline__ bool slot_valid(const Geom &g, const UnitRow &ur, int
     return ur.jv && tau >= lane && tau - lane < g.nx;
 }
 
-// progress word: unit * (T+1) + steps completed
-__device__ __forceinline__ void wait_unit(volatile unsigned long long *prog, int W, i64 unit, int steps, int T,
-                                          unsigned long long &cw, i64 &cu)
+#ifdef SKEW_TIMING
+__device__ unsigned long long g_skew_timing[4];  // cycles waiting, cycles total, steps, units (block 0 only)
+#define SKT_NOW(v) long long v = clock64()
+#define SKT_ADD(slot, val) \
+    if ((threadIdx.x & 31) == 0 && blockIdx.x == 0) atomicAdd(&g_skew_timing[slot], (unsigned long long)(val))
+#else
+#define SKT_NOW(v)
+#define SKT_ADD(slot, val)
+#endif
+
+#ifdef SKEW_CHECK
+// first out-of-bounds access: what (1 coef, 2 in_nat, 3 in_skew, 4 acc_in, 5 zp, 6 zop, 7 aop, 8 zz, 9 zy),
+// block, warp, lane, offset, count; the access itself is then redirected to the base
+__device__ long long g_skc[6];
+__device__ __forceinline__ bool skc_bad(const double *p, const double *base, long long count, int what)
+{
+    if (p >= base && p < base + count) return false;
+    if (atomicCAS((unsigned long long *)&g_skc[0], 0ull, (unsigned long long)what) == 0ull) {
+        g_skc[1] = blockIdx.x;
+        g_skc[2] = threadIdx.x >> 5;
+        g_skc[3] = threadIdx.x & 31;
+        g_skc[4] = p - base;
+        g_skc[5] = count;
+    }
+    return true;
+}
+#define SKC(ptr, base, count, what) skc_bad((ptr), (base), (count), what)
+#else
+#define SKC(ptr, base, count, what)
+#endif
+
+// progress word of a warp: (sweep position of its unit) * (T+1) + steps completed
+// (32-bit: units per half * (T+1) < 2^32 for every grid the kernels take)
+__device__ __forceinline__ void wait_unit(volatile unsigned *prog, int unit, int steps, int T, unsigned &cw, int &cu)
 {
     if (unit < 0) return;
-    const unsigned long long need = (unsigned long long)unit * (T + 1) + (unsigned long long)(steps < T ? steps : T);
+    const unsigned need = (unsigned)unit * (unsigned)(T + 1) + (unsigned)(steps < T ? steps : T);
     if (cu == unit && cw >= need) return;
-    unsigned long long w = 0;
+    unsigned w = 0;
     if ((threadIdx.x & 31) == 0) {
         do {
-            w = prog[unit % W];
+            w = prog[unit % WARPS];
         } while (w < need);
         __threadfence_block();
     }
@@ -138,7 +171,7 @@ __device__ __forceinline__ void wait_unit(volatile unsigned long long *prog, int
     cu = unit;
 }
 
-__device__ __forceinline__ void publish(volatile unsigned long long *prog, int warp, unsigned long long word)
+__device__ __forceinline__ void publish(volatile unsigned *prog, int warp, unsigned word)
 {
     __syncwarp();
     if ((threadIdx.x & 31) == 0) {
@@ -149,15 +182,17 @@ __device__ __forceinline__ void publish(volatile unsigned long long *prog, int w
 
 // Static operands (coefficient rows, the input row -- gathered from the
 // natural layout in the forward sweep, so no separate conversion pass -- and
-// the accumulator being updated) are staged into a
-// per-warp shared-memory ring by cp.async, PS steps ahead, continuously
-// across the warp's units; only the x-dependent operands (z of the
-// neighbour units, gated by their progress words) use a register
-// look-ahead of PF steps.
+// the accumulator being updated) are staged into a per-warp shared-memory
+// ring by cp.async, PS steps ahead, continuously across the warp's units;
+// only the x-dependent operands (z of the neighbour units, gated by their
+// progress words) use a register look-ahead of PF steps.  Every address
+// walks by a constant stride per step and is recomputed once per unit (the
+// sweep is issue-bound: 24 warps share an SM, so instructions per step, not
+// latency, set its speed).
 #ifndef SKEW_PS
 #define SKEW_PS 4
 #endif
-constexpr int PS = SKEW_PS;  // cp.async ring depth (steps)
+constexpr int PS = SKEW_PS;  // cp.async ring depth (steps), a power of two
 constexpr int ROWS = 6;     // rows per stage: up to 4 coefficient rows, the input row, acc
 __host__ __device__ constexpr int ring_doubles() { return WARPS * PS * ROWS * 32; }
 
@@ -178,136 +213,210 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 //      neighbour units) and also written to the natural-layout outputs:
 //      zout[row] = value and/or acc_out[row] += value (precond_pcg.py:64).
 template <bool FWD>
-__device__ void sweep(const Geom &g, i64 u_lo, i64 u_hi, const double *__restrict__ coef, const double *in,
-                      double *z, volatile unsigned long long *prog, double *ring, double *zout, double *acc_out)
+__device__ void sweep(const Geom &g, int u_lo, int u_hi, const double *__restrict__ coef, const double *in,
+                      double *z, volatile unsigned *prog, double *ring, double *zout, double *acc_out)
 {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
-    const int T = g.T, G = g.G;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int T = g.T, G = g.G, nx = g.nx;
     constexpr int NC = FWD ? 3 : 4;
-    const i64 nunits = u_hi - u_lo;
-    const i64 nmine = nunits > warp ? (nunits - warp + W - 1) / W : 0;  // units of this warp
-    auto unit_of = [&](i64 v) { return FWD ? u_lo + v : u_hi - 1 - v; };
-    auto step_tau = [&](int q) { return FWD ? q : T - 1 - q; };  // q: step index in sweep order
-    // The stager walks this warp's steps (unit round sr, step sq) PS steps
-    // ahead of the solver and copies them into ring slot (step index) % PS.
-    i64 sr = 0;
-    int sq = 0;
-    unsigned sj = 0;
-    i64 su = nmine > 0 ? unit_of(warp) : 0;
-    UnitRow sur = unit_row(g, su, lane);
+    constexpr int dt = FWD ? 1 : -1;  // tau step
+    const int nunits = u_hi - u_lo;
+    const int nmine = nunits > warp ? (nunits - warp + WARPS - 1) / WARPS : 0;  // units of this warp
+    auto unit_of = [&](int v) { return FWD ? u_lo + v : u_hi - 1 - v; };
+    const int tau0 = FWD ? 0 : T - 1;
+    const bool has_zo = zout != nullptr, has_ao = acc_out != nullptr;
+    // natural row of (unit u, lane, tau) is rowbase(u) + tau; the lane's slot
+    // holds a cell when its line exists and 0 <= tau - lane < nx
+    auto rowbase = [&](int u) {
+        const int k = u / G, grp = u - k * G;
+        return g.nxy * k + (i64)nx * (grp * 32 + lane) - lane;
+    };
+    auto jvalid = [&](int u) { return (u % G) * 32 + lane < g.ny; };
+    // ---- stager: unit round sr, step sq, running pointers
+    int sr = 0, sq = 0, stau = tau0;
+    unsigned sslot = 0;
+    bool sjv = false;
+    const double *scs = coef, *sin = in;
+    double *sacc = acc_out;
+    auto stage_unit = [&]() {
+        const int u = unit_of(warp + sr * WARPS);
+        const i64 rb = rowbase(u);
+        sjv = jvalid(u);
+        stau = tau0;
+        scs = coef + ((i64)u * T + tau0) * (32 * NC) + lane;
+        sin = FWD ? in + rb + tau0 : in + ((i64)u * T + tau0) * 32 + lane;
+        if (!FWD && has_ao) sacc = acc_out + rb + tau0;
+    };
+    if (nmine > 0) stage_unit();
     auto stage = [&]() {
         if (sr < nmine) {
-            const i64 u = su;
-            const int tau = step_tau(sq);
-            double *dst = ring + (sj % PS) * ROWS * 32 + lane;
-            const double *cs = coef + (u * T + tau) * (i64)32 * NC + lane;
+            double *dst = ring + sslot * (ROWS * 32) + lane;
 #pragma unroll
-            for (int c = 0; c < NC; c++) cp_async8(dst + c * 32, cs + c * 32);
-            if (FWD || acc_out) {
-                const bool ok = slot_valid(g, sur, tau, lane);  // empty slots have no natural row
-                const i64 row = sur.base + tau;
-                if (FWD) {
-                    if (ok)
-                        cp_async8(dst + 4 * 32, in + row);
-                    else
-                        dst[4 * 32] = 0.0;
-                } else if (ok) {
-                    cp_async8(dst + 5 * 32, acc_out + row);
+            for (int c = 0; c < NC; c++) {
+                const double *pc = scs + c * 32;
+#ifdef SKEW_CHECK
+                if (SKC(pc, coef, g.skew_size() * NC, 1)) pc = coef;
+#endif
+                cp_async8(dst + c * 32, pc);
+            }
+            const bool ok = sjv && (unsigned)(stau - lane) < (unsigned)nx;
+            if (FWD) {
+                if (ok) {
+                    const double *pi = sin;
+#ifdef SKEW_CHECK
+                    if (SKC(pi, in, g.n, 2)) pi = in;
+#endif
+                    cp_async8(dst + 4 * 32, pi);
+                }
+                else
+                    dst[4 * 32] = 0.0;
+            } else {
+                const double *pi = sin;
+#ifdef SKEW_CHECK
+                if (SKC(pi, in, g.skew_size(), 3)) pi = in;
+#endif
+                cp_async8(dst + 4 * 32, pi);
+                if (has_ao && ok) {
+                    const double *pa = sacc;
+#ifdef SKEW_CHECK
+                    if (SKC(pa, acc_out, g.n, 4)) pa = acc_out;
+#endif
+                    cp_async8(dst + 5 * 32, pa);
                 }
             }
-            if (!FWD) cp_async8(dst + 4 * 32, in + (u * T + tau) * 32 + lane);
+            scs += dt * 32 * NC;
+            sin += FWD ? 1 : -32;
+            sacc += dt;
+            stau += dt;
             if (++sq == T) {
                 sq = 0;
-                if (++sr < nmine) {
-                    su = unit_of(warp + sr * W);
-                    sur = unit_row(g, su, lane);
-                }
+                if (++sr < nmine) stage_unit();
             }
         }
-        sj++;
+        sslot = (sslot + 1) & (PS - 1);
         cp_async_commit();  // one group per step, empty past the end
     };
     for (int k = 0; k < PS; k++) stage();
-    unsigned long long cw1 = 0, cw2 = 0;
-    i64 cu1 = -1, cu2 = -1;
-    unsigned j = 0;  // step index of this warp (all units)
-    for (i64 v = warp; v < nunits; v += W) {  // v: position in sweep order
-        const i64 u = unit_of(v);
-        const bool has_y = FWD ? (u % G) > 0 : (u % G) < G - 1;            // neighbour unit in the same plane
-        const bool has_z = FWD ? (u - G) >= u_lo : (u + G) < u_hi;         // previous plane inside the half
-        const i64 uy = FWD ? u - 1 : u + 1, uz = FWD ? u - G : u + G;
-        const i64 vy = v - 1, vz = v - G;                                   // their sweep positions
-        double *zu = z + u * (i64)T * 32;
-        const UnitRow ur = unit_row(g, u, lane);
-        const double *zyu = z + uy * (i64)T * 32;
-        const double *zzu = z + uz * (i64)T * 32;
+    SKT_NOW(tsw0);
+    unsigned cw1 = 0, cw2 = 0;
+    int cu1 = -1, cu2 = -1;
+    unsigned slot = 0;  // ring slot of the solver's step
+    unsigned jsteps = 0;
+    for (int v = warp; v < nunits; v += WARPS) {  // v: position in sweep order
+        const int u = unit_of(v);
+        const bool has_y = FWD ? (u % G) > 0 : (u % G) < G - 1;  // neighbour unit in the same plane
+        const bool has_z = FWD ? (u - G) >= u_lo : (u + G) < u_hi;  // previous plane inside the half
+        const int uy = FWD ? u - 1 : u + 1, uz = FWD ? u - G : u + G;
+        const int vy = v - 1, vz = v - G;  // their sweep positions
+        const bool jv = jvalid(u);
+        const bool edge = FWD ? lane == 0 : lane == 31;
+        // running pointers at step q = 0 (tau = tau0)
+        double *zp = z + ((i64)u * T + tau0) * 32 + lane;
+        const double *zzp = z + ((i64)uz * T + tau0) * 32 + lane;
+        // neighbour unit's edge lane at tau + 31 (FWD) / tau - 31 (BWD)
+        const double *zyp = z + ((i64)uy * T + tau0 + dt * 31) * 32 + (FWD ? 31 : 0);
+        const i64 rb = rowbase(u);
+        // (pointer arithmetic only; dereferenced only through has_zo / has_ao)
+        double *zop = zout + rb + tau0;
+        double *aop = acc_out + rb + tau0;
         // register ring of the x-dependent operands for steps q .. q+PF-1
         double rzz[PF], rzy[PF];
-        auto load = [&](int slot, int q) {
-            const int tau = step_tau(q);
-            rzz[slot] = has_z ? __ldcg(zzu + (i64)tau * 32 + lane) : 0.0;
-            // lane 0 (FWD) / lane 31 (BWD) reads the neighbour unit's edge lane
-            const int ty = FWD ? tau + 31 : tau - 31;
-            const bool edge = FWD ? lane == 0 : lane == 31;
-            rzy[slot] = (has_y && edge && ty >= 0 && ty < T) ? __ldcg(zyu + (i64)ty * 32 + (FWD ? 31 : 0)) : 0.0;
+        auto load = [&](int slot_, int q) {
+            const double *pz = zzp + (i64)q * dt * 32;
+#ifdef SKEW_CHECK
+            if (has_z && SKC(pz, z, g.skew_size(), 8)) pz = z;
+#endif
+            rzz[slot_] = has_z ? __ldcg(pz) : 0.0;
+            const int ty = FWD ? q + 31 : T - 1 - q - 31;  // neighbour's tau
+            const double *py = zyp + (i64)q * dt * 32;
+#ifdef SKEW_CHECK
+            if (has_y && edge && ty >= 0 && ty < T && SKC(py, z, g.skew_size(), 9)) py = z;
+#endif
+            rzy[slot_] = (has_y && edge && ty >= 0 && ty < T) ? __ldcg(py) : 0.0;
         };
         // dependencies for the first PF steps
-        if (has_y) wait_unit(prog, W, vy, PF + 32, T, cw1, cu1);
-        if (has_z) wait_unit(prog, W, vz, PF, T, cw2, cu2);
+        SKT_NOW(tw0);
+        if (has_y) wait_unit(prog, vy, PF + 32, T, cw1, cu1);
+        if (has_z) wait_unit(prog, vz, PF, T, cw2, cu2);
+        SKT_NOW(tw1);
+        SKT_ADD(0, tw1 - tw0);
+        SKT_ADD(3, 1);
 #pragma unroll
         for (int q = 0; q < PF; q++) load(q, q);
         double zprev = 0.0;
+        int tau = tau0;
         for (int q0 = 0; q0 < T; q0 += PF) {
             // operands of steps q0+PF .. q0+2PF-1 become loadable once the
             // neighbours are that far ahead
             if (q0 + PF < T) {
-                if (has_y) wait_unit(prog, W, vy, q0 + 2 * PF + 32, T, cw1, cu1);
-                if (has_z) wait_unit(prog, W, vz, q0 + 2 * PF, T, cw2, cu2);
+                SKT_NOW(tw2);
+                if (has_y) wait_unit(prog, vy, q0 + 2 * PF + 32, T, cw1, cu1);
+                if (has_z) wait_unit(prog, vz, q0 + 2 * PF, T, cw2, cu2);
+                SKT_NOW(tw3);
+                SKT_ADD(0, tw3 - tw2);
             }
 #pragma unroll
             for (int d = 0; d < PF; d++) {
                 const int q = q0 + d;
                 if (q >= T) break;
-                cp_async_wait<PS - 1>();  // this lane's copies of step j have landed
-                const double *sg = ring + (j % PS) * ROWS * 32 + lane;
-                double rc[4];
-#pragma unroll
-                for (int c = 0; c < 4; c++) rc[c] = c < NC ? sg[c * 32] : 1.0;
+                cp_async_wait<PS - 1>();  // this lane's copies of this step have landed
+                const double *sg = ring + slot * (ROWS * 32) + lane;
+                slot = (slot + 1) & (PS - 1);
                 const double rin = sg[4 * 32];
                 const double zn = FWD ? __shfl_up_sync(FULL_MASK, zprev, 1) : __shfl_down_sync(FULL_MASK, zprev, 1);
-                const double zy = (FWD ? lane == 0 : lane == 31) ? rzy[d] : zn;
+                const double zy = edge ? rzy[d] : zn;
                 double acc = rin;
-                acc = sub_rn(acc, mul_rn(rc[0], zprev));
-                acc = sub_rn(acc, mul_rn(rc[1], zy));
-                acc = sub_rn(acc, mul_rn(rc[2], rzz[d]));
-                const double zv = FWD ? acc : acc / rc[3];
-                zu[(i64)step_tau(q) * 32 + lane] = zv;
-                if (!FWD && slot_valid(g, ur, step_tau(q), lane)) {
-                    const i64 row = ur.base + step_tau(q);
-                    if (zout) zout[row] = zv;
-                    if (acc_out) acc_out[row] = add_rn(sg[5 * 32], zv);
+                acc = sub_rn(acc, mul_rn(sg[0], zprev));
+                acc = sub_rn(acc, mul_rn(sg[32], zy));
+                acc = sub_rn(acc, mul_rn(sg[64], rzz[d]));
+                const double zv = FWD ? acc : acc / sg[96];
+#ifdef SKEW_CHECK
+                if (!SKC(zp, z, g.skew_size(), 5))
+#endif
+                    *zp = zv;
+                if (!FWD && jv && (unsigned)(tau - lane) < (unsigned)nx) {
+                    if (has_zo) {
+#ifdef SKEW_CHECK
+                        if (!SKC(zop, zout, g.n, 6))
+#endif
+                            *zop = zv;
+                    }
+                    if (has_ao) {
+#ifdef SKEW_CHECK
+                        if (!SKC(aop, acc_out, g.n, 7))
+#endif
+                            *aop = add_rn(sg[5 * 32], zv);
+                    }
                 }
                 zprev = zv;
+                zp += dt * 32;
+                if (!FWD) {
+                    zop += dt;
+                    aop += dt;
+                }
+                tau += dt;
                 if (q + PF < T) load(d, q + PF);
-                stage();  // refill this slot (each lane reads only its own copies)
-                j++;
+                stage();  // refill the ring (each lane reads only its own copies)
+                jsteps++;
             }
             if (((q0 / PF) & 1) == 1 || q0 + PF >= T)
-                publish(prog, warp, (unsigned long long)v * (T + 1) + (q0 + PF < T ? q0 + PF : T));
+                publish(prog, warp, (unsigned)v * (T + 1) + (q0 + PF < T ? q0 + PF : T));
         }
-        publish(prog, warp, (unsigned long long)v * (T + 1) + T);
+        publish(prog, warp, (unsigned)v * (T + 1) + T);
     }
     cp_async_wait<0>();
+    SKT_NOW(tsw1);
+    SKT_ADD(1, tsw1 - tsw0);
+    SKT_ADD(2, jsteps);
 }
 
-// r: rhs (B, N) natural; z / acc: natural outputs (either may be null)
 __global__ void __launch_bounds__(WARPS * 32) k_apply(const double *__restrict__ fw, const double *__restrict__ bw,
                                                       const double *__restrict__ r, double *zf, double *zb,
                                                       double *z, double *acc, i64 split, int nx, int ny, int nz,
                                                       const int32_t *__restrict__ active)
 {
     extern __shared__ __align__(16) double skew_ring[];
-    __shared__ unsigned long long prog[WARPS];
+    __shared__ unsigned prog[WARPS];
     const Geom g(nx, ny, nz);
     const i64 sys = blockIdx.x >> 1;
     const int half = blockIdx.x & 1;
@@ -321,11 +430,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_apply(const double *__restrict__
     double *zn = z ? z + sys * g.n : nullptr, *an = acc ? acc + sys * g.n : nullptr;
     double *zfs = zf + sys * per, *zbs = zb + sys * per;
     double *ring = skew_ring + (size_t)(threadIdx.x >> 5) * PS * ROWS * 32;
-    if (threadIdx.x < WARPS) prog[threadIdx.x] = 0ull;
+    if (threadIdx.x < WARPS) prog[threadIdx.x] = 0u;
     __syncthreads();
     sweep<true>(g, u_lo, u_hi, fws, rn, zfs, prog, ring, nullptr, nullptr);
     __syncthreads();
-    if (threadIdx.x < WARPS) prog[threadIdx.x] = 0ull;
+    if (threadIdx.x < WARPS) prog[threadIdx.x] = 0u;
     __syncthreads();
     sweep<false>(g, u_lo, u_hi, bws, zfs, zbs, prog, ring, zn, an);
 }
@@ -389,3 +498,24 @@ extern "C" int ntd_ilu0_skew_apply(const double *coef, int64_t split, const doub
                                                                          active);
     NTD_CHECK_LAUNCH("ilu0 skew apply");
 }
+
+#ifdef SKEW_TIMING
+extern "C" int ntd_skew_timing(unsigned long long *out, int reset)
+{
+    cudaMemcpyFromSymbol(out, skew::g_skew_timing, sizeof(unsigned long long) * 4);
+    if (reset) {
+        unsigned long long z[4] = {0, 0, 0, 0};
+        cudaMemcpyToSymbol(skew::g_skew_timing, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
+
+#ifdef SKEW_CHECK
+extern "C" int ntd_skew_check(long long *out)
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, skew::g_skc, sizeof(long long) * 6);
+    return 0;
+}
+#endif
