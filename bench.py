@@ -301,11 +301,11 @@ def run_ntd(args):
     xa = torch.empty_like(v)
     R = 5
     for _ in range(2):
-        D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, Bg, z=xa, skew=P.skew, work=P.skew_work)
+        D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, Bg, z=xa, skew=P.skew, work=P.skew_work, ctas=P.ilu_ctas)
     e4 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     e4[0].record()
     for _ in range(R):
-        D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, Bg, z=xa, skew=P.skew, work=P.skew_work)
+        D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, Bg, z=xa, skew=P.skew, work=P.skew_work, ctas=P.ilu_ctas)
     e4[1].record()
     e5 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     e5[0].record()

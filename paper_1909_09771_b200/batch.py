@@ -176,7 +176,7 @@ class BatchSolver:
             lo, hi = grp.lo, grp.hi
             grp.pcg.a4 = None if a4 is None else a4[lo:hi]
             grp.precond = D.CombinedDevice(grp.a, self.nx, self.ny, self.nz, hi - lo, pre=pre[lo:hi], ilu=f[lo:hi],
-                                           split=split, a4=grp.pcg.a4)
+                                           split=split, a4=grp.pcg.a4, ilu_ctas=D.ilu0_ctas(self.batch))
         torch.cuda.synchronize()
         self.setup_seconds = perf_counter() - t0
         return self

@@ -152,32 +152,71 @@ __device__ __forceinline__ bool skc_bad(const double *p, const double *base, lon
 #define SKC(ptr, base, count, what)
 #endif
 
-// progress word of a warp: (sweep position of its unit) * (T+1) + steps completed
-// (32-bit: units per half * (T+1) < 2^32 for every grid the kernels take)
-__device__ __forceinline__ void wait_unit(volatile unsigned *prog, int unit, int steps, int T, unsigned &cw, int &cu)
+// Progress words.  The units of a system half are shared by the warps of
+// NC CTAs (a thread-block cluster when NC > 1, so all are co-resident): unit
+// position v belongs to cluster-wide warp v % (NC*WARPS), whose CTA holds
+// its progress word = v * (T+1) + steps completed (32-bit: units per half *
+// (T+1) < 2^32 for every grid the kernels take).  Words are published with
+// release and polled with acquire semantics at cluster scope (the z rows they
+// guard are global memory, read with L2-coherent loads).
+struct Prog {
+    volatile unsigned *local;  // this CTA's words (WARPS)
+    int nc, crank;             // CTAs per half, this CTA's rank in the cluster
+};
+
+__device__ __forceinline__ unsigned prog_read(const Prog &P, int gw)
+{
+    const int cta = gw / WARPS, idx = gw - cta * WARPS;
+    if (P.nc == 1) return P.local[idx];
+    unsigned la = (unsigned)__cvta_generic_to_shared((const void *)(P.local + idx)), ra, w;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(cta));
+    asm volatile("ld.acquire.cluster.shared::cluster.u32 %0, [%1];" : "=r"(w) : "r"(ra) : "memory");
+    return w;
+}
+
+__device__ __forceinline__ void wait_unit(const Prog &P, int WT, int unit, int steps, int T, unsigned &cw, int &cu)
 {
     if (unit < 0) return;
     const unsigned need = (unsigned)unit * (unsigned)(T + 1) + (unsigned)(steps < T ? steps : T);
     if (cu == unit && cw >= need) return;
     unsigned w = 0;
     if ((threadIdx.x & 31) == 0) {
+        long long spins = 0;
         do {
-            w = prog[unit % WARPS];
+            w = prog_read(P, unit % WT);
+            // a protocol error must not hang the GPU: fail the launch instead
+            if (++spins > (1ll << 26)) __trap();
         } while (w < need);
-        __threadfence_block();
+        if (P.nc == 1)
+            __threadfence_block();
+        else
+            asm volatile("fence.acq_rel.cluster;" ::: "memory");
     }
     w = __shfl_sync(FULL_MASK, w, 0);
     cw = w;
     cu = unit;
 }
 
-__device__ __forceinline__ void publish(volatile unsigned *prog, int warp, unsigned word)
+__device__ __forceinline__ void publish(const Prog &P, int warp, unsigned word)
 {
     __syncwarp();
     if ((threadIdx.x & 31) == 0) {
-        __threadfence_block();
-        prog[warp] = word;
+        if (P.nc == 1) {
+            __threadfence_block();
+            P.local[warp] = word;
+        } else {
+            asm volatile("fence.acq_rel.cluster;" ::: "memory");
+            asm volatile("st.relaxed.cluster.shared::cta.u32 [%0], %1;" ::"r"(
+                             (unsigned)__cvta_generic_to_shared((const void *)(P.local + warp))),
+                         "r"(word)
+                         : "memory");
+        }
     }
+}
+
+__device__ __forceinline__ void cluster_sync()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // Static operands (coefficient rows, the input row -- gathered from the
@@ -214,14 +253,15 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 //      zout[row] = value and/or acc_out[row] += value (precond_pcg.py:64).
 template <bool FWD>
 __device__ void sweep(const Geom &g, int u_lo, int u_hi, const double *__restrict__ coef, const double *in,
-                      double *z, volatile unsigned *prog, double *ring, double *zout, double *acc_out)
+                      double *z, const Prog &prog, double *ring, double *zout, double *acc_out)
 {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, lwarp = threadIdx.x >> 5;
+    const int WT = WARPS * prog.nc, warp = prog.crank * WARPS + lwarp;  // cluster-wide warp
     const int T = g.T, G = g.G, nx = g.nx;
     constexpr int NC = FWD ? 3 : 4;
     constexpr int dt = FWD ? 1 : -1;  // tau step
     const int nunits = u_hi - u_lo;
-    const int nmine = nunits > warp ? (nunits - warp + WARPS - 1) / WARPS : 0;  // units of this warp
+    const int nmine = nunits > warp ? (nunits - warp + WT - 1) / WT : 0;  // units of this warp
     auto unit_of = [&](int v) { return FWD ? u_lo + v : u_hi - 1 - v; };
     const int tau0 = FWD ? 0 : T - 1;
     const bool has_zo = zout != nullptr, has_ao = acc_out != nullptr;
@@ -239,7 +279,7 @@ __device__ void sweep(const Geom &g, int u_lo, int u_hi, const double *__restric
     const double *scs = coef, *sin = in;
     double *sacc = acc_out;
     auto stage_unit = [&]() {
-        const int u = unit_of(warp + sr * WARPS);
+        const int u = unit_of(warp + sr * WT);
         const i64 rb = rowbase(u);
         sjv = jvalid(u);
         stau = tau0;
@@ -302,7 +342,7 @@ __device__ void sweep(const Geom &g, int u_lo, int u_hi, const double *__restric
     int cu1 = -1, cu2 = -1;
     unsigned slot = 0;  // ring slot of the solver's step
     unsigned jsteps = 0;
-    for (int v = warp; v < nunits; v += WARPS) {  // v: position in sweep order
+    for (int v = warp; v < nunits; v += WT) {  // v: position in sweep order
         const int u = unit_of(v);
         const bool has_y = FWD ? (u % G) > 0 : (u % G) < G - 1;  // neighbour unit in the same plane
         const bool has_z = FWD ? (u - G) >= u_lo : (u + G) < u_hi;  // previous plane inside the half
@@ -336,8 +376,8 @@ __device__ void sweep(const Geom &g, int u_lo, int u_hi, const double *__restric
         };
         // dependencies for the first PF steps
         SKT_NOW(tw0);
-        if (has_y) wait_unit(prog, vy, PF + 32, T, cw1, cu1);
-        if (has_z) wait_unit(prog, vz, PF, T, cw2, cu2);
+        if (has_y) wait_unit(prog, WT, vy, PF + 32, T, cw1, cu1);
+        if (has_z) wait_unit(prog, WT, vz, PF, T, cw2, cu2);
         SKT_NOW(tw1);
         SKT_ADD(0, tw1 - tw0);
         SKT_ADD(3, 1);
@@ -350,8 +390,8 @@ __device__ void sweep(const Geom &g, int u_lo, int u_hi, const double *__restric
             // neighbours are that far ahead
             if (q0 + PF < T) {
                 SKT_NOW(tw2);
-                if (has_y) wait_unit(prog, vy, q0 + 2 * PF + 32, T, cw1, cu1);
-                if (has_z) wait_unit(prog, vz, q0 + 2 * PF, T, cw2, cu2);
+                if (has_y) wait_unit(prog, WT, vy, q0 + 2 * PF + 32, T, cw1, cu1);
+                if (has_z) wait_unit(prog, WT, vz, q0 + 2 * PF, T, cw2, cu2);
                 SKT_NOW(tw3);
                 SKT_ADD(0, tw3 - tw2);
             }
@@ -400,9 +440,9 @@ __device__ void sweep(const Geom &g, int u_lo, int u_hi, const double *__restric
                 jsteps++;
             }
             if (((q0 / PF) & 1) == 1 || q0 + PF >= T)
-                publish(prog, warp, (unsigned)v * (T + 1) + (q0 + PF < T ? q0 + PF : T));
+                publish(prog, lwarp, (unsigned)v * (T + 1) + (q0 + PF < T ? q0 + PF : T));
         }
-        publish(prog, warp, (unsigned)v * (T + 1) + T);
+        publish(prog, lwarp, (unsigned)v * (T + 1) + T);
     }
     cp_async_wait<0>();
     SKT_NOW(tsw1);
@@ -410,16 +450,20 @@ __device__ void sweep(const Geom &g, int u_lo, int u_hi, const double *__restric
     SKT_ADD(2, jsteps);
 }
 
+// grid: 2 * batch * nc CTAs; CTA b works on system (b / nc) / 2, half
+// (b / nc) % 2, as rank b % nc of its cluster of nc CTAs (nc = 1: no cluster)
 __global__ void __launch_bounds__(WARPS * 32) k_apply(const double *__restrict__ fw, const double *__restrict__ bw,
                                                       const double *__restrict__ r, double *zf, double *zb,
                                                       double *z, double *acc, i64 split, int nx, int ny, int nz,
-                                                      const int32_t *__restrict__ active)
+                                                      const int32_t *__restrict__ active, int nc)
 {
     extern __shared__ __align__(16) double skew_ring[];
-    __shared__ unsigned prog[WARPS];
+    __shared__ unsigned prog_s[WARPS];
     const Geom g(nx, ny, nz);
-    const i64 sys = blockIdx.x >> 1;
-    const int half = blockIdx.x & 1;
+    const int hb = blockIdx.x / nc;
+    const i64 sys = hb >> 1;
+    const int half = hb & 1;
+    // every CTA of a cluster takes the same early exits (same system / half)
     if (active && !active[sys]) return;
     const i64 ksplit = split / g.nxy;
     const i64 u_lo = half ? ksplit * g.G : 0, u_hi = half ? g.units : ksplit * g.G;
@@ -430,13 +474,17 @@ __global__ void __launch_bounds__(WARPS * 32) k_apply(const double *__restrict__
     double *zn = z ? z + sys * g.n : nullptr, *an = acc ? acc + sys * g.n : nullptr;
     double *zfs = zf + sys * per, *zbs = zb + sys * per;
     double *ring = skew_ring + (size_t)(threadIdx.x >> 5) * PS * ROWS * 32;
-    if (threadIdx.x < WARPS) prog[threadIdx.x] = 0u;
-    __syncthreads();
-    sweep<true>(g, u_lo, u_hi, fws, rn, zfs, prog, ring, nullptr, nullptr);
-    __syncthreads();
-    if (threadIdx.x < WARPS) prog[threadIdx.x] = 0u;
-    __syncthreads();
-    sweep<false>(g, u_lo, u_hi, bws, zfs, zbs, prog, ring, zn, an);
+    const Prog P{prog_s, nc, (int)(blockIdx.x % nc)};
+    if (threadIdx.x < WARPS) prog_s[threadIdx.x] = 0u;
+    if (nc > 1) cluster_sync(); else __syncthreads();
+    sweep<true>(g, (int)u_lo, (int)u_hi, fws, rn, zfs, P, ring, nullptr, nullptr);
+    // the backward sweep reads every unit's forward result
+    if (nc > 1) cluster_sync(); else __syncthreads();
+    if (threadIdx.x < WARPS) prog_s[threadIdx.x] = 0u;
+    if (nc > 1) cluster_sync(); else __syncthreads();
+    sweep<false>(g, (int)u_lo, (int)u_hi, bws, zfs, zbs, P, ring, zn, an);
+    // no CTA leaves while another may still poll its progress words
+    if (nc > 1) cluster_sync();
 }
 
 }  // namespace skew
@@ -473,10 +521,22 @@ extern "C" int64_t ntd_ilu0_skew_work_doubles(int64_t nx, int64_t ny, int64_t nz
     return g.skew_size() * batch * 2;  // forward, backward (skewed)
 }
 
+extern "C" int ntd_ilu0_skew_apply_ex(const double *coef, int64_t split, const double *r, double *z, double *acc,
+                                      double *work, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+                                      const int32_t *active, int64_t ctas_per_half, void *stream);
+
 extern "C" int ntd_ilu0_skew_apply(const double *coef, int64_t split, const double *r, double *z, double *acc,
                                    double *work, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
                                    const int32_t *active, void *stream)
 {
+    return ntd_ilu0_skew_apply_ex(coef, split, r, z, acc, work, nx, ny, nz, batch, active, 1, stream);
+}
+
+extern "C" int ntd_ilu0_skew_apply_ex(const double *coef, int64_t split, const double *r, double *z, double *acc,
+                                      double *work, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+                                      const int32_t *active, int64_t ctas_per_half, void *stream)
+{
+    if (ctas_per_half < 1 || ctas_per_half > 8) return NTD_EINVAL;
     if (!coef || !r || !work || (!z && !acc) || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
     const skew::Geom g((int)nx, (int)ny, (int)nz);
     if (split % g.nxy != 0) return NTD_ENOTSUP;
@@ -493,9 +553,30 @@ extern "C" int ntd_ilu0_skew_apply(const double *coef, int64_t split, const doub
         }
         attr_set = true;
     }
-    skew::k_apply<<<(unsigned)(2 * batch), skew::WARPS * 32, smem, st>>>(coef, coef + per * batch * 3, r, zf, zb, z,
-                                                                         acc, split, (int)nx, (int)ny, (int)nz,
-                                                                         active);
+    const int nc = (int)ctas_per_half;
+    if (nc == 1) {
+        skew::k_apply<<<(unsigned)(2 * batch), skew::WARPS * 32, smem, st>>>(
+            coef, coef + per * batch * 3, r, zf, zb, z, acc, split, (int)nx, (int)ny, (int)nz, active, 1);
+        NTD_CHECK_LAUNCH("ilu0 skew apply");
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * batch * nc));
+    cfg.blockDim = dim3(skew::WARPS * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = nc;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, skew::k_apply, coef, (const double *)(coef + per * batch * 3), r, zf,
+                                       zb, z, acc, (i64)split, (int)nx, (int)ny, (int)nz, active, nc);
+    if (e != cudaSuccess) {
+        ntd::set_error("ilu0 skew apply (cluster)", e);
+        return NTD_ELAUNCH;
+    }
     NTD_CHECK_LAUNCH("ilu0 skew apply");
 }
 

@@ -94,17 +94,30 @@ def ilu0_skew_build(f_dev, split, nx, ny, nz, batch):
     return coef
 
 
-def ilu0_apply(f_dev, split, r_dev, nx, ny, nz, batch, z=None, acc=None, active=None, skew=None, work=None):
+SMS = 148
+
+
+def ilu0_ctas(systems_on_gpu):
+    """CTAs per system half for the skewed ILU0 sweep: a cluster of up to 4
+    when the GPU's whole load (all systems, every stream group) leaves SMs
+    idle, else 1 (one CTA per half already fills the GPU)."""
+    return max(1, min(4, SMS // max(1, 2 * systems_on_gpu)))
+
+
+def ilu0_apply(f_dev, split, r_dev, nx, ny, nz, batch, z=None, acc=None, active=None, skew=None, work=None,
+               ctas=None):
     """z = (LU)^-1 r (and/or acc += z).  skew: coefficient records from
-    ilu0_skew_build (fast path); work: scratch for it."""
+    ilu0_skew_build (fast path); work: scratch for it; ctas: CTAs per system
+    half (default: sized for this batch alone, ilu0_ctas)."""
     if z is None and acc is None:
         z = torch.empty_like(r_dev)
     if skew is not None:
         need = _lib.load().ntd_ilu0_skew_work_doubles(nx, ny, nz, batch)
         if work is None or work.numel() < need:
             work = torch.empty(need, dtype=torch.float64, device=_dev())
-        _lib.call("ntd_ilu0_skew_apply", _lib.ptr(skew), split, _lib.ptr(r_dev), _lib.ptr(z), _lib.ptr(acc),
-                  _lib.ptr(work), nx, ny, nz, batch, _lib.ptr(active), _lib.stream())
+        nc = ilu0_ctas(batch) if ctas is None else int(ctas)
+        _lib.call("ntd_ilu0_skew_apply_ex", _lib.ptr(skew), split, _lib.ptr(r_dev), _lib.ptr(z), _lib.ptr(acc),
+                  _lib.ptr(work), nx, ny, nz, batch, _lib.ptr(active), nc, _lib.stream())
         return z
     if z is None:
         z = torch.empty_like(r_dev)
@@ -140,8 +153,9 @@ class CombinedDevice:
     (precond_pcg.py:28-65), all buffers preallocated on the device."""
 
     def __init__(self, a_dev, nx, ny, nz, batch, pre=None, ilu=None, split=None, solve=None, skew=None,
-                 a4="auto"):
+                 a4="auto", ilu_ctas=None):
         self.a, self.nx, self.ny, self.nz, self.batch = a_dev, nx, ny, nz, batch
+        self.ilu_ctas = ilu0_ctas(batch) if ilu_ctas is None else ilu_ctas
         self.a4 = sym_pack(a_dev, nx, ny, nz, batch) if isinstance(a4, str) else a4
         n = nx * ny * nz
         self.n = n
@@ -169,7 +183,8 @@ class CombinedDevice:
         if self.skew is not None and self.skew_work is None:
             self.skew_work = torch.empty(_lib.load().ntd_ilu0_skew_work_doubles(*g), dtype=torch.float64,
                                          device=_dev())
-        ilu0_apply(self.ilu, self.split, r, *g, z=self.w, active=active, skew=self.skew, work=self.skew_work)
+        ilu0_apply(self.ilu, self.split, r, *g, z=self.w, active=active, skew=self.skew, work=self.skew_work,
+                   ctas=self.ilu_ctas)
         op, nb = (self.a, 7) if self.a4 is None else (self.a4, 4)
         if self.fused:
             _lib.call("ntd_residual_to_slot", _lib.ptr(op), nb, _lib.ptr(self.pre), _lib.ptr(r), _lib.ptr(self.w),
@@ -194,7 +209,7 @@ class CombinedDevice:
             residual(self.a, r, self.w, *g, t=self.t, v=self.xn, z_out=z, active=active, a4=self.a4)
         if self.skew is not None:
             ilu0_apply(self.ilu, self.split, self.t, *g, z=None, acc=z, active=active, skew=self.skew,
-                       work=self.skew_work)
+                       work=self.skew_work, ctas=self.ilu_ctas)
         else:
             ilu0_apply(self.ilu, self.split, self.t, *g, z=self.xn, acc=z, active=active)
         return z

@@ -54,7 +54,7 @@ for B in sizes:
     row = {"B": B}
     row["ntd_apply"] = timed(lambda: D.ntd_apply(P.pre, v, nx, ny, nz, B, x=x, work=P.work, solve=P.solve))
     row["ilu0_apply"] = timed(lambda: D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, B, z=x, skew=P.skew,
-                                                   work=P.skew_work))
+                                                   work=P.skew_work, ctas=P.ilu_ctas))
     row["residual"] = timed(lambda: D.residual(a, v, x, nx, ny, nz, B, t=z))
     row["combined"] = timed(lambda: P.apply(v, z))
     res = s.solve(b)
