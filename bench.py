@@ -201,15 +201,20 @@ def run_ntd(args):
     cfg = args.config
     n_total = args.systems or (64 if cfg == 4 else 1)
     mine = shard(n_total, world, rank)
-    inputs = [system_inputs(cfg, s) for s in mine]
-    nx, ny, nz = inputs[0][2]
+    # seeded kappa fields on the host, assembled on the
+    # device (ntd_assemble, bitwise the reference's _assemble_kernel)
+    from paper_1909_09771_b200 import problems
+    nx, ny, nz = problems.CONFIGS[cfg]["grid"]
     n = nx * ny * nz
     B = len(mine)
-    a_host = np.stack([inp[0] for inp in inputs])
-    a_dev = torch.from_numpy(a_host).cuda()
-    del a_host
-    xt_dev = torch.from_numpy(np.stack([inp[1] for inp in inputs])).cuda()
-    del inputs
+    kaps, xts, bc = [], [], None
+    for s in mine:
+        kap, bc, rng = problems.baseline_kappa(cfg, s)
+        kaps.append(kap)
+        xts.append(rng.uniform(-1.0, 1.0, n))
+    a_dev = D.assemble(torch.from_numpy(np.stack(kaps)).cuda(), nx, ny, nz, bc)
+    xt_dev = torch.from_numpy(np.stack(xts)).cuda()
+    del kaps, xts
     b_dev = torch.empty_like(xt_dev)
     _lib.call("ntd_spmv", _lib.ptr(a_dev), _lib.ptr(xt_dev), _lib.ptr(b_dev), nx, ny, nz, B, None, _lib.stream())
     b_host = b_dev.cpu().pin_memory()

@@ -48,6 +48,14 @@ const char *ntd_last_error(void);
 /* Largest nx the line kernels are instantiated for. */
 int64_t ntd_max_nx(void);
 
+/* Cell-centred finite-volume assembly of the 7-point operator a (B,7,N) from
+ * a cellwise kappa (B,N) (problem_gen.py:87-133 _assemble_kernel, same
+ * operation order: bitwise).  dirichlet: bit mask of the Dirichlet faces
+ * (bit 0 x-, 1 x+, 2 y-, 3 y+, 4 z-, 5 z+; 63 = the reference's all-Dirichlet);
+ * a Neumann face adds nothing to the diagonal. */
+int ntd_assemble(const double *kappa, double *a, int64_t nx, int64_t ny,
+                 int64_t nz, int64_t dirichlet, int64_t batch, void *stream);
+
 /* y = A x, bitwise equal to the reference (banded_core.py:95-130, spmv /
  * _spmv_kernel): same summation order, no FMA contraction. */
 int ntd_spmv(const double *a, const double *x, double *y, int64_t nx,

@@ -27,6 +27,7 @@ _SIGS = {
     "ntd_version": (ctypes.c_char_p, []),
     "ntd_last_error": (ctypes.c_char_p, []),
     "ntd_max_nx": (_I, []),
+    "ntd_assemble": (_INT, [_P, _P, _I, _I, _I, _I, _I, _P]),
     "ntd_spmv": (_INT, [_P, _P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_residual": (_INT, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_sym_pack": (_INT, [_P, _P, _P, _I, _I, _I, _I, _P]),
@@ -65,7 +66,7 @@ EXPORTED = tuple(_SIGS)
 # kernels launched by one successful call of each entry point (counted for
 # bench.py's gpu_launches; see the launch sites in csrc/)
 KERNELS_PER_CALL = {
-    "ntd_spmv": 1, "ntd_residual": 1, "ntd_dot": 2, "ntd_pcg_init": 3, "ntd_pcg_start": 3,
+    "ntd_assemble": 1, "ntd_spmv": 1, "ntd_residual": 1, "ntd_dot": 2, "ntd_pcg_init": 3, "ntd_pcg_start": 3,
     "ntd_pcg_spmv_alpha": 2, "ntd_pcg_update_residual": 3, "ntd_pcg_direction": 3, "ntd_factor": 1,
     "ntd_apply": 3, "ntd_solve_bands": 1, "ntd_ilu0_factor": 2, "ntd_ilu0_apply": 1, "ntd_ilu0_skew_build": 1,
     "ntd_ilu0_skew_apply": 1, "ntd_ilu0_skew_apply_ex": 1, "ntd_sym_pack": 1, "ntd_residual_sym": 1, "ntd_pcg_spmv_alpha_sym": 2,

@@ -30,6 +30,18 @@ def ntd_factor_message(code, plane, row):
     return f"plane {plane}: non-finite sandwich adjustment"
 
 
+def assemble(kappa_dev, nx, ny, nz, dirichlet=(True,) * 6):
+    """7-band operators (B,7,N) from cellwise kappa (B, nz, ny, nx) or (B, N)
+    on the device (problem_gen.py:87-133, bitwise); dirichlet: six face flags
+    x-, x+, y-, y+, z-, z+ (False = Neumann)."""
+    k = kappa_dev.reshape(-1, nx * ny * nz).contiguous()
+    batch = k.shape[0]
+    mask = sum(1 << f for f, on in enumerate(dirichlet) if on)
+    a = torch.empty((batch, 7, nx * ny * nz), dtype=torch.float64, device=k.device)
+    _lib.call("ntd_assemble", _lib.ptr(k), _lib.ptr(a), nx, ny, nz, mask, batch, _lib.stream())
+    return a
+
+
 def ntd_factor(a_dev, nx, ny, nz, batch):
     """factor_level3 on B systems.  Returns (pre (B,7,N), status (B,3) host)."""
     lib = _lib.load()

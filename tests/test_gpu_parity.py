@@ -186,3 +186,26 @@ def test_fused_slot_stages_bitwise(ntd, golden):
             cd.fused = False
             z2 = cd.apply(r, torch.empty_like(r)).clone()
             assert torch.equal(z1, z2), (name, a4)
+
+
+def test_device_assembly_bitwise(ntd):
+    """ntd_assemble (problem_gen.py:87-133 on the device) is
+    bitwise the host restatement (itself pinned bitwise to the reference by
+    test_problems.py) on the reference's fields, degenerate grids, and the
+    BASELINE fields including config 2's Neumann faces."""
+    import torch
+    from paper_1909_09771_b200 import device as D
+    from paper_1909_09771_b200 import problems
+    cases = []
+    for field in (1, 2, 3):
+        for grid in ((7, 5, 6), (1, 3, 2), (2, 1, 1), (1, 1, 1), (12, 12, 12)):
+            cases.append((problems.reference_kappa(field, *grid), grid, problems.ALL_DIRICHLET))
+    for cfg, s in ((1, 0), (2, 0), (3, 0), (4, 0), (4, 63)):
+        kap, bc, _ = problems.baseline_kappa(cfg, s)
+        cases.append((kap, problems.CONFIGS[cfg]["grid"], bc))
+    rng = np.random.default_rng(5)
+    cases.append((np.exp(rng.normal(0, 3, (9, 4, 11))), (11, 4, 9), (True, False, False, True, True, False)))
+    for kap, (nx, ny, nz), bc in cases:
+        want = problems.assemble_kappa(kap, nx, ny, nz, bc)
+        got = D.assemble(torch.from_numpy(np.ascontiguousarray(kap)).cuda(), nx, ny, nz, bc)
+        assert np.array_equal(got[0].cpu().numpy(), want), ((nx, ny, nz), bc)
