@@ -188,6 +188,13 @@ int ntd_residual_to_slot(const double *a, int64_t bands, const double *pre,
 int ntd_apply_slot(const double *solve, double *work, int64_t nx, int64_t ny,
                    int64_t nz, int64_t batch, const int32_t *active,
                    void *stream);
+/* ntd_apply_slot with ctas_per_system = 2: the two level-3 halves of each
+ * system run on two SMs (a thread-block cluster), for batches that leave SMs
+ * idle. */
+int ntd_apply_slot_ex(const double *solve, double *work, int64_t nx,
+                      int64_t ny, int64_t nz, int64_t batch,
+                      const int32_t *active, int64_t ctas_per_system,
+                      void *stream);
 int ntd_residual_from_slot(const double *a, int64_t bands, const double *work,
                            const double *r, const double *w, double *z_out,
                            double *t, int64_t nx, int64_t ny, int64_t nz,

@@ -176,7 +176,8 @@ class BatchSolver:
             lo, hi = grp.lo, grp.hi
             grp.pcg.a4 = None if a4 is None else a4[lo:hi]
             grp.precond = D.CombinedDevice(grp.a, self.nx, self.ny, self.nz, hi - lo, pre=pre[lo:hi], ilu=f[lo:hi],
-                                           split=split, a4=grp.pcg.a4, ilu_ctas=D.ilu0_ctas(self.batch))
+                                           split=split, a4=grp.pcg.a4, ilu_ctas=D.ilu0_ctas(self.batch),
+                                           ntd_ctas_=D.ntd_ctas(self.batch))
         torch.cuda.synchronize()
         self.setup_seconds = perf_counter() - t0
         return self

@@ -234,10 +234,20 @@ extern "C" int ntd_residual_to_slot(const double *a, int64_t bands, const double
     return ntd::check_launch("ntd_residual_to_slot");
 }
 
+extern "C" int ntd_apply_slot_ex(const double *solve, double *work, int64_t nx, int64_t ny, int64_t nz,
+                                 int64_t batch, const int32_t *active, int64_t ctas_per_system, void *stream);
+
 extern "C" int ntd_apply_slot(const double *solve, double *work, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
                               const int32_t *active, void *stream)
 {
+    return ntd_apply_slot_ex(solve, work, nx, ny, nz, batch, active, 1, stream);
+}
+
+extern "C" int ntd_apply_slot_ex(const double *solve, double *work, int64_t nx, int64_t ny, int64_t nz,
+                                 int64_t batch, const int32_t *active, int64_t ctas_per_system, void *stream)
+{
     if (!solve || !work || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
+    if (ctas_per_system != 1 && ctas_per_system != 2) return NTD_EINVAL;
     int K;
     if (!slot_path(nx, work, solve, &K)) return NTD_ENOTSUP;
     cudaStream_t st = (cudaStream_t)stream;
@@ -247,7 +257,9 @@ extern "C" int ntd_apply_slot(const double *solve, double *work, int64_t nx, int
     if (cudaMemsetAsync(zpl, 0, sizeof(double) * zn, st) != cudaSuccess) return ntd::check_launch("memset");
     switch (K) {
 #define SLCASE(KK) \
-    case KK: return launch_apply_sl_k<KK>(solve, bsl, xsl, xssl, zpl, (int)nx, (int)ny, (int)nz, batch, active, st);
+    case KK:                                                                                                       \
+        return launch_apply_sl_k<KK>(solve, bsl, xsl, xssl, zpl, (int)nx, (int)ny, (int)nz, batch, active, st,    \
+                                     (int)ctas_per_system);
         SLCASE(1) SLCASE(2) SLCASE(3) SLCASE(4) SLCASE(5) SLCASE(6) SLCASE(8) SLCASE(11)
 #undef SLCASE
     default: return NTD_ENOTSUP;

@@ -62,6 +62,15 @@ __host__ __device__ constexpr int depth_of(int K)
                : (232448 - 1024 - static_smem_of(K)) / (4 * stage_of(K) * 8);
 }
 
+// split kernel (one level-3 half per CTA, 2 solver warps): its own depth
+__host__ __device__ constexpr int static_smem2_of(int K) { return 2 * 2 * (32 * K + 1) * 8 + 2 * 2 * 8 * 8; }
+__host__ __device__ constexpr int depth2_of(int K)
+{
+    return (232448 - 1024 - static_smem2_of(K)) / (2 * stage_of(K) * 8) > 8
+               ? 8
+               : (232448 - 1024 - static_smem2_of(K)) / (2 * stage_of(K) * 8);
+}
+
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(void *bar)
 {
@@ -801,17 +810,26 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
     for (int i = 0; i < cnt; i++) ustep(i, ya, yat);
 }
 
-template <int K, int D>
-__global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ solve, const double *__restrict__ bsl,
-                                                  double *xsl, double *xssl, const double *__restrict__ zpl, int nx,
-                                                  int ny, int nz, const int32_t *__restrict__ active)
+__device__ __forceinline__ void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// NP = 2: one CTA per system, both level-3 halves (warp pairs) on one SM.
+// NP = 1: a cluster of two CTAs per system, one level-3 half each on its own
+// SM (solver and producer warps then each have an SM sub-partition to
+// themselves); the level-3 phase boundaries are cluster barriers.
+template <int K, int D, int NP>
+__global__ void __launch_bounds__(128 * NP, 1) k_apply(const double *__restrict__ solve, const double *__restrict__ bsl,
+                                                       double *xsl, double *xssl, const double *__restrict__ zpl,
+                                                       int nx, int ny, int nz, const int32_t *__restrict__ active)
 {
     extern __shared__ __align__(128) double sl_ring[];
-    __shared__ double ex[2][2 * 2 * (32 * K + 1)];
-    __shared__ __align__(8) unsigned long long bars[4][2 * D];
+    __shared__ double ex[NP][2 * 2 * (32 * K + 1)];
+    __shared__ __align__(8) unsigned long long bars[2 * NP][2 * D];
     constexpr int LR = lr_of(K);
-    const i64 sys = blockIdx.x;
-    if (active && !active[sys]) return;
+    const i64 sys = NP == 2 ? blockIdx.x : blockIdx.x >> 1;
+    if (active && !active[sys]) return;  // both CTAs of a cluster leave together
     const i64 nsl = (i64)nz * ny * LR;
     SlArrays S;
     S.solve = solve + sys * (i64)nz * ny * recd_of(K);
@@ -820,8 +838,9 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
     S.xs = xssl + sys * nsl;
     S.zero = zpl;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool producer = warp >= 4;
-    const int sw = warp & 3, pair = sw >> 1, w2 = sw & 1, bar = 1 + pair;
+    const bool producer = warp >= 2 * NP;
+    const int sw = warp & (2 * NP - 1);  // solver warp this warp is (or feeds)
+    const int pair = NP == 2 ? sw >> 1 : (int)(blockIdx.x & 1), w2 = sw & 1, bar = NP == 2 ? 1 + pair : 1;
     Ring<K, D> R;
     R.base = sl_ring + (size_t)sw * D * stage_of(K);
     R.full = bars[sw];
@@ -834,6 +853,12 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    auto phase_sync = [&]() {
+        if constexpr (NP == 2)
+            __syncthreads();
+        else
+            cluster_sync_all();
+    };
     const LaneSl<K> L(lane);
     Seq Q;
     Q.ny = ny;
@@ -841,7 +866,7 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
     Q.w2 = w2;
     Q.cnt = w2 == 0 ? Q.t2 : (ny - 1 - Q.t2);
     unsigned rec = 0;
-    double *myex = ex[pair];
+    double *myex = ex[NP == 2 ? pair : 0];
     int parity = 0;
     const int t3 = (nz - 1) / 2;
     // The warp pair's plane schedule: level-3 lower sweep (ntd_solve.py:198-221),
@@ -888,7 +913,7 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
         else
             solve_plane<K, D, M_LOWER3, false>(S, desc(i), Q, nx, bar, myex, parity, R, L, rec);
     }
-    __syncthreads();
+    phase_sync();
     if (pair == 0) {
         if (producer) {
             fence_proxy_async();
@@ -897,7 +922,7 @@ __global__ void __launch_bounds__(256, 1) k_apply(const double *__restrict__ sol
             solve_plane<K, D, M_LOWER3, true>(S, desc(nlow), Q, nx, bar, myex, parity, R, L, rec);
         }
     }
-    __syncthreads();
+    phase_sync();
     if (producer) fence_proxy_async();  // x (read as xo) was written by generic stores
     for (int i = nlow + ntw; i < nplanes; i++) {
         if (producer)
@@ -913,7 +938,7 @@ template <int K>
 int launch_prep_sl_k(double *solve, i64 lines_total, cudaStream_t st);
 template <int K>
 int launch_apply_sl_k(const double *solve, const double *bsl, double *xsl, double *xssl, const double *zpl, int nx,
-                      int ny, int nz, i64 batch, const int32_t *active, cudaStream_t st);
+                      int ny, int nz, i64 batch, const int32_t *active, cudaStream_t st, int ctas_per_system = 1);
 
 #define NTD_INSTANTIATE_SL(K)                                                                                     \
     template <>                                                                                                    \
@@ -925,16 +950,45 @@ int launch_apply_sl_k(const double *solve, const double *bsl, double *xsl, doubl
     }                                                                                                              \
     template <>                                                                                                    \
     int launch_apply_sl_k<K>(const double *solve, const double *bsl, double *xsl, double *xssl, const double *zpl,   \
-                             int nx, int ny, int nz, i64 batch, const int32_t *active, cudaStream_t st)            \
+                             int nx, int ny, int nz, i64 batch, const int32_t *active, cudaStream_t st,            \
+                             int ctas_per_system)                                                                  \
     {                                                                                                              \
+        if (ctas_per_system == 2) {                                                                                \
+            constexpr int D2 = sl::depth2_of(K);                                                                   \
+            const size_t smem2 = (size_t)2 * D2 * sl::stage_of(K) * 8;                                             \
+            cudaError_t e2 = cudaFuncSetAttribute(sl::k_apply<K, D2, 1>,                                          \
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);        \
+            if (e2 != cudaSuccess) {                                                                               \
+                ntd::set_error("ntd_apply smem", e2);                                                              \
+                return NTD_ELAUNCH;                                                                                \
+            }                                                                                                      \
+            cudaLaunchConfig_t cfg = {};                                                                           \
+            cfg.gridDim = dim3((unsigned)(2 * batch));                                                             \
+            cfg.blockDim = dim3(128);                                                                              \
+            cfg.dynamicSmemBytes = smem2;                                                                          \
+            cfg.stream = st;                                                                                       \
+            cudaLaunchAttribute attr[1];                                                                           \
+            attr[0].id = cudaLaunchAttributeClusterDimension;                                                      \
+            attr[0].val.clusterDim.x = 2;                                                                          \
+            attr[0].val.clusterDim.y = 1;                                                                          \
+            attr[0].val.clusterDim.z = 1;                                                                          \
+            cfg.attrs = attr;                                                                                      \
+            cfg.numAttrs = 1;                                                                                      \
+            e2 = cudaLaunchKernelEx(&cfg, sl::k_apply<K, D2, 1>, solve, bsl, xsl, xssl, zpl, nx, ny, nz, active);  \
+            if (e2 != cudaSuccess) {                                                                               \
+                ntd::set_error("ntd_apply (cluster)", e2);                                                         \
+                return NTD_ELAUNCH;                                                                                \
+            }                                                                                                      \
+            return ntd::check_launch("ntd_apply");                                                                 \
+        }                                                                                                          \
         constexpr int D = sl::depth_of(K);                                                                         \
         const size_t smem = (size_t)4 * D * sl::stage_of(K) * 8;                                                   \
-        cudaError_t e = cudaFuncSetAttribute(sl::k_apply<K, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+        cudaError_t e = cudaFuncSetAttribute(sl::k_apply<K, D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                              (int)smem);                                                           \
         if (e != cudaSuccess) {                                                                                    \
             ntd::set_error("ntd_apply smem", e);                                                                   \
             return NTD_ELAUNCH;                                                                                    \
         }                                                                                                          \
-        sl::k_apply<K, D><<<(unsigned)batch, 256, smem, st>>>(solve, bsl, xsl, xssl, zpl, nx, ny, nz, active);     \
+        sl::k_apply<K, D, 2><<<(unsigned)batch, 256, smem, st>>>(solve, bsl, xsl, xssl, zpl, nx, ny, nz, active);  \
         return ntd::check_launch("ntd_apply");                                                                     \
     }

@@ -7,6 +7,8 @@ factors (B, 7, N), vectors (B, N) -- and calls libntdgpu.so through the C ABI
 solver both sit on top of these functions.
 """
 
+import os
+
 import torch
 
 from . import _lib
@@ -116,6 +118,18 @@ def ilu0_ctas(systems_on_gpu):
     return max(1, min(4, SMS // max(1, 2 * systems_on_gpu)))
 
 
+def ntd_ctas(systems_on_gpu):
+    """CTAs per system for the NTD apply sweep: 2 (one level-3 half per SM,
+    a cluster of two) while the GPU's systems fit one CTA per SM, else 1.
+    Measured on the config-4 batch: 2 is faster at every size up to 64
+    systems per GPU (4327 -> 4747 Munk-iter/s at 64, 1795 -> 1947 at 16).
+    NTD_APPLY_CTAS=1|2 overrides (experiments)."""
+    env = os.environ.get("NTD_APPLY_CTAS")
+    if env:
+        return int(env)
+    return 2 if 2 * systems_on_gpu <= SMS else 1
+
+
 def ilu0_apply(f_dev, split, r_dev, nx, ny, nz, batch, z=None, acc=None, active=None, skew=None, work=None,
                ctas=None):
     """z = (LU)^-1 r (and/or acc += z).  skew: coefficient records from
@@ -165,9 +179,10 @@ class CombinedDevice:
     (precond_pcg.py:28-65), all buffers preallocated on the device."""
 
     def __init__(self, a_dev, nx, ny, nz, batch, pre=None, ilu=None, split=None, solve=None, skew=None,
-                 a4="auto", ilu_ctas=None):
+                 a4="auto", ilu_ctas=None, ntd_ctas_=None):
         self.a, self.nx, self.ny, self.nz, self.batch = a_dev, nx, ny, nz, batch
         self.ilu_ctas = ilu0_ctas(batch) if ilu_ctas is None else ilu_ctas
+        self.ntd_ctas = ntd_ctas(batch) if ntd_ctas_ is None else ntd_ctas_
         self.a4 = sym_pack(a_dev, nx, ny, nz, batch) if isinstance(a4, str) else a4
         n = nx * ny * nz
         self.n = n
@@ -207,8 +222,8 @@ class CombinedDevice:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record()
         if self.fused:
-            _lib.call("ntd_apply_slot", _lib.ptr(self.solve), _lib.ptr(self.work), *g, _lib.ptr(active),
-                      _lib.stream())
+            _lib.call("ntd_apply_slot_ex", _lib.ptr(self.solve), _lib.ptr(self.work), *g, _lib.ptr(active),
+                      self.ntd_ctas, _lib.stream())
         else:
             ntd_apply(self.pre, self.t, *g, x=self.xn, work=self.work, active=active, solve=self.solve)
         if self.ntd_events is not None:

@@ -32,8 +32,8 @@ int main(int argc, char **argv)
     cudaMemset(bs, 0, 8 * nsl * B); cudaMemset(xs, 0, 8 * nsl * B); cudaMemset(xss, 0, 8 * nsl * B);
     constexpr int D = sl::depth_of(3);
     size_t smem = (size_t)4 * D * sl::stage_of(K) * 8;
-    cudaFuncSetAttribute(sl::k_apply<3, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sl::k_apply<3, D><<<B, 256, smem>>>(sv, bs, xs, xss, zp, nx, ny, nz, nullptr);
+    cudaFuncSetAttribute(sl::k_apply<3, D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sl::k_apply<3, D, 2><<<B, 256, smem>>>(sv, bs, xs, xss, zp, nx, ny, nz, nullptr);
     cudaDeviceSynchronize();
 #ifdef NTD_TIMING
     unsigned long long zero[64] = {0};
@@ -41,7 +41,7 @@ int main(int argc, char **argv)
 #endif
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    sl::k_apply<3, D><<<B, 256, smem>>>(sv, bs, xs, xss, zp, nx, ny, nz, nullptr);
+    sl::k_apply<3, D, 2><<<B, 256, smem>>>(sv, bs, xs, xss, zp, nx, ny, nz, nullptr);
     cudaEventRecord(e1);
     cudaDeviceSynchronize();
     float ms; cudaEventElapsedTime(&ms, e0, e1);
