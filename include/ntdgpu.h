@@ -233,14 +233,15 @@ int ntd_ilu0_skew_apply(const double *coef, int64_t split, const double *r,
                         double *z, double *acc, double *work, int64_t nx,
                         int64_t ny, int64_t nz, int64_t batch,
                         const int32_t *active, void *stream);
-/* The same with ctas_per_half (1..8) CTAs sweeping each system half as a
- * thread-block cluster (progress words in distributed shared memory): more
- * warps in flight per half when the batch leaves SMs idle. */
+/* The same with ctas_per_half (1..8) CTAs of warps_per_cta (1..24) warps
+ * sweeping each system half as a thread-block cluster, one CTA per SM
+ * (progress words in distributed shared memory): more warps in flight and
+ * fewer warps per SM sub-partition when the batch leaves SMs idle. */
 int ntd_ilu0_skew_apply_ex(const double *coef, int64_t split, const double *r,
                            double *z, double *acc, double *work, int64_t nx,
                            int64_t ny, int64_t nz, int64_t batch,
                            const int32_t *active, int64_t ctas_per_half,
-                           void *stream);
+                           int64_t warps_per_cta, void *stream);
 
 #ifdef __cplusplus
 }

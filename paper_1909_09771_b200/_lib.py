@@ -59,7 +59,7 @@ _SIGS = {
     "ntd_ilu0_skew_build": (_INT, [_P, _P, _I, _I, _I, _I, _I, _P]),
     "ntd_ilu0_skew_work_doubles": (_I, [_I, _I, _I, _I]),
     "ntd_ilu0_skew_apply": (_INT, [_P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
-    "ntd_ilu0_skew_apply_ex": (_INT, [_P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _I, _P]),
+    "ntd_ilu0_skew_apply_ex": (_INT, [_P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _P]),
 }
 
 EXPORTED = tuple(_SIGS)

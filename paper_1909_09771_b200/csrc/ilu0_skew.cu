@@ -160,13 +160,13 @@ __device__ __forceinline__ bool skc_bad(const double *p, const double *base, lon
 // release and polled with acquire semantics at cluster scope (the z rows they
 // guard are global memory, read with L2-coherent loads).
 struct Prog {
-    volatile unsigned *local;  // this CTA's words (WARPS)
-    int nc, crank;             // CTAs per half, this CTA's rank in the cluster
+    volatile unsigned *local;  // this CTA's words (nw)
+    int nc, crank, nw;         // CTAs per half, this CTA's rank in the cluster, warps per CTA
 };
 
 __device__ __forceinline__ unsigned prog_read(const Prog &P, int gw)
 {
-    const int cta = gw / WARPS, idx = gw - cta * WARPS;
+    const int cta = gw / P.nw, idx = gw - cta * P.nw;
     if (P.nc == 1) return P.local[idx];
     unsigned la = (unsigned)__cvta_generic_to_shared((const void *)(P.local + idx)), ra, w;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(cta));
@@ -256,7 +256,7 @@ __device__ void sweep(const Geom &g, int u_lo, int u_hi, const double *__restric
                       double *z, const Prog &prog, double *ring, double *zout, double *acc_out)
 {
     const int lane = threadIdx.x & 31, lwarp = threadIdx.x >> 5;
-    const int WT = WARPS * prog.nc, warp = prog.crank * WARPS + lwarp;  // cluster-wide warp
+    const int WT = prog.nw * prog.nc, warp = prog.crank * prog.nw + lwarp;  // cluster-wide warp
     const int T = g.T, G = g.G, nx = g.nx;
     constexpr int NC = FWD ? 3 : 4;
     constexpr int dt = FWD ? 1 : -1;  // tau step
@@ -474,13 +474,14 @@ __global__ void __launch_bounds__(WARPS * 32) k_apply(const double *__restrict__
     double *zn = z ? z + sys * g.n : nullptr, *an = acc ? acc + sys * g.n : nullptr;
     double *zfs = zf + sys * per, *zbs = zb + sys * per;
     double *ring = skew_ring + (size_t)(threadIdx.x >> 5) * PS * ROWS * 32;
-    const Prog P{prog_s, nc, (int)(blockIdx.x % nc)};
-    if (threadIdx.x < WARPS) prog_s[threadIdx.x] = 0u;
+    const int nw = blockDim.x >> 5;
+    const Prog P{prog_s, nc, (int)(blockIdx.x % nc), nw};
+    if (threadIdx.x < nw) prog_s[threadIdx.x] = 0u;
     if (nc > 1) cluster_sync(); else __syncthreads();
     sweep<true>(g, (int)u_lo, (int)u_hi, fws, rn, zfs, P, ring, nullptr, nullptr);
     // the backward sweep reads every unit's forward result
     if (nc > 1) cluster_sync(); else __syncthreads();
-    if (threadIdx.x < WARPS) prog_s[threadIdx.x] = 0u;
+    if (threadIdx.x < nw) prog_s[threadIdx.x] = 0u;
     if (nc > 1) cluster_sync(); else __syncthreads();
     sweep<false>(g, (int)u_lo, (int)u_hi, bws, zfs, zbs, P, ring, zn, an);
     // no CTA leaves while another may still poll its progress words
@@ -523,20 +524,23 @@ extern "C" int64_t ntd_ilu0_skew_work_doubles(int64_t nx, int64_t ny, int64_t nz
 
 extern "C" int ntd_ilu0_skew_apply_ex(const double *coef, int64_t split, const double *r, double *z, double *acc,
                                       double *work, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
-                                      const int32_t *active, int64_t ctas_per_half, void *stream);
+                                      const int32_t *active, int64_t ctas_per_half, int64_t warps_per_cta,
+                                      void *stream);
 
 extern "C" int ntd_ilu0_skew_apply(const double *coef, int64_t split, const double *r, double *z, double *acc,
                                    double *work, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
                                    const int32_t *active, void *stream)
 {
-    return ntd_ilu0_skew_apply_ex(coef, split, r, z, acc, work, nx, ny, nz, batch, active, 1, stream);
+    return ntd_ilu0_skew_apply_ex(coef, split, r, z, acc, work, nx, ny, nz, batch, active, 1, skew::WARPS, stream);
 }
 
 extern "C" int ntd_ilu0_skew_apply_ex(const double *coef, int64_t split, const double *r, double *z, double *acc,
                                       double *work, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
-                                      const int32_t *active, int64_t ctas_per_half, void *stream)
+                                      const int32_t *active, int64_t ctas_per_half, int64_t warps_per_cta,
+                                      void *stream)
 {
-    if (ctas_per_half < 1 || ctas_per_half > 8) return NTD_EINVAL;
+    if (ctas_per_half < 1 || ctas_per_half > 8 || warps_per_cta < 1 || warps_per_cta > skew::WARPS)
+        return NTD_EINVAL;
     if (!coef || !r || !work || (!z && !acc) || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
     const skew::Geom g((int)nx, (int)ny, (int)nz);
     if (split % g.nxy != 0) return NTD_ENOTSUP;
@@ -553,16 +557,19 @@ extern "C" int ntd_ilu0_skew_apply_ex(const double *coef, int64_t split, const d
         }
         attr_set = true;
     }
-    const int nc = (int)ctas_per_half;
+    const int nc = (int)ctas_per_half, nw = (int)warps_per_cta;
     if (nc == 1) {
-        skew::k_apply<<<(unsigned)(2 * batch), skew::WARPS * 32, smem, st>>>(
-            coef, coef + per * batch * 3, r, zf, zb, z, acc, split, (int)nx, (int)ny, (int)nz, active, 1);
+        skew::k_apply<<<(unsigned)(2 * batch), nw * 32, smem, st>>>(coef, coef + per * batch * 3, r, zf, zb, z, acc,
+                                                                    split, (int)nx, (int)ny, (int)nz, active, 1);
         NTD_CHECK_LAUNCH("ilu0 skew apply");
     }
+    // a cluster spreads its CTAs over SMs only if two cannot share one: ask
+    // for more than half of an SM's shared memory
+    const int smem_c = smem > 120 * 1024 ? smem : 120 * 1024;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(2 * batch * nc));
-    cfg.blockDim = dim3(skew::WARPS * 32);
-    cfg.dynamicSmemBytes = smem;
+    cfg.blockDim = dim3(nw * 32);
+    cfg.dynamicSmemBytes = smem_c;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -111,11 +111,24 @@ def ilu0_skew_build(f_dev, split, nx, ny, nz, batch):
 SMS = 148
 
 
+ILU0_WARPS = 24  # warps per CTA of the one-CTA-per-half sweep (skew::WARPS)
+
+
 def ilu0_ctas(systems_on_gpu):
-    """CTAs per system half for the skewed ILU0 sweep: a cluster of up to 4
-    when the GPU's whole load (all systems, every stream group) leaves SMs
-    idle, else 1 (one CTA per half already fills the GPU)."""
-    return max(1, min(4, SMS // max(1, 2 * systems_on_gpu)))
+    """(CTAs per system half, warps per CTA) for the skewed ILU0 sweep: a
+    cluster of up to 4 CTAs on separate SMs when the GPU's whole load (all
+    systems, every stream group) leaves SMs idle, else one 24-warp CTA per
+    half.  NTD_ILU0_CTAS="c,w" overrides (experiments)."""
+    env = os.environ.get("NTD_ILU0_CTAS")
+    if env:
+        c, w = (int(v) for v in env.split(","))
+        return c, w
+    # measured (tools/ilu0_ctas_scan.py, 96^3, ms per apply at 1 / 8 / 16
+    # systems): 1x24 1.25/1.27/1.28, 2x24 1.10/1.12/1.15, 4x12 0.95/0.99/1.03
+    c = max(1, min(4, SMS // max(1, 2 * systems_on_gpu)))
+    if c >= 4:
+        return 4, 12
+    return (2, ILU0_WARPS) if c >= 2 else (1, ILU0_WARPS)
 
 
 def ntd_ctas(systems_on_gpu):
@@ -133,17 +146,18 @@ def ntd_ctas(systems_on_gpu):
 def ilu0_apply(f_dev, split, r_dev, nx, ny, nz, batch, z=None, acc=None, active=None, skew=None, work=None,
                ctas=None):
     """z = (LU)^-1 r (and/or acc += z).  skew: coefficient records from
-    ilu0_skew_build (fast path); work: scratch for it; ctas: CTAs per system
-    half (default: sized for this batch alone, ilu0_ctas)."""
+    ilu0_skew_build (fast path); work: scratch for it; ctas: (CTAs per
+    system half, warps per CTA) (default: sized for this batch alone,
+    ilu0_ctas)."""
     if z is None and acc is None:
         z = torch.empty_like(r_dev)
     if skew is not None:
         need = _lib.load().ntd_ilu0_skew_work_doubles(nx, ny, nz, batch)
         if work is None or work.numel() < need:
             work = torch.empty(need, dtype=torch.float64, device=_dev())
-        nc = ilu0_ctas(batch) if ctas is None else int(ctas)
+        nc, nw = ilu0_ctas(batch) if ctas is None else ctas
         _lib.call("ntd_ilu0_skew_apply_ex", _lib.ptr(skew), split, _lib.ptr(r_dev), _lib.ptr(z), _lib.ptr(acc),
-                  _lib.ptr(work), nx, ny, nz, batch, _lib.ptr(active), nc, _lib.stream())
+                  _lib.ptr(work), nx, ny, nz, batch, _lib.ptr(active), nc, nw, _lib.stream())
         return z
     if z is None:
         z = torch.empty_like(r_dev)

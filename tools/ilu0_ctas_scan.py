@@ -21,7 +21,7 @@ for B in sizes:
     v = torch.rand((B, nx * ny * nz), dtype=torch.float64, device="cuda")
     x = torch.empty_like(v)
     row = []
-    for c in (1, 2, 3, 4, 6, 8):
+    for c in ((1, 24), (2, 24), (4, 24), (2, 12), (4, 12), (4, 8), (8, 6), (8, 8), (4, 6), (8, 12)):
         D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, B, z=x, skew=P.skew, ctas=c)
         e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         e[0].record()
@@ -29,5 +29,5 @@ for B in sizes:
             D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, B, z=x, skew=P.skew, ctas=c)
         e[1].record()
         torch.cuda.synchronize()
-        row.append(f"{c}:{e[0].elapsed_time(e[1]) / 5:.3f}")
+        row.append(f"{c[0]}x{c[1]}:{e[0].elapsed_time(e[1]) / 5:.3f}")
     print(f"B={B} ms by ctas/half:", " ".join(row), flush=True)
