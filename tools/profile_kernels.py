@@ -23,9 +23,12 @@ _lib.call("ntd_spmv", _lib.ptr(a), _lib.ptr(xt), _lib.ptr(b), nx, ny, nz, B, Non
 s = BatchSolver(a, nx, ny, nz, groups=1).setup()
 v = torch.rand_like(b)
 x = torch.empty_like(b)
+P = s.precond
 for _ in range(2):
-    D.ntd_apply(s.precond.pre, v, nx, ny, nz, B, x=x, solve=s.precond.solve)
-    D.ilu0_apply(s.precond.ilu, s.precond.split, v, nx, ny, nz, B, z=x, skew=s.precond.skew)
+    # the NTD sweep as the solver launches it (slot layout, ctas per system)
+    _lib.call("ntd_apply_slot_ex", _lib.ptr(P.solve), _lib.ptr(P.work), nx, ny, nz, B, None, P.ntd_ctas,
+              _lib.stream())
+    D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, B, z=x, skew=P.skew, ctas=P.ilu_ctas)
     D.residual(a, v, x, nx, ny, nz, B, a4=s.precond.a4)
 torch.cuda.synchronize()
 print("ok")
