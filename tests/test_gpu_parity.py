@@ -209,3 +209,40 @@ def test_device_assembly_bitwise(ntd):
         want = problems.assemble_kappa(kap, nx, ny, nz, bc)
         got = D.assemble(torch.from_numpy(np.ascontiguousarray(kap)).cuda(), nx, ny, nz, bc)
         assert np.array_equal(got[0].cpu().numpy(), want), ((nx, ny, nz), bc)
+
+
+def test_sm_mappings_bitwise(ntd):
+    """The ILU0 sweep with one CTA per system half or a cluster of CTAs per
+    half, and the NTD sweep with one or two CTAs per system, give bitwise the
+    same results (config 2 plus a small odd grid, two systems per launch)."""
+    import torch
+    from paper_1909_09771_b200 import _lib, problems
+    from paper_1909_09771_b200 import device as D
+    from paper_1909_09771_b200.batch import BatchSolver
+    grids = [problems.baseline_config(2)]
+    rng = np.random.default_rng(9)
+    kap = np.exp(rng.normal(0, 2, (10, 37, 21)))
+    grids.append((problems.assemble_kappa(kap, 21, 37, 10), None, (21, 37, 10)))
+    for data, _, (nx, ny, nz) in grids:
+        n = nx * ny * nz
+        A = torch.from_numpy(np.stack([data, data])).cuda()
+        s = BatchSolver(A, nx, ny, nz, groups=1).setup()
+        P = s.precond
+        v = torch.from_numpy(rng.uniform(-1, 1, (2, n))).cuda()
+        outs = []
+        for ctas in ((1, 24), (2, 24), (4, 12), (8, 6)):
+            z = torch.empty_like(v)
+            D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, 2, z=z, skew=P.skew, ctas=ctas)
+            outs.append(z)
+        assert all(torch.equal(outs[0], o) for o in outs[1:]), (nx, ny, nz)
+        if P.fused:
+            xs = []
+            for c in (1, 2):
+                P.work.zero_()
+                _lib.call("ntd_residual_to_slot", _lib.ptr(P.a4), 4, _lib.ptr(P.pre), _lib.ptr(v), _lib.ptr(outs[0]),
+                          _lib.ptr(P.work), nx, ny, nz, 2, None, _lib.stream())
+                _lib.call("ntd_apply_slot_ex", _lib.ptr(P.solve), _lib.ptr(P.work), nx, ny, nz, 2, None, c,
+                          _lib.stream())
+                sl = _lib.load().ntd_apply_work_doubles(nx, ny, nz, 2)
+                xs.append(P.work[: sl].clone())
+            assert torch.equal(xs[0], xs[1]), (nx, ny, nz)
