@@ -195,6 +195,10 @@ int ntd_apply_slot_ex(const double *solve, double *work, int64_t nx,
                       int64_t ny, int64_t nz, int64_t batch,
                       const int32_t *active, int64_t ctas_per_system,
                       void *stream);
+/* Measurement switch: 0 disables the split sweep's shared-memory plane
+ * buffers (the solver then reads neighbour and lower-sweep lines from global
+ * memory, as the one-CTA sweep does).  Results are bitwise the same. */
+int ntd_set_smb(int on);
 int ntd_residual_from_slot(const double *a, int64_t bands, const double *work,
                            const double *r, const double *w, double *z_out,
                            double *t, int64_t nx, int64_t ny, int64_t nz,

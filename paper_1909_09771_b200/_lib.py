@@ -52,6 +52,7 @@ _SIGS = {
     "ntd_residual_to_slot": (_INT, [_P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_apply_slot": (_INT, [_P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_apply_slot_ex": (_INT, [_P, _P, _I, _I, _I, _I, _P, _I, _P]),
+    "ntd_set_smb": (_INT, [ctypes.c_int]),
     "ntd_residual_from_slot": (_INT, [_P, _I, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_ilu0_factor": (_INT, [_P, _P, _I, _P, _I, _I, _I, _I, _P]),
     "ntd_ilu0_apply": (_INT, [_P, _I, _P, _P, _P, _I, _I, _I, _I, _P, _P]),

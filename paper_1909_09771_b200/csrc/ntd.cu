@@ -299,3 +299,10 @@ extern "C" int ntd_factor(const double *a, double *pre, double *work, int64_t *s
     int K = pick_k(nx);
     NTD_DISPATCH(launch_factor_k, a, pre, work, status, (int)nx, (int)ny, (int)nz, batch, (cudaStream_t)stream);
 }
+
+// A/B switch for the split sweep's shared-memory plane buffers (experiments)
+extern "C" int ntd_set_smb(int on)
+{
+    sl::g_ntd_smb = on != 0;
+    return 0;
+}

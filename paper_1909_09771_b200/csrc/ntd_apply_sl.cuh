@@ -71,6 +71,15 @@ __host__ __device__ constexpr int depth2_of(int K)
                : (232448 - 1024 - static_smem2_of(K)) / (2 * stage_of(K) * 8);
 }
 
+// SMB split kernel: ring depth left beside the two plane buffers, sized for
+// ny <= 32K+1 (a half-plane of 16K+1 lines per solver warp); < 2: no SMB
+__host__ __device__ constexpr int depth_smb_of(int K)
+{
+    return (232448 - 1024 - static_smem2_of(K) - 2 * (16 * K + 1) * lr_of(K) * 8) / (2 * stage_of(K) * 8) > 8
+               ? 8
+               : (232448 - 1024 - static_smem2_of(K) - 2 * (16 * K + 1) * lr_of(K) * 8) / (2 * stage_of(K) * 8);
+}
+
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(void *bar)
 {
@@ -271,6 +280,7 @@ struct Ring {
 };
 
 struct PlaneDesc {
+    bool nbuf;     // SMB: the level-3 neighbour y1 is the plane this warp processed last (in its smem buffer)
     i64 prec;      // record index of the plane's first line (plane * ny)
     int mode;      // M_LOWER3 / M_UPPER3
     int c1;        // record offset of the level-3 coupling C1 (two: L3 then U3 = C2)
@@ -553,9 +563,15 @@ __device__ __forceinline__ void prefetch_l1(const double *p)
 }
 
 // ---------------- solver: one plane
-template <int K, int D, int MODE, bool TWO>
+// SMB: the warp keeps its half of the plane it processed last in shared
+// memory (pbuf, lines lo_line.. of the half incl. the twist line): each line
+// slot holds the neighbour plane's final x until this plane's lower sweep
+// replaces it with the lower-sweep value, which the upper sweep replaces with
+// this plane's final x.  The solver then issues no global loads per line.
+template <int K, int D, int MODE, bool TWO, bool SMB = false>
 __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q, int nx, int bar_id, double *ex,
-                            int &parity, const Ring<K, D> &R, const LaneSl<K> &L, unsigned &rec)
+                            int &parity, const Ring<K, D> &R, const LaneSl<K> &L, unsigned &rec,
+                            double *pbuf = nullptr)
 {
     constexpr int LR = lr_of(K);
     const int lane = threadIdx.x & 31, w2 = Q.w2;
@@ -580,6 +596,12 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
         y1 = P.nbrUp ? xpl + plr : xpl - plr;
     }
     double *xlow = (lower3 ? S.x : S.xs) + P.prec * LR;  // lower-sweep store of this plane
+    if constexpr (SMB) {
+        // line q of this half lives at pbuf + (q - lo_line) * LR
+        double *bq = pbuf - (i64)(Q.w2 == 0 ? 0 : Q.t2) * LR;
+        xlow = bq;
+        if (P.nbuf) y1 = bq;
+    }
     const int gL = L.desc ? o_nu(K) : o_nl(K), gU = L.desc ? o_nl(K) : o_nu(K);
     auto srec = [&](int off, int q) { return S.solve + (P.prec + q) * (i64)recd_of(K) + off; };
     double xprev[K], xprevt = 0.0;
@@ -724,14 +746,18 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
         const double nlt = srec(o_nl(K), q)[L.tw], nut = srec(o_nu(K), q)[L.tw];
         if (lower3) {
             ld_rec(S.b + (P.prec + q) * LR, L, rhs, rhst);
+            // the neighbours' twist lines: y1 (buffer or global) is plane p-1
+            // unless only the upper neighbour exists (descending half)
+            const double *ym = SMB && P.nbuf && !P.up ? y1 : xpl - plr;
+            const double *yp = SMB && P.nbuf && P.up ? y1 : xpl + plr;
             if (P.hasM) {
                 double y[K], yt;
-                ld_rec(xpl - plr + q * LR, L, y, yt);
+                ld_rec(ym + q * LR, L, y, yt);
                 sub_mul(rhs, rhst, srec(o_l3(K), q), L, y, yt);
             }
             if (P.hasP) {
                 double y[K], yt;
-                ld_rec(xpl + plr + q * LR, L, y, yt);
+                ld_rec(yp + q * LR, L, y, yt);
                 sub_mul(rhs, rhst, srec(o_u3(K), q), L, y, yt);
             }
         } else {
@@ -746,7 +772,22 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
         if (t2 < ny - 1) sub_mul(rhs, rhst, srec(o_u2(K), q), L, xd, xdt);
         const LinePrep PP = line_prep<K>(lane & 15, aL, aU);
         line_solve4<K>(PP, nx, t, aL, rhs, aU, rhst, nlt, nut, xn, xnt);
-        if (w2 == 0) {
+        if constexpr (SMB) {
+            // both warps keep the twist line's final value in their buffers
+            double nv[K], nvt = xnt;
+#pragma unroll
+            for (int k = 0; k < K; k++) nv[k] = xn[k];
+            if (!lower3) {
+                double xo[K], xot;
+                ld_rec(xpl + q * LR, L, xo, xot);
+#pragma unroll
+                for (int k = 0; k < K; k++) nv[k] = xo[k] - xn[k];
+                nvt = xot - xnt;
+            }
+            if (w2 == 0) st_rec(xpl + q * LR, L, nv, nvt);
+            __syncwarp();  // every lane has read the old twist slot (twist element is shared)
+            st_rec(xlow + q * LR, L, nv, nvt);
+        } else if (w2 == 0) {
             if (lower3) {
                 st_rec(xpl + q * LR, L, xn, xnt);
             } else {
@@ -799,6 +840,7 @@ __device__ void solve_plane(const SlArrays &S, const PlaneDesc &P, const Seq &Q,
         }
         mbar_arrive(&R.empty[st]);
         st_rec(xpl + Q.qup(i) * LR, L, nv, nvt);
+        if constexpr (SMB) st_rec(xlow + Q.qup(i) * LR, L, nv, nvt);  // (xlow is the buffer)
         if (PIPE) {
             fin_prep(nxo, lane);
             if (WAIT_AHEAD && i + 2 < cnt && !ok2) mbar_wait(full(rec + 2), par(rec + 2));
@@ -819,7 +861,9 @@ __device__ __forceinline__ void cluster_sync_all()
 // NP = 1: a cluster of two CTAs per system, one level-3 half each on its own
 // SM (solver and producer warps then each have an SM sub-partition to
 // themselves); the level-3 phase boundaries are cluster barriers.
-template <int K, int D, int NP>
+// SMB (split kernel only): each solver warp keeps its half of the last
+// processed plane in shared memory after the ring (solve_plane).
+template <int K, int D, int NP, bool SMB = false>
 __global__ void __launch_bounds__(128 * NP, 1) k_apply(const double *__restrict__ solve, const double *__restrict__ bsl,
                                                        double *xsl, double *xssl, const double *__restrict__ zpl,
                                                        int nx, int ny, int nz, const int32_t *__restrict__ active)
@@ -843,6 +887,9 @@ __global__ void __launch_bounds__(128 * NP, 1) k_apply(const double *__restrict_
     const int pair = NP == 2 ? sw >> 1 : (int)(blockIdx.x & 1), w2 = sw & 1, bar = NP == 2 ? 1 + pair : 1;
     Ring<K, D> R;
     R.base = sl_ring + (size_t)sw * D * stage_of(K);
+    // SMB plane buffer of this solver warp: max(t2+1, ny-t2) lines
+    const int bl = (ny - 1) / 2 + 1 > ny - (ny - 1) / 2 ? (ny - 1) / 2 + 1 : ny - (ny - 1) / 2;
+    double *pbuf = sl_ring + (size_t)2 * NP * D * stage_of(K) + (size_t)sw * bl * LR;
     R.full = bars[sw];
     R.empty = bars[sw] + D;
     if (!producer && lane == 0) {
@@ -875,6 +922,10 @@ __global__ void __launch_bounds__(128 * NP, 1) k_apply(const double *__restrict_
     const int ntw = pair == 0 ? 1 : 0;
     auto desc = [&](int idx) {
         PlaneDesc P;
+        // the neighbour is the plane this pair processed last, except for
+        // each sweep's first plane (none / another pair's) and the twist
+        // plane's upper neighbour (y2, pair 1's)
+        P.nbuf = idx > 0 && !(pair == 1 && idx == nlow);
         P.two = false;
         P.hasM = P.hasP = P.nbrUp = P.up = false;
         if (idx < nlow) {
@@ -911,7 +962,7 @@ __global__ void __launch_bounds__(128 * NP, 1) k_apply(const double *__restrict_
         if (producer)
             produce(i);
         else
-            solve_plane<K, D, M_LOWER3, false>(S, desc(i), Q, nx, bar, myex, parity, R, L, rec);
+            solve_plane<K, D, M_LOWER3, false, SMB>(S, desc(i), Q, nx, bar, myex, parity, R, L, rec, pbuf);
     }
     phase_sync();
     if (pair == 0) {
@@ -919,7 +970,7 @@ __global__ void __launch_bounds__(128 * NP, 1) k_apply(const double *__restrict_
             fence_proxy_async();
             produce(nlow);
         } else {
-            solve_plane<K, D, M_LOWER3, true>(S, desc(nlow), Q, nx, bar, myex, parity, R, L, rec);
+            solve_plane<K, D, M_LOWER3, true, SMB>(S, desc(nlow), Q, nx, bar, myex, parity, R, L, rec, pbuf);
         }
     }
     phase_sync();
@@ -928,7 +979,7 @@ __global__ void __launch_bounds__(128 * NP, 1) k_apply(const double *__restrict_
         if (producer)
             produce(i);
         else
-            solve_plane<K, D, M_UPPER3, false>(S, desc(i), Q, nx, bar, myex, parity, R, L, rec);
+            solve_plane<K, D, M_UPPER3, false, SMB>(S, desc(i), Q, nx, bar, myex, parity, R, L, rec, pbuf);
     }
 }
 
@@ -939,6 +990,43 @@ int launch_prep_sl_k(double *solve, i64 lines_total, cudaStream_t st);
 template <int K>
 int launch_apply_sl_k(const double *solve, const double *bsl, double *xsl, double *xssl, const double *zpl, int nx,
                       int ny, int nz, i64 batch, const int32_t *active, cudaStream_t st, int ctas_per_system = 1);
+
+namespace sl {
+// host switch for A/B measurements (ntd_set_smb); on by default
+inline bool g_ntd_smb = true;
+}
+
+template <int K>
+int launch_apply_smb(const double *solve, const double *bsl, double *xsl, double *xssl, const double *zpl, int nx,
+                     int ny, int nz, i64 batch, const int32_t *active, cudaStream_t st, int bl)
+{
+    constexpr int Ds = sl::depth_smb_of(K) >= 2 ? sl::depth_smb_of(K) : 2;
+    const size_t smem = (size_t)2 * Ds * sl::stage_of(K) * 8 + (size_t)2 * bl * sl::lr_of(K) * 8;
+    cudaError_t e = cudaFuncSetAttribute(sl::k_apply<K, Ds, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) {
+        ntd::set_error("ntd_apply smem", e);
+        return NTD_ELAUNCH;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * batch));
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, sl::k_apply<K, Ds, 1, true>, solve, bsl, xsl, xssl, zpl, nx, ny, nz, active);
+    if (e != cudaSuccess) {
+        ntd::set_error("ntd_apply (cluster)", e);
+        return NTD_ELAUNCH;
+    }
+    return ntd::check_launch("ntd_apply");
+}
 
 #define NTD_INSTANTIATE_SL(K)                                                                                     \
     template <>                                                                                                    \
@@ -953,6 +1041,11 @@ int launch_apply_sl_k(const double *solve, const double *bsl, double *xsl, doubl
                              int nx, int ny, int nz, i64 batch, const int32_t *active, cudaStream_t st,            \
                              int ctas_per_system)                                                                  \
     {                                                                                                              \
+        const int bl_ = (ny - 1) / 2 + 1 > ny - (ny - 1) / 2 ? (ny - 1) / 2 + 1 : ny - (ny - 1) / 2;             \
+        if constexpr (sl::depth_smb_of(K) >= 2) {                                                                  \
+            if (ctas_per_system == 2 && bl_ <= 16 * K + 1 && sl::g_ntd_smb)                                        \
+                return launch_apply_smb<K>(solve, bsl, xsl, xssl, zpl, nx, ny, nz, batch, active, st, bl_);        \
+        }                                                                                                          \
         if (ctas_per_system == 2) {                                                                                \
             constexpr int D2 = sl::depth2_of(K);                                                                   \
             const size_t smem2 = (size_t)2 * D2 * sl::stage_of(K) * 8;                                             \

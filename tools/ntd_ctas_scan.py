@@ -18,9 +18,11 @@ for B in sizes:
     s = BatchSolver(a, nx, ny, nz, groups=1).setup()
     P = s.precond
     row = []
-    for c in (1, 2):
+    for c in (1, 2, "2-nosmb"):
+        _lib.load().ntd_set_smb(0 if c == "2-nosmb" else 1)
+        c_ = 2 if c == "2-nosmb" else c
         def run():
-            _lib.call("ntd_apply_slot_ex", _lib.ptr(P.solve), _lib.ptr(P.work), nx, ny, nz, B, None, c,
+            _lib.call("ntd_apply_slot_ex", _lib.ptr(P.solve), _lib.ptr(P.work), nx, ny, nz, B, None, c_,
                       _lib.stream())
         run()
         e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -30,6 +32,7 @@ for B in sizes:
         e[1].record()
         torch.cuda.synchronize()
         row.append(f"{c}:{e[0].elapsed_time(e[1]) / 3:.3f}")
+    _lib.load().ntd_set_smb(1)
     print(f"B={B} ntd apply ms by ctas/system:", " ".join(row), flush=True)
     del s, P, a
     torch.cuda.empty_cache()
