@@ -421,6 +421,11 @@ def stencil_roofline(solver, B, n, nx, ny, nz):
         "spmv_dot": (48, lambda: _lib.call("ntd_pcg_spmv_alpha_sym", _lib.ptr(a4), _lib.ptr(cg.p), _lib.ptr(cg.ap),
                                            _lib.ptr(cg.state), _lib.ptr(cg.flags), _lib.ptr(cg.active), nx, ny, nz,
                                            B, _lib.ptr(cg.work), _lib.stream())),
+        # x, r axpys (x, r, p, ap read, x, r written: 48) + true residual (A 32 + b, x: 48)
+        "update_true_residual": (96, lambda: _lib.call(
+            "ntd_pcg_update_residual_sym", _lib.ptr(a4), _lib.ptr(r), _lib.ptr(cg.x), _lib.ptr(cg.r), _lib.ptr(cg.p),
+            _lib.ptr(cg.ap), _lib.ptr(cg.state), _lib.ptr(cg.flags), _lib.ptr(cg.active), _lib.ptr(cg.history), 2,
+            nx, ny, nz, B, _lib.ptr(cg.work), _lib.stream())),
     }
     out = {}
     for name, (bpu, fn) in cases.items():
