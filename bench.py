@@ -426,6 +426,10 @@ def stencil_roofline(solver, B, n, nx, ny, nz):
             "ntd_pcg_update_residual_sym", _lib.ptr(a4), _lib.ptr(r), _lib.ptr(cg.x), _lib.ptr(cg.r), _lib.ptr(cg.p),
             _lib.ptr(cg.ap), _lib.ptr(cg.state), _lib.ptr(cg.flags), _lib.ptr(cg.active), _lib.ptr(cg.history), 2,
             nx, ny, nz, B, _lib.ptr(cg.work), _lib.stream())),
+        # r.z (16) + p = beta p + z (p, z read, p written: 24)
+        "direction": (40, lambda: _lib.call("ntd_pcg_direction", _lib.ptr(cg.r), _lib.ptr(w), _lib.ptr(cg.p),
+                                            _lib.ptr(cg.state), _lib.ptr(cg.active), n, B, _lib.ptr(cg.work),
+                                            _lib.stream())),
     }
     out = {}
     for name, (bpu, fn) in cases.items():
