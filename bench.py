@@ -27,6 +27,8 @@ import time
 
 import numpy as np
 
+# stream groups need hardware queues (before any CUDA context; see batch.py)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
