@@ -193,9 +193,17 @@ def run_ntd(args):
     import torch
     import torch.distributed as dist
     world, rank, local = dist_env()
-    torch.cuda.set_device(local)
+    # NTD_BENCH_ONE_GPU=1 (validation only): every rank on cuda:0 with gloo
+    # statistics exchange, to exercise the multi-rank path on a 1-GPU box (the
+    # ranks share nothing on the data path, so none waits on another)
+    one_gpu = os.environ.get("NTD_BENCH_ONE_GPU") == "1"
+    gpu = 0 if one_gpu else local
+    torch.cuda.set_device(gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1909_09771_b200 import _lib
     from paper_1909_09771_b200 import device as D
     from paper_1909_09771_b200.batch import BatchSolver
@@ -241,7 +249,7 @@ def run_ntd(args):
     _lib.reset_launch_count()
     for grp in solver.groups:
         grp.precond.ntd_events = []
-    with ClockSampler(local) as clk:
+    with ClockSampler(gpu) as clk:
         barrier()
         ev[0].record()
         work_local = 0
@@ -326,7 +334,7 @@ def run_ntd(args):
 
     # ---- reductions over ranks (NCCL: max of timings, sum of work, one all_gather of stats)
     from paper_1909_09771_b200 import dist as pdist
-    dev = torch.device("cuda", local)
+    dev = torch.device("cpu") if one_gpu else torch.device("cuda", local)
     times = pdist.reduce_max([t_dev, t_e2e, t_apply, t_ilu, t_spmv, setup_s, -apply_gbs], dev)
     work = pdist.reduce_sum([work_local, work_e2e, launches], dev)
     stats = pdist.gather_stats([[s, it, int(cv), rr] for s, it, cv, rr in
