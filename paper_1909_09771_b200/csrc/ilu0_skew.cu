@@ -241,6 +241,13 @@ __device__ __forceinline__ void cp_async8(double *dst, const double *src)
                  "l"(src)
                  : "memory");
 }
+// the same with zero fill: nothing is read when !ok (the slot holds no cell)
+__device__ __forceinline__ void cp_async8_zf(double *dst, const double *src, bool ok)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(ok ? 8 : 0)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -291,15 +298,17 @@ __device__ void sweep(const Geom &g, int u_lo, int u_hi, const double *__restric
     auto stage = [&]() {
         if (sr < nmine) {
             double *dst = ring + sslot * (ROWS * 32) + lane;
+            const bool ok = sjv && (unsigned)(stau - lane) < (unsigned)nx;
+            // empty slots: zero-filled, not read (their coefficients are 0;
+            // the backward solve masks its division there)
 #pragma unroll
             for (int c = 0; c < NC; c++) {
                 const double *pc = scs + c * 32;
 #ifdef SKEW_CHECK
                 if (SKC(pc, coef, g.skew_size() * NC, 1)) pc = coef;
 #endif
-                cp_async8(dst + c * 32, pc);
+                cp_async8_zf(dst + c * 32, pc, ok);
             }
-            const bool ok = sjv && (unsigned)(stau - lane) < (unsigned)nx;
             if (FWD) {
                 if (ok) {
                     const double *pi = sin;
@@ -315,13 +324,13 @@ __device__ void sweep(const Geom &g, int u_lo, int u_hi, const double *__restric
 #ifdef SKEW_CHECK
                 if (SKC(pi, in, g.skew_size(), 3)) pi = in;
 #endif
-                cp_async8(dst + 4 * 32, pi);
-                if (has_ao && ok) {
-                    const double *pa = sacc;
+                cp_async8_zf(dst + 4 * 32, pi, ok);
+                if (has_ao) {
+                    const double *pa = ok ? sacc : acc_out;  // (empty slots: any valid address)
 #ifdef SKEW_CHECK
                     if (SKC(pa, acc_out, g.n, 4)) pa = acc_out;
 #endif
-                    cp_async8(dst + 5 * 32, pa);
+                    cp_async8_zf(dst + 5 * 32, pa, ok);
                 }
             }
             scs += dt * 32 * NC;
@@ -409,12 +418,13 @@ __device__ void sweep(const Geom &g, int u_lo, int u_hi, const double *__restric
                 acc = sub_rn(acc, mul_rn(sg[0], zprev));
                 acc = sub_rn(acc, mul_rn(sg[32], zy));
                 acc = sub_rn(acc, mul_rn(sg[64], rzz[d]));
-                const double zv = FWD ? acc : acc / sg[96];
+                const bool valid = jv && (unsigned)(tau - lane) < (unsigned)nx;
+                const double zv = FWD ? acc : (valid ? acc / sg[96] : 0.0);
 #ifdef SKEW_CHECK
                 if (!SKC(zp, z, g.skew_size(), 5))
 #endif
                     *zp = zv;
-                if (!FWD && jv && (unsigned)(tau - lane) < (unsigned)nx) {
+                if (!FWD && valid) {
                     if (has_zo) {
 #ifdef SKEW_CHECK
                         if (!SKC(zop, zout, g.n, 6))
