@@ -24,14 +24,14 @@ lib = _lib.load()
 fn = lib.ntd_skew_timing
 fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
 buf = (ctypes.c_ulonglong * 4)()
-ctas = int(os.environ.get("SKEW_CTAS", "0")) or P.ilu_ctas
+env = os.environ.get("SKEW_CTAS")  # "c,w"
+ctas = tuple(int(t) for t in env.split(",")) if env else P.ilu_ctas
 D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, B, z=x, skew=P.skew, ctas=ctas)
 torch.cuda.synchronize()
 fn(buf, 1)
 R = 5
 for _ in range(R):
-    ctas = int(os.environ.get("SKEW_CTAS", "0")) or P.ilu_ctas
-D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, B, z=x, skew=P.skew, ctas=ctas)
+    D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, B, z=x, skew=P.skew, ctas=ctas)
 torch.cuda.synchronize()
 fn(buf, 1)
 wait, total, steps, units = (buf[i] / R for i in range(4))
