@@ -116,7 +116,7 @@ ILU0_WARPS = 24  # warps per CTA of the one-CTA-per-half sweep (skew::WARPS)
 
 def ilu0_ctas(systems_on_gpu):
     """(CTAs per system half, warps per CTA) for the skewed ILU0 sweep: a
-    cluster of up to 4 CTAs on separate SMs when the GPU's whole load (all
+    cluster of up to 8 CTAs on separate SMs when the GPU's whole load (all
     systems, every stream group) leaves SMs idle, else one 24-warp CTA per
     half.  NTD_ILU0_CTAS="c,w" overrides (experiments)."""
     env = os.environ.get("NTD_ILU0_CTAS")
@@ -124,8 +124,12 @@ def ilu0_ctas(systems_on_gpu):
         c, w = (int(v) for v in env.split(","))
         return c, w
     # measured (tools/ilu0_ctas_scan.py, 96^3, ms per apply at 1 / 8 / 16
-    # systems): 1x24 1.25/1.27/1.28, 2x24 1.10/1.12/1.15, 4x12 0.95/0.99/1.03
-    c = max(1, min(4, SMS // max(1, 2 * systems_on_gpu)))
+    # systems): 1x24 1.25/1.27/1.28, 2x24 1.10/1.12/1.15, 4x12 0.95/0.99/1.03;
+    # 8x6 0.84 at 1 system.  Whole solves (bench.py): 8x6 instead of 4x12 is
+    # 1-2.5% faster for configs 1-3 and 8 systems, 10% slower at 16 systems
+    c = max(1, min(8, SMS // max(1, 2 * systems_on_gpu)))
+    if c >= 8:
+        return 8, 6
     if c >= 4:
         return 4, 12
     return (2, ILU0_WARPS) if c >= 2 else (1, ILU0_WARPS)
