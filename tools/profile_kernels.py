@@ -1,6 +1,6 @@
 """Launch the hot kernels on a config-4 sub-batch for ncu (debug/profiling aid).
 
-    python tools/profile_kernels.py [systems]
+    PROFILE_BATCH=64 python tools/profile_kernels.py [systems]
 """
 import os
 import sys
@@ -24,11 +24,15 @@ s = BatchSolver(a, nx, ny, nz, groups=1).setup()
 v = torch.rand_like(b)
 x = torch.empty_like(b)
 P = s.precond
+# the CTA mappings the solver uses for the whole batch it belongs to
+# (PROFILE_BATCH systems on the GPU; bench.py: 64 in 16 stream groups)
+full = int(os.environ.get("PROFILE_BATCH", "64"))
+ilu_ctas, ntd_ctas = D.ilu0_ctas(full), D.ntd_ctas(full)
 for _ in range(2):
     # the NTD sweep as the solver launches it (slot layout, ctas per system)
-    _lib.call("ntd_apply_slot_ex", _lib.ptr(P.solve), _lib.ptr(P.work), nx, ny, nz, B, None, P.ntd_ctas,
+    _lib.call("ntd_apply_slot_ex", _lib.ptr(P.solve), _lib.ptr(P.work), nx, ny, nz, B, None, ntd_ctas,
               _lib.stream())
-    D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, B, z=x, skew=P.skew, ctas=P.ilu_ctas)
+    D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, B, z=x, skew=P.skew, ctas=ilu_ctas)
     D.residual(a, v, x, nx, ny, nz, B, a4=s.precond.a4)
 torch.cuda.synchronize()
 print("ok")
