@@ -375,6 +375,7 @@ def run_ntd(args):
                          "launches_timed": len(evs)},
             "kernels_ms": {"ntd_apply": 1e3 * t_apply, "ilu0_apply": 1e3 * t_ilu, "spmv": 1e3 * t_spmv},
             "stencil_roofline": stencil,
+            "step_hbm": _step_hbm(cfg, Bg, n, work[0] / t_dev, stencil, peak[0]),
             "setup_seconds": setup_s,
             "iterations": {"min": min(iters), "max": max(iters), "mean": float(np.mean(iters)),
                            "within_1_of_reference": ref_match, "systems": len(iters)},
@@ -457,6 +458,24 @@ def _traffic(cfg, systems):
         return None if rec is None else float(rec["bytes_per_launch"])
     except (OSError, ValueError, KeyError):
         return None
+
+
+def _step_hbm(cfg, systems, n, unknown_iters_per_s, stencil, peak):
+    """The whole PCG iteration against HBM: DRAM bytes per unknown-iteration
+    (NTD and 2 ILU0 sweeps measured by ncu, profiles/roofline_traffic.json;
+    stencil/CG kernels at their algorithmic bytes) x the measured rate."""
+    try:
+        with open(os.path.join(REPO, "profiles", "roofline_traffic.json")) as fh:
+            rec = json.load(fh)
+        ntd = rec[f"cfg{cfg}-{systems}"]["bytes_per_launch"] / (systems * n)
+        ilu = rec[f"ilu0-cfg{cfg}-{systems}"]["bytes_per_launch"] / (systems * n)
+    except (OSError, ValueError, KeyError):
+        return None
+    sten = sum(v["bytes_per_unknown"] for v in stencil.values()) if stencil else 0
+    bpu = ntd + 2 * ilu + sten
+    gbs = bpu * unknown_iters_per_s / 1e9
+    return {"bytes_per_unknown_iter": round(bpu, 1), "ntd": round(ntd, 1), "ilu0_x2": round(2 * ilu, 1),
+            "stencil_cg": sten, "achieved_gbs": gbs, "frac": gbs / peak}
 
 
 def _measured_peak():
