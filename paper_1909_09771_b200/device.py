@@ -7,6 +7,7 @@ factors (B, 7, N), vectors (B, N) -- and calls libntdgpu.so through the C ABI
 solver both sit on top of these functions.
 """
 
+import contextlib
 import os
 
 import torch
@@ -220,6 +221,21 @@ class CombinedDevice:
         # fused residual <-> NTD apply stages on the slot layout when available
         self.fused = self.solve is not None and n < 2 ** 31
         self.ntd_events = None  # list: (start, end) CUDA events around every NTD apply (bench timing)
+        # optional stream (e.g. of another priority) for the ILU0 / NTD sweeps;
+        # the stencil kernels stay on the caller's stream
+        self.sweep_stream = None
+
+    @contextlib.contextmanager
+    def _sweep(self):
+        s = self.sweep_stream
+        if s is None:
+            yield
+            return
+        cur = torch.cuda.current_stream()
+        s.wait_stream(cur)
+        with torch.cuda.stream(s):
+            yield
+        cur.wait_stream(s)
 
     def apply(self, r, z, active=None):
         """z = M^{-1} r:  w = ilu(r); t = r - A w; z = ntd(t) + w;
@@ -228,35 +244,38 @@ class CombinedDevice:
         if self.skew is not None and self.skew_work is None:
             self.skew_work = torch.empty(_lib.load().ntd_ilu0_skew_work_doubles(*g), dtype=torch.float64,
                                          device=_dev())
-        ilu0_apply(self.ilu, self.split, r, *g, z=self.w, active=active, skew=self.skew, work=self.skew_work,
-                   ctas=self.ilu_ctas)
+        with self._sweep():
+            ilu0_apply(self.ilu, self.split, r, *g, z=self.w, active=active, skew=self.skew, work=self.skew_work,
+                       ctas=self.ilu_ctas)
         op, nb = (self.a, 7) if self.a4 is None else (self.a4, 4)
         if self.fused:
             _lib.call("ntd_residual_to_slot", _lib.ptr(op), nb, _lib.ptr(self.pre), _lib.ptr(r), _lib.ptr(self.w),
                       _lib.ptr(self.work), *g, _lib.ptr(active), _lib.stream())
         else:
             residual(self.a, r, self.w, *g, t=self.t, active=active, a4=self.a4)
-        if self.ntd_events is not None:
-            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            ev[0].record()
-        if self.fused:
-            _lib.call("ntd_apply_slot_ex", _lib.ptr(self.solve), _lib.ptr(self.work), *g, _lib.ptr(active),
-                      self.ntd_ctas, _lib.stream())
-        else:
-            ntd_apply(self.pre, self.t, *g, x=self.xn, work=self.work, active=active, solve=self.solve)
-        if self.ntd_events is not None:
-            ev[1].record()
-            self.ntd_events.append(ev)
+        with self._sweep():
+            if self.ntd_events is not None:
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                ev[0].record()
+            if self.fused:
+                _lib.call("ntd_apply_slot_ex", _lib.ptr(self.solve), _lib.ptr(self.work), *g, _lib.ptr(active),
+                          self.ntd_ctas, _lib.stream())
+            else:
+                ntd_apply(self.pre, self.t, *g, x=self.xn, work=self.work, active=active, solve=self.solve)
+            if self.ntd_events is not None:
+                ev[1].record()
+                self.ntd_events.append(ev)
         if self.fused:
             _lib.call("ntd_residual_from_slot", _lib.ptr(op), nb, _lib.ptr(self.work), _lib.ptr(r),
                       _lib.ptr(self.w), _lib.ptr(z), _lib.ptr(self.t), *g, _lib.ptr(active), _lib.stream())
         else:
             residual(self.a, r, self.w, *g, t=self.t, v=self.xn, z_out=z, active=active, a4=self.a4)
-        if self.skew is not None:
-            ilu0_apply(self.ilu, self.split, self.t, *g, z=None, acc=z, active=active, skew=self.skew,
-                       work=self.skew_work, ctas=self.ilu_ctas)
-        else:
-            ilu0_apply(self.ilu, self.split, self.t, *g, z=self.xn, acc=z, active=active)
+        with self._sweep():
+            if self.skew is not None:
+                ilu0_apply(self.ilu, self.split, self.t, *g, z=None, acc=z, active=active, skew=self.skew,
+                           work=self.skew_work, ctas=self.ilu_ctas)
+            else:
+                ilu0_apply(self.ilu, self.split, self.t, *g, z=self.xn, acc=z, active=active)
         return z
 
 
