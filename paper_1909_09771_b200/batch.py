@@ -179,7 +179,11 @@ class BatchSolver:
         # high-priority stream of their own, so an SM freed by a short stencil
         # kernel goes to a waiting sweep CTA first: +1.8% on the 64-system
         # batch (8 alternating runs).  NTD_SWEEP_PRIO=off / lo for experiments.
+        # Two streams per group: only while they all get a hardware queue of
+        # their own (32 groups -> 64 streams on 32 queues: 20% slower).
         prio = os.environ.get("NTD_SWEEP_PRIO", "hi")
+        if 2 * len(self.groups) > int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8")):
+            prio = "off"
         for grp in self.groups:
             lo, hi = grp.lo, grp.hi
             grp.pcg.a4 = None if a4 is None else a4[lo:hi]
