@@ -460,6 +460,9 @@ def _traffic(cfg, systems):
         return None
 
 
+PCG_ITER_BYTES_PER_UNKNOWN = 488
+
+
 def _step_hbm(cfg, systems, n, unknown_iters_per_s, stencil, peak):
     """The whole PCG iteration against HBM: DRAM bytes per unknown-iteration
     (NTD and 2 ILU0 sweeps measured by ncu, profiles/roofline_traffic.json;
@@ -474,8 +477,13 @@ def _step_hbm(cfg, systems, n, unknown_iters_per_s, stencil, peak):
     sten = sum(v["bytes_per_unknown"] for v in stencil.values()) if stencil else 0
     bpu = ntd + 2 * ilu + sten
     gbs = bpu * unknown_iters_per_s / 1e9
+    # canonical algorithmic bytes of one ntd+ilu0 PCG
+    # iteration (each distinct input read once, A as 4 symmetric bands)
+    canon = PCG_ITER_BYTES_PER_UNKNOWN * unknown_iters_per_s / 1e9
     return {"bytes_per_unknown_iter": round(bpu, 1), "ntd": round(ntd, 1), "ilu0_x2": round(2 * ilu, 1),
-            "stencil_cg": sten, "achieved_gbs": gbs, "frac": gbs / peak}
+            "stencil_cg": sten, "achieved_gbs": gbs, "frac": gbs / peak,
+            "canonical_bytes_per_unknown_iter": PCG_ITER_BYTES_PER_UNKNOWN, "canonical_gbs": canon,
+            "canonical_frac": canon / peak, "canonical_frac_of_8tbs": canon / 8000.0}
 
 
 def _measured_peak():
