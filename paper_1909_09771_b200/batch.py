@@ -204,7 +204,32 @@ class BatchSolver:
         """Solve all systems.  x_out: optional device (B, N) tensor that
         receives the solutions (default: the solver's own buffer), so a caller
         can copy one solve's x to the host while the next solve runs."""
-        b = as_device(b_dev).reshape(self.batch, self.n)
+        return self._solve(as_device(b_dev).reshape(self.batch, self.n), tol, x_out)
+
+    def solve_host(self, b_host, x_host, tol=1e-8):
+        """Solve from and to host memory: b_host, x_host (B, N) fp64 CPU
+        tensors (pinned for asynchronous copies).  Each stream group uploads
+        its slice of b on its own stream just before its PCG starts and
+        downloads its slice of x as soon as the host sees that all its systems
+        have stopped, so the transfers overlap the other groups' sweeps.
+        x_host holds the solutions when this returns."""
+        if tuple(b_host.shape) != (self.batch, self.n) or tuple(x_host.shape) != (self.batch, self.n):
+            raise ValueError(f"b_host and x_host must have shape ({self.batch}, {self.n})")
+        if b_host.is_cuda or x_host.is_cuda:
+            raise ValueError("solve_host takes host tensors; use solve() for device tensors")
+        if getattr(self, "_b_dev", None) is None:
+            self._b_dev = torch.empty((self.batch, self.n), dtype=torch.float64, device=self.a.device)
+        b = self._b_dev
+
+        def upload(grp):
+            b[grp.lo:grp.hi].copy_(b_host[grp.lo:grp.hi], non_blocking=True)
+
+        def download(grp):
+            x_host[grp.lo:grp.hi].copy_(self.x[grp.lo:grp.hi], non_blocking=True)
+
+        return self._solve(b, tol, None, on_start=upload, on_done=download)
+
+    def _solve(self, b, tol, x_out, on_start=None, on_done=None):
         x = self.x if x_out is None else x_out.reshape(self.batch, self.n)
         for grp in self.groups:
             grp.pcg.x = x[grp.lo:grp.hi]
@@ -212,7 +237,7 @@ class BatchSolver:
         t0 = perf_counter()
         for grp in self.groups:
             grp.stream.wait_stream(cur)  # b may have been produced on the caller's stream
-        self._run(b, tol)
+        self._run(b, tol, on_start, on_done)
         for grp in self.groups:
             cur.wait_stream(grp.stream)
         fl = torch.cat([grp.pcg.flags for grp in self.groups]).cpu()
@@ -233,35 +258,58 @@ class BatchSolver:
                 grp.flags_host[slot].copy_(grp.pcg.flags, non_blocking=True)
                 grp.events[slot].record(grp.stream)
 
-    def _any_active(self, slot):
+    def _any_active(self, slot, on_done=None, done=None):
+        """Whether any system is still iterating (flags of the copy in
+        `slot`).  on_done(grp) is enqueued on a group's stream the first time
+        all its systems have stopped (their later kernels are masked no-ops)."""
         act = _lib.NTD_FL["ACTIVE"]
         alive = False
         for grp in self.groups:
             grp.events[slot].synchronize()
-            alive = alive or bool(grp.flags_host[slot][:, act].any())
+            g_alive = bool(grp.flags_host[slot][:, act].any())
+            alive = alive or g_alive
+            if not g_alive and on_done is not None and grp not in done:
+                done.add(grp)
+                with torch.cuda.stream(grp.stream):
+                    on_done(grp)
         return alive
 
-    def _run(self, b, tol):
+    def _run(self, b, tol, on_start=None, on_done=None):
         """PCG (precond_pcg.py:84-119) on every group, enqueued round-robin.
         Iteration it's update is enqueued before the host looks at the flags
         of iteration it-1, so the GPU always has queued work."""
         groups = self.groups
+        done = set()
+        try:
+            self._run_groups(b, tol, on_start, on_done, done)
+        finally:
+            if on_done is not None:
+                for grp in groups:
+                    if grp not in done:
+                        done.add(grp)
+                        with torch.cuda.stream(grp.stream):
+                            on_done(grp)
+
+    def _run_groups(self, b, tol, on_start, on_done, done):
+        groups = self.groups
         for grp in groups:
             with torch.cuda.stream(grp.stream):
+                if on_start is not None:
+                    on_start(grp)
                 grp.pcg.init(b[grp.lo:grp.hi], tol)
         self._flags_async(0)
         for grp in groups:
             with torch.cuda.stream(grp.stream):
                 z = grp.pcg.r if grp.precond is None else grp.precond.apply(grp.pcg.r, grp.pcg.z, grp.pcg.active)
                 grp.pcg.start(z)
-        if not self._any_active(0):
+        if not self._any_active(0, on_done, done):
             return
         for it in range(1, self.max_iters + 1):
             for grp in groups:
                 with torch.cuda.stream(grp.stream):
                     grp.pcg.step_update()
             self._flags_async(it % 2)
-            if it >= 2 and not self._any_active((it - 1) % 2):
+            if it >= 2 and not self._any_active((it - 1) % 2, on_done, done):
                 break  # everything had converged at it-1; iteration it was fully masked
             if it == self.max_iters:
                 break

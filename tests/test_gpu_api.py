@@ -285,3 +285,29 @@ def test_batch_solver_output_buffer_and_groups(ntd):
         xs.append((res.iterations, out.clone()))
     assert xs[0][0] == xs[1][0] and torch.equal(xs[0][1], xs[1][1])
     assert float((xs[0][1] - xt).abs().max()) < 1e-3  # relres 1e-8 on kappa contrasts of ~1e6
+
+
+def test_batch_solver_host_buffers(ntd):
+    """BatchSolver.solve_host: per-group uploads/downloads on the group
+    streams give bitwise the device-buffer solve's solutions, also when the
+    groups stop at different iterations; bad shapes raise ValueError."""
+    import pytest
+    import torch
+    from paper_1909_09771_b200 import problems
+    from paper_1909_09771_b200.batch import BatchSolver
+    ins = [problems.baseline_config(4, s) for s in (0, 2, 14, 23)]  # 21, 24, 19, 25 iterations
+    nx, ny, nz = ins[0][2]
+    A = torch.from_numpy(np.stack([d for d, _, _ in ins])).cuda()
+    b = np.stack([ntd.spmv(ntd.BandedMatrix(nx, ny, nz, d), x) for d, x, _ in ins])
+    solver = BatchSolver(A, nx, ny, nz, groups=4).setup()
+    want = solver.solve(torch.from_numpy(b).cuda(), 1e-8)
+    x_dev, its = want.x.clone(), list(want.iterations)
+    b_host = torch.from_numpy(b).pin_memory()
+    x_host = torch.full_like(b_host, float("nan")).pin_memory()
+    for _ in range(2):
+        got = solver.solve_host(b_host, x_host, 1e-8)
+        assert list(got.iterations) == its and len(set(its)) > 1
+        assert torch.equal(x_host, x_dev.cpu())
+        x_host.fill_(float("nan"))
+    with pytest.raises(ValueError):
+        solver.solve_host(b_host[:2], x_host[:2])
