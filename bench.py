@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--systems", type=int, default=None, help="batch size (config 4: 64)")
     ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--precond", default="ntd+ilu0", choices=["ntd+ilu0", "ntd"],
+                    help="preconditioner (SURVEY.md 8(d) also reports ntd-only for configs 1 and 3)")
     ap.add_argument("--cpu-systems", type=int, default=None, help="CPU baseline sample size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -124,7 +126,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU leg
-def cpu_solve_systems(cfg, systems, threads, tol):
+def cpu_solve_systems(cfg, systems, threads, tol, kind="ntd+ilu0"):
     """Oracle (C restatement of the reference) PCG on `systems`, `threads`
     systems at a time.  Returns (unknown-iterations, solve seconds wall,
     setup seconds wall, iterations list)."""
@@ -138,7 +140,7 @@ def cpu_solve_systems(cfg, systems, threads, tol):
         data, x_true, (nx, ny, nz) = inp
         b = oracle.spmv(data, x_true, nx, ny, nz)
         pre = oracle.factor_level3(data, nx, ny, nz)
-        ilu = oracle.build_block_ilu0(data, nx, ny, nz)
+        ilu = oracle.build_block_ilu0(data, nx, ny, nz) if kind == "ntd+ilu0" else None
         return data, b, (nx, ny, nz), pre, ilu
 
     t0 = time.perf_counter()
@@ -148,7 +150,7 @@ def cpu_solve_systems(cfg, systems, threads, tol):
 
     def solve(item):
         data, b, (nx, ny, nz), pre, ilu = item
-        _, it, conv, _ = oracle.pcg(data, b, nx, ny, nz, tol=tol, pre=pre, ilu=ilu)
+        _, it, conv, _ = oracle.pcg(data, b, nx, ny, nz, kind=kind, tol=tol, pre=pre, ilu=ilu)
         return nx * ny * nz * it, it
 
     t0 = time.perf_counter()
@@ -168,21 +170,21 @@ def run_reference(args):
     n_sys = args.systems or (64 if cfg == 4 else 1)
     systems = list(range(min(sample, n_sys)))
     for _ in range(args.warmup):
-        cpu_solve_systems(cfg, systems[:1], 1, args.tol)
+        cpu_solve_systems(cfg, systems[:1], 1, args.tol, args.precond)
     vals, ts = [], []
     for _ in range(args.steps):
-        work, t, _, iters = cpu_solve_systems(cfg, systems, sample, args.tol)
+        work, t, _, iters = cpu_solve_systems(cfg, systems, sample, args.tol, args.precond)
         vals.append(work / t / 1e6)
         ts.append(t)
     v = float(np.median(vals))
-    desc = (f"{len(systems)} of the {n_sys} config-{cfg} systems per step, each a full ntd+ilu0 PCG solve "
+    desc = (f"{len(systems)} of the {n_sys} config-{cfg} systems per step, each a full {args.precond} PCG solve "
             f"to {args.tol:g} by the C oracle (restatement of the reference kernels), one system per thread")
     out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(ts)), "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "impl": "reference",
            "config": {"workload": f"cfg{cfg}", "systems": n_sys, "grid": "96^3" if cfg == 4 else None,
-                      "precond": "ntd+ilu0", "tol": args.tol, "parallelism": "cpu-threads"},
+                      "precond": args.precond, "tol": args.tol, "parallelism": "cpu-threads"},
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": sample, "kind": "port", "sample": desc},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -230,7 +232,7 @@ def run_ntd(args):
     b_host = b_dev.cpu().pin_memory()
     x_host = torch.empty_like(b_host).pin_memory()
 
-    solver = BatchSolver(a_dev, nx, ny, nz, "ntd+ilu0", max_iters=200)
+    solver = BatchSolver(a_dev, nx, ny, nz, args.precond, max_iters=200 if args.precond == "ntd+ilu0" else 400)
     solver.setup()
     setup_s = solver.setup_seconds
 
@@ -294,11 +296,12 @@ def run_ntd(args):
     v = torch.rand((Bg, n), dtype=torch.float64, device="cuda")
     xa = torch.empty_like(v)
     R = 5
-    for _ in range(2):
+    has_ilu = args.precond == "ntd+ilu0"
+    for _ in range(2 if has_ilu else 0):
         D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, Bg, z=xa, skew=P.skew, work=P.skew_work, ctas=P.ilu_ctas)
     e4 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     e4[0].record()
-    for _ in range(R):
+    for _ in range(R if has_ilu else 0):
         D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, Bg, z=xa, skew=P.skew, work=P.skew_work, ctas=P.ilu_ctas)
     e4[1].record()
     e5 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -327,7 +330,7 @@ def run_ntd(args):
         iters = [int(v) for v in stats[:, 1]]
         sys_ids = [int(v) for v in stats[:, 0]]
         ref_match = None
-        if cfg == 4:
+        if cfg == 4 and args.precond == "ntd+ilu0":
             ref_match = sum(abs(it - CFG4_REF_ITERS[s]) <= 1 for s, it in zip(sys_ids, iters))
         achieved = apply_gbs
         peak = _measured_peak()
@@ -337,7 +340,7 @@ def run_ntd(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE config recipe, SURVEY.md 8(d))",
             "config": {"workload": f"cfg{cfg}", "systems": n_total, "grid": f"{nx}x{ny}x{nz}",
-                       "precond": "ntd+ilu0", "tol": args.tol, "parallelism": f"batch-shard x{world}",
+                       "precond": args.precond, "tol": args.tol, "parallelism": f"batch-shard x{world}",
                        "stream_groups": len(solver.groups), "systems_per_ntd_launch": Bg,
                        "l2": "inputs larger than L2 (each batch vector %.0f MB)" % (8 * n * B / 1e6)},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n * B * world,
@@ -352,9 +355,10 @@ def run_ntd(args):
                          "concurrent_launches": len(solver.groups),
                          "aggregate_gbs": NTD_APPLY_BYTES_PER_UNKNOWN * work[0] / t_dev / 1e9,
                          "launches_timed": len(evs)},
-            "kernels_ms": {"ntd_apply": 1e3 * t_apply, "ilu0_apply": 1e3 * t_ilu, "spmv": 1e3 * t_spmv},
+            "kernels_ms": {"ntd_apply": 1e3 * t_apply, "ilu0_apply": 1e3 * t_ilu if has_ilu else None,
+                           "spmv": 1e3 * t_spmv},
             "stencil_roofline": stencil,
-            "step_hbm": _step_hbm(cfg, Bg, n, work[0] / t_dev, stencil, peak[0]),
+            "step_hbm": _step_hbm(cfg, Bg, n, work[0] / t_dev, stencil, peak[0]) if has_ilu else None,
             "setup_seconds": setup_s,
             "iterations": {"min": min(iters), "max": max(iters), "mean": float(np.mean(iters)),
                            "within_1_of_reference": ref_match, "systems": len(iters)},
@@ -477,9 +481,9 @@ def cpu_baseline(args):
     cores = os.cpu_count() or 1
     sample = args.cpu_systems or min(cores, 8)
     systems = list(range(sample))
-    work, t, _, iters = cpu_solve_systems(args.config, systems, sample, args.tol)
+    work, t, _, iters = cpu_solve_systems(args.config, systems, sample, args.tol, args.precond)
     return {"value": work / t / 1e6, "unit": UNIT, "cores": sample, "kind": "port",
-            "sample": f"{sample} config-{args.config} systems, full ntd+ilu0 PCG solve each (C oracle), "
+            "sample": f"{sample} config-{args.config} systems, full {args.precond} PCG solve each (C oracle), "
                       f"one system per host thread; solve wall {t:.1f} s, iterations {iters}"}
 
 

@@ -170,6 +170,12 @@ int64_t ntd_apply_work_doubles(int64_t nx, int64_t ny, int64_t nz,
 int ntd_apply(const double *pre, const double *solve, const double *b,
               double *x, double *work, int64_t nx, int64_t ny, int64_t nz,
               int64_t batch, const int32_t *active, void *stream);
+/* ntd_apply with 1 or 2 CTAs per system (2: the two level-3 halves of each
+ * system on two SMs, a thread-block cluster).  Bitwise the same result. */
+int ntd_apply_ex(const double *pre, const double *solve, const double *b,
+                 double *x, double *work, int64_t nx, int64_t ny, int64_t nz,
+                 int64_t batch, const int32_t *active, int64_t ctas_per_system,
+                 void *stream);
 
 /* Fused combined-preconditioner stages around the NTD apply (the middle of
  * precond_pcg.py:57-65), working on the apply's slot-layout buffers in

@@ -49,6 +49,7 @@ _SIGS = {
     "ntd_solve_doubles": (_I, [_I, _I, _I, _I]),
     "ntd_solve_bands": (_INT, [_P, _P, _I, _I, _I, _I, _P]),
     "ntd_apply": (_INT, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
+    "ntd_apply_ex": (_INT, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _I, _P]),
     "ntd_residual_to_slot": (_INT, [_P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_apply_slot": (_INT, [_P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_apply_slot_ex": (_INT, [_P, _P, _I, _I, _I, _I, _P, _I, _P]),
@@ -70,7 +71,7 @@ EXPORTED = tuple(_SIGS)
 KERNELS_PER_CALL = {
     "ntd_assemble": 1, "ntd_spmv": 1, "ntd_residual": 1, "ntd_dot": 2, "ntd_pcg_init": 3, "ntd_pcg_start": 3,
     "ntd_pcg_spmv_alpha": 2, "ntd_pcg_update_residual": 3, "ntd_pcg_direction": 3, "ntd_factor": 1,
-    "ntd_apply": 3, "ntd_solve_bands": 1, "ntd_ilu0_factor": 2, "ntd_ilu0_apply": 1, "ntd_ilu0_skew_build": 1,
+    "ntd_apply": 3, "ntd_apply_ex": 3, "ntd_solve_bands": 1, "ntd_ilu0_factor": 2, "ntd_ilu0_apply": 1, "ntd_ilu0_skew_build": 1,
     "ntd_ilu0_skew_apply": 1, "ntd_ilu0_skew_apply_ex": 1, "ntd_sym_pack": 1, "ntd_residual_sym": 1, "ntd_pcg_spmv_alpha_sym": 2,
     "ntd_pcg_update_residual_sym": 3, "ntd_residual_to_slot": 1, "ntd_apply_slot": 1, "ntd_apply_slot_ex": 1,
     "ntd_residual_from_slot": 1,

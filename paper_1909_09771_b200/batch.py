@@ -124,8 +124,8 @@ class BatchSolver:
     extra enqueued iteration does no work for them)."""
 
     def __init__(self, a_dev, nx, ny, nz, kind="ntd+ilu0", max_iters=200, groups=None):
-        if kind not in ("ntd+ilu0", "none"):
-            raise ValueError("BatchSolver supports 'ntd+ilu0' and 'none'")
+        if kind not in ("ntd+ilu0", "ntd", "none"):
+            raise ValueError("BatchSolver supports 'ntd+ilu0', 'ntd' and 'none'")
         self.a = as_device(a_dev)
         self.batch = self.a.shape[0]
         self.nx, self.ny, self.nz = nx, ny, nz
@@ -170,10 +170,11 @@ class BatchSolver:
             s, code, plane, row = bad[0]
             raise FactorizationError(f"system {s}: " + D.ntd_factor_message(code, plane, row))
         split = self.n // 2
-        f, st2 = D.ilu0_factor(self.a, *g, split)
-        bad = [s for s in range(self.batch) if int(st2[s, 0])]
-        if bad:
-            raise FactorizationError(f"system {bad[0]}: zero or non-finite pivot at row {int(st2[bad[0], 2])}")
+        if self.kind == "ntd+ilu0":
+            f, st2 = D.ilu0_factor(self.a, *g, split)
+            bad = [s for s in range(self.batch) if int(st2[s, 0])]
+            if bad:
+                raise FactorizationError(f"system {bad[0]}: zero or non-finite pivot at row {int(st2[bad[0], 2])}")
         a4 = D.sym_pack(self.a, *g)  # symmetric 4-band operator for the stencil kernels
         # The latency-bound sweeps (ILU0, NTD) of every group run on a
         # high-priority stream of their own, so an SM freed by a short stencil
@@ -187,9 +188,13 @@ class BatchSolver:
         for grp in self.groups:
             lo, hi = grp.lo, grp.hi
             grp.pcg.a4 = None if a4 is None else a4[lo:hi]
-            grp.precond = D.CombinedDevice(grp.a, self.nx, self.ny, self.nz, hi - lo, pre=pre[lo:hi], ilu=f[lo:hi],
-                                           split=split, a4=grp.pcg.a4, ilu_ctas=D.ilu0_ctas(self.batch),
-                                           ntd_ctas_=D.ntd_ctas(self.batch))
+            if self.kind == "ntd":
+                grp.precond = D.NtdDevice(pre[lo:hi], self.nx, self.ny, self.nz, hi - lo,
+                                          ntd_ctas_=D.ntd_ctas(self.batch))
+            else:
+                grp.precond = D.CombinedDevice(grp.a, self.nx, self.ny, self.nz, hi - lo, pre=pre[lo:hi],
+                                               ilu=f[lo:hi], split=split, a4=grp.pcg.a4,
+                                               ilu_ctas=D.ilu0_ctas(self.batch), ntd_ctas_=D.ntd_ctas(self.batch))
             if prio in ("hi", "lo") and len(self.groups) > 1:
                 lo_p, hi_p = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") \
                     else (0, -1)

@@ -99,10 +99,22 @@ static unsigned grid_for(i64 total)
     return (unsigned)(blocks > 0 ? blocks : 1);
 }
 
+extern "C" int ntd_apply_ex(const double *pre, const double *solve, const double *b, double *x, double *work,
+                            int64_t nx, int64_t ny, int64_t nz, int64_t batch, const int32_t *active,
+                            int64_t ctas_per_system, void *stream);
+
 extern "C" int ntd_apply(const double *pre, const double *solve, const double *b, double *x, double *work,
                          int64_t nx, int64_t ny, int64_t nz, int64_t batch, const int32_t *active, void *stream)
 {
+    return ntd_apply_ex(pre, solve, b, x, work, nx, ny, nz, batch, active, 1, stream);
+}
+
+extern "C" int ntd_apply_ex(const double *pre, const double *solve, const double *b, double *x, double *work,
+                            int64_t nx, int64_t ny, int64_t nz, int64_t batch, const int32_t *active,
+                            int64_t ctas_per_system, void *stream)
+{
     if (!pre || !b || !x || !work || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
+    if (ctas_per_system != 1 && ctas_per_system != 2) return NTD_EINVAL;
     const int K = pick_k(nx);
     const char *force = getenv("NTD_APPLY_PATH");
     const int depth = K > 0 ? sl_depth(K) : 0;
@@ -126,7 +138,8 @@ extern "C" int ntd_apply(const double *pre, const double *solve, const double *b
         switch (K) {
 #define SLCASE(KK)                                                                                                \
     case KK:                                                                                                       \
-        rc = launch_apply_sl_k<KK>(solve, bsl, xsl, xssl, zpl, (int)nx, (int)ny, (int)nz, batch, active, st);    \
+        rc = launch_apply_sl_k<KK>(solve, bsl, xsl, xssl, zpl, (int)nx, (int)ny, (int)nz, batch, active, st,     \
+                                   (int)ctas_per_system);                                                          \
         break;
             SLCASE(1) SLCASE(2) SLCASE(3) SLCASE(4) SLCASE(5) SLCASE(6) SLCASE(8) SLCASE(11)
 #undef SLCASE

@@ -68,14 +68,16 @@ def solve_bands(pre_dev, nx, ny, nz, batch):
     return sv
 
 
-def ntd_apply(pre_dev, b_dev, nx, ny, nz, batch, x=None, work=None, active=None, solve=None):
+def ntd_apply(pre_dev, b_dev, nx, ny, nz, batch, x=None, work=None, active=None, solve=None, ctas=None):
+    """x = M_NTD^{-1} b on B systems; ctas: CTAs per system (default
+    ntd_ctas(batch)); results are bitwise independent of it."""
     lib = _lib.load()
     if x is None:
         x = torch.empty_like(b_dev)
     if work is None or work.numel() < lib.ntd_apply_work_doubles(nx, ny, nz, batch):
         work = torch.empty(lib.ntd_apply_work_doubles(nx, ny, nz, batch), dtype=torch.float64, device=_dev())
-    _lib.call("ntd_apply", _lib.ptr(pre_dev), _lib.ptr(solve), _lib.ptr(b_dev), _lib.ptr(x), _lib.ptr(work), nx,
-              ny, nz, batch, _lib.ptr(active), _lib.stream())
+    _lib.call("ntd_apply_ex", _lib.ptr(pre_dev), _lib.ptr(solve), _lib.ptr(b_dev), _lib.ptr(x), _lib.ptr(work), nx,
+              ny, nz, batch, _lib.ptr(active), ntd_ctas(batch) if ctas is None else ctas, _lib.stream())
     return x
 
 
@@ -276,6 +278,34 @@ class CombinedDevice:
                            work=self.skew_work, ctas=self.ilu_ctas)
             else:
                 ilu0_apply(self.ilu, self.split, self.t, *g, z=self.xn, acc=z, active=active)
+        return z
+
+
+class NtdDevice:
+    """NTD-only preconditioner z = M_NTD^{-1} r on B systems (the reference
+    CLI's 'ntd' kind: factor_level3 + ntd_apply, bench_cli.py:113-142)."""
+
+    def __init__(self, pre, nx, ny, nz, batch, ntd_ctas_=None):
+        self.pre, self.nx, self.ny, self.nz, self.batch = pre, nx, ny, nz, batch
+        self.ntd_ctas = ntd_ctas(batch) if ntd_ctas_ is None else ntd_ctas_
+        self.solve = solve_bands(pre, nx, ny, nz, batch)
+        self.work = torch.zeros(_lib.load().ntd_apply_work_doubles(nx, ny, nz, batch), dtype=torch.float64,
+                                device=_dev())
+        self.ntd_events = None
+        self.sweep_stream = None
+
+    _sweep = CombinedDevice._sweep
+
+    def apply(self, r, z, active=None):
+        with self._sweep():
+            if self.ntd_events is not None:
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                ev[0].record()
+            ntd_apply(self.pre, r, self.nx, self.ny, self.nz, self.batch, x=z, work=self.work, active=active,
+                      solve=self.solve, ctas=self.ntd_ctas)
+            if self.ntd_events is not None:
+                ev[1].record()
+                self.ntd_events.append(ev)
         return z
 
 

@@ -311,3 +311,20 @@ def test_batch_solver_host_buffers(ntd):
         x_host.fill_(float("nan"))
     with pytest.raises(ValueError):
         solver.solve_host(b_host[:2], x_host[:2])
+
+
+def test_batch_solver_ntd_only(ntd):
+    """BatchSolver(kind='ntd') (the reference CLI's 'ntd' preconditioner) on
+    config 1 takes the drop-in pcg's iteration count with the same
+    preconditioner and converges (ntd-only for configs 1, 3)."""
+    import torch
+    from paper_1909_09771_b200 import problems
+    from paper_1909_09771_b200.batch import BatchSolver, build_precond
+    data, x_true, (nx, ny, nz) = problems.baseline_config(1)
+    a = ntd.BandedMatrix(nx, ny, nz, data)
+    b = ntd.spmv(a, x_true)
+    _, st = ntd.pcg(a, b, build_precond(a, "ntd"), tol=1e-8, max_iters=400)
+    solver = BatchSolver(torch.from_numpy(data[None]).cuda(), nx, ny, nz, kind="ntd", max_iters=400).setup()
+    res = solver.solve(torch.from_numpy(b[None]).cuda(), 1e-8)
+    assert res.converged[0] and res.final_relres[0] < 1e-8
+    assert abs(res.iterations[0] - st.iterations) <= 1, (res.iterations, st.iterations)
