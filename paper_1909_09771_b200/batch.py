@@ -269,15 +269,30 @@ class BatchSolver:
         all its systems have stopped (their later kernels are masked no-ops)."""
         act = _lib.NTD_FL["ACTIVE"]
         alive = False
+        n_act = 0
         for grp in self.groups:
             grp.events[slot].synchronize()
-            g_alive = bool(grp.flags_host[slot][:, act].any())
-            alive = alive or g_alive
-            if not g_alive and on_done is not None and grp not in done:
+            g_act = int(grp.flags_host[slot][:, act].sum())
+            n_act += g_act
+            alive = alive or g_act > 0
+            if g_act == 0 and on_done is not None and grp not in done:
                 done.add(grp)
                 with torch.cuda.stream(grp.stream):
                     on_done(grp)
+        self._map_ctas(n_act)
         return alive
+
+    def _map_ctas(self, systems):
+        """ILU0 CTA mapping for the systems still iterating (masked systems'
+        CTAs exit at once): as the batch converges, the stragglers' sweeps
+        spread over the SMs the finished systems freed.  Bitwise the same
+        results for every mapping."""
+        if not self._dynamic_ctas:
+            return
+        ctas = D.ilu0_ctas(max(1, systems))
+        for grp in self.groups:
+            if isinstance(grp.precond, D.CombinedDevice):
+                grp.precond.ilu_ctas = ctas
 
     def _run(self, b, tol, on_start=None, on_done=None):
         """PCG (precond_pcg.py:84-119) on every group, enqueued round-robin.
@@ -297,6 +312,8 @@ class BatchSolver:
 
     def _run_groups(self, b, tol, on_start, on_done, done):
         groups = self.groups
+        self._dynamic_ctas = os.environ.get("NTD_DYNAMIC_CTAS", "1") != "0"
+        self._map_ctas(self.batch)
         for grp in groups:
             with torch.cuda.stream(grp.stream):
                 if on_start is not None:
