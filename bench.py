@@ -241,10 +241,10 @@ def run_ntd(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up
-    res = None
-    for _ in range(args.warmup):
-        res = solver.solve(b_dev, args.tol)
+    # warm-up (the same pipelined call the timed region makes)
+    solver.reserve(max(args.steps, args.warmup))
+    res = solver.solve_many([b_dev] * args.warmup, args.tol, x_outs=[solver.x] * args.warmup)[-1]
+    solver.solve_host_many([b_host], [x_host], args.tol)
     barrier()
     # ---- device-timed steps (inputs resident)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -255,8 +255,9 @@ def run_ntd(args):
         barrier()
         ev[0].record()
         work_local = 0
-        for _ in range(args.steps):
-            res = solver.solve(b_dev, args.tol)
+        # K solves of the batch, pipelined per stream group (solve_many:
+        # a group starts the next solve as soon as its own systems stop)
+        for res in solver.solve_many([b_dev] * args.steps, args.tol, x_outs=[solver.x] * args.steps):
             work_local += n * sum(res.iterations)
         ev[1].record()
         barrier()
@@ -267,15 +268,14 @@ def run_ntd(args):
         grp.precond.ntd_events_timed = evs_keep
     t_dev = ev[0].elapsed_time(ev[1]) / 1e3
     # ---- e2e through the public API with host buffers: every step uploads
-    # its b from pinned host memory and downloads its x (BatchSolver.solve_host:
+    # its b from pinned host memory and downloads its x (BatchSolver.solve_host_many:
     # each stream group moves its own slice on its own stream, so the copies
     # overlap the other groups' sweeps), all inside the timed region
     ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     barrier()
     ev2[0].record()
     work_e2e = 0
-    for k in range(args.steps):
-        r2 = solver.solve_host(b_host, x_host, args.tol)
+    for r2 in solver.solve_host_many([b_host] * args.steps, [x_host] * args.steps, args.tol):
         work_e2e += n * sum(r2.iterations)
     ev2[1].record()
     barrier()

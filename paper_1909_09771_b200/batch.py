@@ -234,6 +234,149 @@ class BatchSolver:
 
         return self._solve(b, tol, None, on_start=upload, on_done=download)
 
+    def solve_many(self, bs, tol=1e-8, x_outs=None):
+        """Solve K right-hand-side batches bs[k] (B, N) one after another,
+        pipelined per stream group: a group starts its slice of solve k+1 as
+        soon as its own systems have stopped in solve k, so the converged
+        groups' SMs go to the next solve instead of idling through the
+        stragglers' last iterations.  Results (one BatchResult per solve) are
+        bitwise those of K solve() calls.  x_outs: optional K device (B, N)
+        tensors (default: one fresh tensor per solve)."""
+        bs = [as_device(b).reshape(self.batch, self.n) for b in bs]
+        if x_outs is None:
+            x_outs = [torch.empty((self.batch, self.n), dtype=torch.float64, device=self.a.device) for _ in bs]
+        xs = [x.reshape(self.batch, self.n) for x in x_outs]
+        return self._solve_pipelined(bs, xs, tol)
+
+    def solve_host_many(self, b_hosts, x_hosts, tol=1e-8):
+        """solve_many from and to host memory (pinned (B, N) CPU tensors):
+        each group uploads its slice of b_hosts[k] when it starts solve k and
+        downloads its slice of x as soon as it has finished it."""
+        for b_host, x_host in zip(b_hosts, x_hosts):
+            if tuple(b_host.shape) != (self.batch, self.n) or tuple(x_host.shape) != (self.batch, self.n):
+                raise ValueError(f"b_hosts and x_hosts must have shape ({self.batch}, {self.n})")
+            if b_host.is_cuda or x_host.is_cuda:
+                raise ValueError("solve_host_many takes host tensors; use solve_many() for device tensors")
+        if getattr(self, "_b_dev", None) is None:
+            self._b_dev = torch.empty((self.batch, self.n), dtype=torch.float64, device=self.a.device)
+        b = self._b_dev  # each group reads and writes only its own slice
+
+        def upload(grp, k):
+            b[grp.lo:grp.hi].copy_(b_hosts[k][grp.lo:grp.hi], non_blocking=True)
+
+        def download(grp, k):
+            x_hosts[k][grp.lo:grp.hi].copy_(self.x[grp.lo:grp.hi], non_blocking=True)
+
+        K = len(b_hosts)
+        return self._solve_pipelined([b] * K, [self.x] * K, tol, upload, download)
+
+    def reserve(self, solves):
+        """Preallocate the per-solve result buffers of solve_many for up to
+        `solves` right-hand sides (pinned host memory is slow to allocate).
+        The buffers are reused by later calls."""
+        bufs = getattr(self, "_pipe_bufs", None) or ([], [], [])
+        while len(bufs[0]) < solves:
+            bufs[0].append(torch.empty_like(self.history))
+            bufs[1].append(torch.zeros((self.batch, _lib.NTD_FL["N"]), dtype=torch.int32))
+            bufs[2].append(torch.zeros((self.batch, _lib.NTD_ST["N"]), dtype=torch.float64).pin_memory())
+        self._pipe_bufs = bufs
+
+    def _solve_pipelined(self, bs, xs, tol, on_start=None, on_done=None):
+        K = len(bs)
+        groups = self.groups
+        cur = torch.cuda.current_stream()
+        t0 = perf_counter()
+        for grp in groups:
+            grp.stream.wait_stream(cur)
+        self.reserve(K)
+        hist, flags_out, state_out = (v[:K] for v in self._pipe_bufs)
+        self._dynamic_ctas = os.environ.get("NTD_DYNAMIC_CTAS", "1") != "0"
+        self._map_ctas(self.batch)
+
+        def begin(grp, it):
+            grp.k_begin = it
+            grp.its = 0
+            with torch.cuda.stream(grp.stream):
+                grp.pcg.x = xs[grp.k][grp.lo:grp.hi]
+                if on_start is not None:
+                    on_start(grp, grp.k)
+                grp.pcg.init(bs[grp.k][grp.lo:grp.hi], tol)
+                z = grp.pcg.r if grp.precond is None else grp.precond.apply(grp.pcg.r, grp.pcg.z, grp.pcg.active)
+                grp.pcg.start(z)
+
+        def finish(grp, slot):
+            k, lo, hi = grp.k, grp.lo, grp.hi
+            flags_out[k][lo:hi] = grp.flags_host[slot]
+            with torch.cuda.stream(grp.stream):
+                state_out[k][lo:hi].copy_(grp.pcg.state, non_blocking=True)
+                hist[k][lo:hi].copy_(grp.pcg.history)
+                if on_done is not None:
+                    on_done(grp, k)
+
+        for grp in groups:
+            grp.k = 0
+            grp.finished = False
+            grp.its_slot = [0, 0]
+            begin(grp, 0)
+        it = 0
+        while not all(grp.finished for grp in groups):
+            it += 1
+            if it > K * (self.max_iters + 3):
+                raise RuntimeError("pipelined solve did not terminate")  # protocol error
+            for grp in groups:
+                if not grp.finished and grp.its < self.max_iters:
+                    with torch.cuda.stream(grp.stream):
+                        grp.pcg.step_update()
+                    grp.its += 1
+            for grp in groups:
+                grp.its_slot[it % 2] = grp.its
+            self._flags_async(it % 2)
+            slot = (it - 1) % 2
+            n_act = 0
+            restarted = set()
+            act = _lib.NTD_FL["ACTIVE"]
+            for grp in groups:
+                if grp.finished:
+                    continue
+                if it < grp.k_begin + 2:  # no flags of this solve yet
+                    n_act += grp.hi - grp.lo
+                    continue
+                grp.events[slot].synchronize()
+                g_act = int(grp.flags_host[slot][:, act].sum())
+                if g_act and grp.its_slot[slot] < self.max_iters:
+                    n_act += g_act
+                    continue
+                finish(grp, slot)
+                restarted.add(grp)
+                grp.k += 1
+                if grp.k < K:
+                    begin(grp, it)
+                    n_act += grp.hi - grp.lo
+                else:
+                    grp.finished = True
+            self._map_ctas(n_act)
+            for grp in groups:
+                if grp.finished or grp in restarted or grp.its >= self.max_iters:
+                    continue
+                with torch.cuda.stream(grp.stream):
+                    z = grp.pcg.r if grp.precond is None else grp.precond.apply(grp.pcg.r, grp.pcg.z,
+                                                                                  grp.pcg.active)
+                    grp.pcg.direction(z)
+        for grp in groups:
+            cur.wait_stream(grp.stream)
+        torch.cuda.current_stream().synchronize()
+        dt = perf_counter() - t0
+        out = []
+        for k in range(K):
+            fl, st = flags_out[k], state_out[k]
+            out.append(BatchResult(
+                x=xs[k], iterations=[int(v) for v in fl[:, _lib.NTD_FL["ITERS"]]],
+                converged=[int(v) == _lib.PCG_CONVERGED for v in fl[:, _lib.NTD_FL["STATUS"]]],
+                final_relres=[float(v) for v in st[:, _lib.NTD_ST["RELRES"]]],
+                status=[int(v) for v in fl[:, _lib.NTD_FL["STATUS"]]],
+                history=hist[k], setup_seconds=self.setup_seconds, solve_seconds=dt))
+        return out
+
     def _solve(self, b, tol, x_out, on_start=None, on_done=None):
         x = self.x if x_out is None else x_out.reshape(self.batch, self.n)
         for grp in self.groups:

@@ -328,3 +328,42 @@ def test_batch_solver_ntd_only(ntd):
     res = solver.solve(torch.from_numpy(b[None]).cuda(), 1e-8)
     assert res.converged[0] and res.final_relres[0] < 1e-8
     assert abs(res.iterations[0] - st.iterations) <= 1, (res.iterations, st.iterations)
+
+
+def test_batch_solver_pipelined_solves(ntd):
+    """solve_many / solve_host_many (each stream group starts the next
+    right-hand side as soon as its own systems stop) give bitwise the results
+    of sequential solve() calls: solutions, iteration counts, final relres and
+    histories; also when the iteration cap stops some systems."""
+    import torch
+    from paper_1909_09771_b200 import problems
+    from paper_1909_09771_b200.batch import BatchSolver
+    ins = [problems.baseline_config(4, s) for s in (0, 2, 14, 23)]  # 21, 24, 19, 25 iterations
+    nx, ny, nz = ins[0][2]
+    n = nx * ny * nz
+    A = torch.from_numpy(np.stack([d for d, _, _ in ins])).cuda()
+    rng = np.random.default_rng(5)
+    bs = []
+    for _ in range(3):
+        xt = rng.uniform(-1, 1, (4, n))
+        bs.append(torch.from_numpy(np.stack([ntd.spmv(ntd.BandedMatrix(nx, ny, nz, d), x)
+                                             for (d, _, _), x in zip(ins, xt)])).cuda())
+    for max_iters in (200, 22):
+        solver = BatchSolver(A, nx, ny, nz, groups=4, max_iters=max_iters).setup()
+        want = []
+        for b in bs:
+            r = solver.solve(b, 1e-8)
+            want.append((r.x.clone(), list(r.iterations), list(r.final_relres), r.history.clone(), list(r.status)))
+        got = solver.solve_many(bs, 1e-8)
+        b_hosts = [b.cpu().pin_memory() for b in bs]
+        x_hosts = [torch.full_like(bh, float("nan")).pin_memory() for bh in b_hosts]
+        got_h = solver.solve_host_many(b_hosts, x_hosts, 1e-8)
+        for k, (x, its, rel, hist, status) in enumerate(want):
+            for g in (got[k], got_h[k]):
+                assert list(g.iterations) == its and list(g.final_relres) == rel and list(g.status) == status
+                for s in range(4):
+                    assert torch.equal(g.history[s, :min(its[s], max_iters)], hist[s, :min(its[s], max_iters)])
+            assert torch.equal(got[k].x, x)
+            assert torch.equal(x_hosts[k], x.cpu())
+        if max_iters == 22:
+            assert any(not c for c in got[0].converged)
