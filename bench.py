@@ -243,7 +243,9 @@ def run_ntd(args):
 
     # warm-up (the same pipelined call the timed region makes)
     solver.reserve(max(args.steps, args.warmup))
-    res = solver.solve_many([b_dev] * args.warmup, args.tol, x_outs=[solver.x] * args.warmup)[-1]
+    # (at least one solve: it also yields the iteration stats checked below)
+    nw = max(1, args.warmup)
+    res = solver.solve_many([b_dev] * nw, args.tol, x_outs=[solver.x] * nw)[-1]
     solver.solve_host_many([b_host], [x_host], args.tol)
     barrier()
     # ---- device-timed steps (inputs resident)

@@ -252,6 +252,8 @@ class BatchSolver:
         """solve_many from and to host memory (pinned (B, N) CPU tensors):
         each group uploads its slice of b_hosts[k] when it starts solve k and
         downloads its slice of x as soon as it has finished it."""
+        if len(b_hosts) != len(x_hosts):
+            raise ValueError("b_hosts and x_hosts must have the same length")
         for b_host, x_host in zip(b_hosts, x_hosts):
             if tuple(b_host.shape) != (self.batch, self.n) or tuple(x_host.shape) != (self.batch, self.n):
                 raise ValueError(f"b_hosts and x_hosts must have shape ({self.batch}, {self.n})")
@@ -283,6 +285,8 @@ class BatchSolver:
 
     def _solve_pipelined(self, bs, xs, tol, on_start=None, on_done=None):
         K = len(bs)
+        if K == 0:
+            return []
         groups = self.groups
         cur = torch.cuda.current_stream()
         t0 = perf_counter()

@@ -358,6 +358,7 @@ def test_batch_solver_pipelined_solves(ntd):
         b_hosts = [b.cpu().pin_memory() for b in bs]
         x_hosts = [torch.full_like(bh, float("nan")).pin_memory() for bh in b_hosts]
         got_h = solver.solve_host_many(b_hosts, x_hosts, 1e-8)
+        assert solver.solve_many([], 1e-8) == [] and solver.solve_host_many([], [], 1e-8) == []
         for k, (x, its, rel, hist, status) in enumerate(want):
             for g in (got[k], got_h[k]):
                 assert list(g.iterations) == its and list(g.final_relres) == rel and list(g.status) == status
