@@ -8,6 +8,7 @@
 // Reductions are deterministic fixed-order trees (per-block partials in a
 // fixed row assignment, then one block per system sums them in order).
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -27,6 +28,24 @@ int check_launch(const char *where)
         return NTD_ELAUNCH;
     }
     return NTD_OK;
+}
+
+static i64 env_int(const char *name, i64 dflt)
+{
+    const char *v = getenv(name);
+    if (!v || !*v) return dflt;
+    i64 x = atoll(v);
+    return x > 0 ? x : dflt;
+}
+i64 rows_block_cap()
+{
+    static const i64 cap = env_int("NTD_ROWS_BLOCKS", 148 * 8);
+    return cap;
+}
+int stn_grid(int full)
+{
+    static const i64 g = env_int("NTD_STN_GRID", 1 << 30);
+    return (int)(g < full ? g : full);
 }
 }  // namespace ntd
 
@@ -85,7 +104,7 @@ __global__ void __launch_bounds__(256) k_spmv(const double *__restrict__ a, cons
 static unsigned grid_rows(i64 n)
 {
     i64 b = (n + 255) / 256;
-    i64 cap = 148 * 8;
+    i64 cap = ntd::rows_block_cap();
     return (unsigned)(b < cap ? (b > 0 ? b : 1) : cap);
 }
 
@@ -354,16 +373,20 @@ __global__ void __launch_bounds__(RED_THREADS) k_spmv_dot(const double *__restri
     if (active && !active[s]) return;
     const double *as = a + s * NB * n, *ps = p + s * n;
     double *aps = ap + s * n;
-    double acc = 0.0;
+    // virtual blocks vb = the partials' owners, so the reduction tree (and the
+    // result) is the same for any grid of at most STN_BLOCKS blocks
+    for (int vb = blockIdx.x; vb < STN_BLOCKS; vb += gridDim.x) {
+        double acc = 0.0;
 #pragma unroll STN_UNROLL
-    for (i64 i = blockIdx.x * (i64)RED_THREADS + threadIdx.x; i < n; i += (i64)STN_BLOCKS * RED_THREADS) {
-        double y = row_of<NB>(as, ps, i, n, nx, nxy);
-        aps[i] = y;
-        acc = add_rn(acc, mul_rn(ps[i], y));
+        for (i64 i = vb * (i64)RED_THREADS + threadIdx.x; i < n; i += (i64)STN_BLOCKS * RED_THREADS) {
+            double y = row_of<NB>(as, ps, i, n, nx, nxy);
+            aps[i] = y;
+            acc = add_rn(acc, mul_rn(ps[i], y));
+        }
+        const double wsum = warp_sum(acc);
+        if ((threadIdx.x & 31) == 0) part[s * MAX_PARTS + vb * (RED_THREADS / 32) + (threadIdx.x >> 5)] = wsum;
     }
     (void)sh;
-    const double wsum = warp_sum(acc);
-    if ((threadIdx.x & 31) == 0) part[s * MAX_PARTS + blockIdx.x * (RED_THREADS / 32) + (threadIdx.x >> 5)] = wsum;
 }
 
 // pap, breakdown check, alpha (precond_pcg.py:99-102)
@@ -394,7 +417,7 @@ static int spmv_alpha_nb(const double *a, const double *p, double *ap, double *s
     if (!a || !p || !ap || !state || !flags || !active || !work || batch < 1) return NTD_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     i64 n = nx * ny * nz;
-    dim3 grid(STN_BLOCKS, (unsigned)batch);
+    dim3 grid(ntd::stn_grid(STN_BLOCKS), (unsigned)batch);
     k_spmv_dot<NB><<<grid, RED_THREADS, 0, st>>>(a, p, ap, work, n, nx, nx * ny, active);
     int rc = ntd::check_launch("spmv_dot");
     if (rc) return rc;
@@ -440,15 +463,17 @@ __global__ void __launch_bounds__(RED_THREADS) k_true_res(const double *__restri
     i64 s = blockIdx.y;
     if (!active[s]) return;
     const double *as = a + s * NB * n, *xs = x + s * n, *bs = b + s * n;
-    double acc = 0.0;
+    for (int vb = blockIdx.x; vb < STN_BLOCKS; vb += gridDim.x) {  // virtual blocks, as in k_spmv_dot
+        double acc = 0.0;
 #pragma unroll STN_UNROLL
-    for (i64 i = blockIdx.x * (i64)RED_THREADS + threadIdx.x; i < n; i += (i64)STN_BLOCKS * RED_THREADS) {
-        double res = add_rn(-row_of<NB>(as, xs, i, n, nx, nxy), bs[i]);
-        acc = add_rn(acc, mul_rn(res, res));
+        for (i64 i = vb * (i64)RED_THREADS + threadIdx.x; i < n; i += (i64)STN_BLOCKS * RED_THREADS) {
+            double res = add_rn(-row_of<NB>(as, xs, i, n, nx, nxy), bs[i]);
+            acc = add_rn(acc, mul_rn(res, res));
+        }
+        const double wsum = warp_sum(acc);
+        if ((threadIdx.x & 31) == 0) part[s * MAX_PARTS + vb * (RED_THREADS / 32) + (threadIdx.x >> 5)] = wsum;
     }
     (void)sh;
-    const double wsum = warp_sum(acc);
-    if ((threadIdx.x & 31) == 0) part[s * MAX_PARTS + blockIdx.x * (RED_THREADS / 32) + (threadIdx.x >> 5)] = wsum;
 }
 
 // relres, history, convergence (precond_pcg.py:106-114)
@@ -490,7 +515,7 @@ static int update_residual_nb(const double *a, const double *b, double *x, doubl
     k_update_xr<<<grid, 256, 0, st>>>(x, r, p, ap, state, n, active);
     int rc = ntd::check_launch("update_xr");
     if (rc) return rc;
-    dim3 g2(STN_BLOCKS, (unsigned)batch);
+    dim3 g2(ntd::stn_grid(STN_BLOCKS), (unsigned)batch);
     k_true_res<NB><<<g2, RED_THREADS, 0, st>>>(a, b, x, work, n, nx, nx * ny, active);
     rc = ntd::check_launch("true_res");
     if (rc) return rc;

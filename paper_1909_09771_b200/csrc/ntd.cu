@@ -239,7 +239,7 @@ extern "C" int ntd_residual_to_slot(const double *a, int64_t bands, const double
     const int K = pick_k(nx);
     if (K <= 0 || !sl_depth(K) || nx * ny * nz >= (1ll << 31)) return NTD_ENOTSUP;
     const i64 n = nx * ny * nz;
-    dim3 grid((unsigned)std::min<i64>((n + 255) / 256, 148 * 8), (unsigned)batch);
+    dim3 grid((unsigned)std::min<i64>((n + 255) / 256, ntd::rows_block_cap()), (unsigned)batch);
     if (bands == 4)
         k_residual_to_sl<4><<<grid, 256, 0, (cudaStream_t)stream>>>(a, pre, r, w, work, n, (int)nx, nx * ny, K, active);
     else
@@ -289,7 +289,7 @@ extern "C" int ntd_residual_from_slot(const double *a, int64_t bands, const doub
     if (K <= 0 || !sl_depth(K) || nx * ny * nz >= (1ll << 31)) return NTD_ENOTSUP;
     const i64 n = nx * ny * nz, s = sl_doubles(nx, ny, nz) * batch;
     const double *xsl = work + s;
-    dim3 grid((unsigned)std::min<i64>((n + 255) / 256, 148 * 8), (unsigned)batch);
+    dim3 grid((unsigned)std::min<i64>((n + 255) / 256, ntd::rows_block_cap()), (unsigned)batch);
     if (bands == 4)
         k_residual_from_sl<4><<<grid, 256, 0, (cudaStream_t)stream>>>(a, r, w, xsl, z_out, t, n, (int)nx, nx * ny,
                                                                       (int)ny, K, active);
