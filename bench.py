@@ -14,6 +14,13 @@ with inputs resident; `e2e` adds the host->device copy of b and the
 device->host copy of x every step (public BatchSolver API).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ntd|reference]
+
+`--gpus N` with N > 1 outside torchrun re-launches itself under
+`torch.distributed.run` with N ranks (one per GPU, NCCL); under torchrun the
+world size must equal N.  At N = 1 the line also carries `configs`: the
+single-system BASELINE configs 1, 2, 3 and 5 (PCG, NTD and combined apply
+rates, % of HBM, iterations against the reference's, apply error against the
+CPU oracle, and a CPU-port baseline for configs 1-3).
 """
 
 import argparse
@@ -56,6 +63,7 @@ def parse():
                     help="preconditioner (SURVEY.md 8(d) also reports ntd-only for configs 1 and 3)")
     ap.add_argument("--cpu-systems", type=int, default=None, help="CPU baseline sample size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the single-system configs 1, 2, 3, 5")
     return ap.parse_args()
 
 
@@ -133,11 +141,8 @@ def cpu_solve_systems(cfg, systems, threads, tol, kind="ntd+ilu0"):
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     import oracle
     from concurrent.futures import ThreadPoolExecutor
-    inputs = [system_inputs(cfg, s) for s in systems]
-    built = []
-
-    def setup(inp):
-        data, x_true, (nx, ny, nz) = inp
+    def setup(s):
+        data, x_true, (nx, ny, nz) = system_inputs(cfg, s)
         b = oracle.spmv(data, x_true, nx, ny, nz)
         pre = oracle.factor_level3(data, nx, ny, nz)
         ilu = oracle.build_block_ilu0(data, nx, ny, nz) if kind == "ntd+ilu0" else None
@@ -145,7 +150,7 @@ def cpu_solve_systems(cfg, systems, threads, tol, kind="ntd+ilu0"):
 
     t0 = time.perf_counter()
     with ThreadPoolExecutor(threads) as ex:
-        built = list(ex.map(setup, inputs))
+        built = list(ex.map(setup, systems))
     t_setup = time.perf_counter() - t0
 
     def solve(item):
@@ -160,12 +165,27 @@ def cpu_solve_systems(cfg, systems, threads, tol, kind="ntd+ilu0"):
     return sum(r[0] for r in res), t_solve, t_setup, [r[1] for r in res]
 
 
+def host_cores():
+    """(cores of the host, cores this process may run on)."""
+    total = os.cpu_count() or 1
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        usable = total
+    return total, usable
+
+
+def cpu_threads():
+    """P = min(64, cores) systems at once, one
+    per thread (the reference has no batch API: one solve per core)."""
+    return max(1, min(64, host_cores()[1]))
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    cores = os.cpu_count() or 1
-    sample = args.cpu_systems or min(cores, 8)
+    sample = args.cpu_systems or cpu_threads()
     cfg = args.config
     n_sys = args.systems or (64 if cfg == 4 else 1)
     systems = list(range(min(sample, n_sys)))
@@ -177,15 +197,18 @@ def run_reference(args):
         vals.append(work / t / 1e6)
         ts.append(t)
     v = float(np.median(vals))
+    total, usable = host_cores()
     desc = (f"{len(systems)} of the {n_sys} config-{cfg} systems per step, each a full {args.precond} PCG solve "
-            f"to {args.tol:g} by the C oracle (restatement of the reference kernels), one system per thread")
+            f"to {args.tol:g} by the C oracle (restatement of the reference kernels), one system per thread, "
+            f"{len(systems)} threads on a host with {total} cores ({usable} usable)")
     out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(ts)), "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "impl": "reference",
            "config": {"workload": f"cfg{cfg}", "systems": n_sys, "grid": "96^3" if cfg == 4 else None,
                       "precond": args.precond, "tol": args.tol, "parallelism": "cpu-threads"},
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": sample, "kind": "port", "sample": desc},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": len(systems), "threads": len(systems),
+                            "host_cores": total, "usable_cores": usable, "kind": "port", "sample": desc},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -371,6 +394,8 @@ def run_ntd(args):
         }
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(args)
+        if world == 1 and cfg == 4 and not args.no_configs:
+            out["configs"] = single_configs(peak[0], cpu=not args.no_cpu_baseline)
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -435,6 +460,113 @@ def stencil_roofline(solver, B, n, nx, ny, nz):
     return out
 
 
+# reference iteration counts of the single-system configs (reference package
+# on the seeded inputs)
+SINGLE_REF_ITERS = {1: 9, 2: 26, 3: 10, 5: 71}
+COMBINED_APPLY_BYTES_PER_UNKNOWN = 304
+PCG_ITER_BYTES = 488
+
+
+def single_configs(peak, cfgs=(1, 2, 3, 5), cpu=True):
+    """BASELINE configs 1, 2, 3, 5 (one system each) through the public API on
+    device-resident inputs: PCG (ntd+ilu0, tol 1e-8) solve rate and
+    iterations against the reference's, the NTD and combined applies alone
+    (CUDA events, median), each against the HBM roofline at the canonical
+    bytes (48 / 304 / 488 B per unknown), apply errors
+    against the CPU oracle (the C restatement of the reference) on a seeded
+    vector, and for configs 1-3 the oracle's own single-thread PCG solve as
+    the CPU baseline."""
+    import torch
+    import paper_1909_09771_b200 as ntd
+    from paper_1909_09771_b200 import _lib, problems
+    from paper_1909_09771_b200 import device as D
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+    out = {}
+    for cfg in cfgs:
+        nx, ny, nz = problems.CONFIGS[cfg]["grid"]
+        n = nx * ny * nz
+        kap, bc, rng = problems.baseline_kappa(cfg, 0)
+        x_true = rng.uniform(-1.0, 1.0, n)
+        a_dev = D.assemble(torch.from_numpy(kap).cuda(), nx, ny, nz, bc)[0]
+        a = ntd.BandedMatrix(nx, ny, nz, a_dev)
+        b = ntd.spmv(a, torch.from_numpy(x_true).cuda())
+        del kap
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cp = ntd.CombinedPrecond(a)
+        setup_s = time.perf_counter() - t0
+        reps = {1: 5, 2: 3, 3: 3, 5: 1}[cfg]
+        solves = []
+        for r in range(reps + 1):
+            x, st = ntd.pcg(a, b, cp, tol=1e-8)
+            if r:
+                solves.append(st.solve_seconds)
+        solve_s = float(np.median(solves))
+        rate = n * st.iterations / solve_s / 1e6
+        # applies alone: CUDA events around R calls on the device-level objects
+        dv = cp._dev
+        v = torch.from_numpy(np.random.default_rng(100 + cfg).uniform(-1.0, 1.0, n)).cuda().reshape(1, n)
+        z = torch.empty_like(v)
+        pre = cp.ntd
+
+        def timed(fn, R):
+            fn()
+            ts = []
+            for _ in range(R):
+                e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                e[0].record()
+                fn()
+                e[1].record()
+                torch.cuda.synchronize()
+                ts.append(e[0].elapsed_time(e[1]) / 1e3)
+            return float(np.median(ts))
+        R = {1: 20, 2: 10, 3: 5, 5: 3}[cfg]
+        t_ntd = timed(lambda: D.ntd_apply(pre.bands.reshape(1, 7, n), v, nx, ny, nz, 1, x=z,
+                                          work=cp.workspace.work(nx, ny, nz), solve=pre.solve), R)
+        t_comb = timed(lambda: dv.apply(v, z), R)
+        t_ilu = timed(lambda: D.ilu0_apply(dv.ilu, dv.split, v, nx, ny, nz, 1, z=z, skew=dv.skew,
+                                           work=dv.skew_work, ctas=dv.ilu_ctas), R)
+        # parity against the oracle on the same vector (the GPU factor is
+        # bitwise the reference's: tests/test_gpu_api.py)
+        vh = v[0].cpu().numpy()
+        pre_h = pre.host()
+        x_gpu = ntd.ntd_apply(pre, vh)
+        x_orc = oracle.ntd_apply(pre_h, vh, nx, ny, nz, nthreads=2)
+        err = float(np.abs(x_gpu - x_orc).max() / np.abs(x_orc).max())
+        rec = {"workload": f"cfg{cfg}", "grid": f"{nx}x{ny}x{nz}", "unknowns": n,
+               "pcg": {"iterations": st.iterations, "reference_iterations": SINGLE_REF_ITERS[cfg],
+                       "converged": st.converged, "final_relres": st.final_relres, "setup_ms": 1e3 * setup_s,
+                       "solve_ms": 1e3 * solve_s, "value": rate, "unit": UNIT,
+                       "hbm_frac_canonical": PCG_ITER_BYTES * rate * 1e6 / 1e9 / peak},
+               "ntd_apply": {"ms": 1e3 * t_ntd, "munknowns_per_s": n / t_ntd / 1e6,
+                             "hbm_frac": NTD_APPLY_BYTES_PER_UNKNOWN * n / t_ntd / 1e9 / peak},
+               "combined_apply": {"ms": 1e3 * t_comb, "munknowns_per_s": n / t_comb / 1e6,
+                                  "hbm_frac": COMBINED_APPLY_BYTES_PER_UNKNOWN * n / t_comb / 1e9 / peak},
+               "ilu0_apply_ms": 1e3 * t_ilu,
+               "ntd_apply_rel_err_vs_oracle": err}
+        if cfg != 5:
+            data = a.host_data()
+            fo, split = oracle.build_block_ilu0(data, nx, ny, nz)
+            zc = oracle.combined_apply(data, pre_h, fo, split, vh, nx, ny, nz)
+            zg = ntd.combined_apply(cp, vh)
+            rec["combined_apply_rel_err_vs_oracle"] = float(np.abs(zg - zc).max() / np.abs(zc).max())
+            if cpu:
+                bh = b.cpu().numpy()
+                t0 = time.perf_counter()
+                _, it_o, conv_o, _ = oracle.pcg(data, bh, nx, ny, nz, tol=1e-8, pre=pre_h, ilu=(fo, split))
+                t_o = time.perf_counter() - t0
+                rec["cpu_baseline"] = {"value": n * it_o / t_o / 1e6, "unit": UNIT, "cores": 1, "threads": 1,
+                                       "kind": "port", "iterations": it_o,
+                                       "sample": f"one full ntd+ilu0 PCG solve of config {cfg} by the C oracle "
+                                                 f"(single thread, factorisations excluded), {t_o:.2f} s"}
+                rec["gpu_over_cpu"] = rate / rec["cpu_baseline"]["value"]
+        out[f"cfg{cfg}"] = rec
+        del cp, a, a_dev, b, x, pre_h
+        torch.cuda.empty_cache()
+    return out
+
+
 def _traffic(cfg, systems):
     """ncu-measured DRAM bytes per launch of the dominant kernel (profiles/)."""
     try:
@@ -480,17 +612,38 @@ def _measured_peak():
 
 
 def cpu_baseline(args):
-    cores = os.cpu_count() or 1
-    sample = args.cpu_systems or min(cores, 8)
+    sample = args.cpu_systems or cpu_threads()
     systems = list(range(sample))
     work, t, _, iters = cpu_solve_systems(args.config, systems, sample, args.tol, args.precond)
-    return {"value": work / t / 1e6, "unit": UNIT, "cores": sample, "kind": "port",
+    total, usable = host_cores()
+    return {"value": work / t / 1e6, "unit": UNIT, "cores": sample, "threads": sample, "host_cores": total,
+            "usable_cores": usable, "kind": "port",
             "sample": f"{sample} config-{args.config} systems, full {args.precond} PCG solve each (C oracle), "
-                      f"one system per host thread; solve wall {t:.1f} s, iterations {iters}"}
+                      f"one system per host thread ({sample} threads, host {total} cores, {usable} usable); "
+                      f"solve wall {t:.1f} s, iterations {iters}"}
+
+
+def relaunch(args):
+    """`--gpus N` outside torchrun: run this script as N ranks under
+    torch.distributed.run (one process per GPU, NCCL on 127.0.0.1)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the communicator log shows every rank
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
     args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:
+        sys.exit(relaunch(args))
+    if world > 1 and world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -93,6 +93,23 @@ int ntd_dot(const double *x, const double *y, double *out, int sqrt_out,
             int64_t n, int64_t batch, double *work, const int32_t *active,
             void *stream);
 
+/* out = alpha*x + y as a new vector (banded_core.py:139-143 axpy: product
+ * rounded, then the sum; bitwise). */
+int ntd_axpy(double alpha, const double *x, const double *y, double *out,
+             int64_t n, void *stream);
+
+/* chains independent bidiagonal recurrences of n cells each (arrays
+ * (chains, n)), chain_bidiagonal_solve (ntd_solve.py:272-300):
+ * x[i] = (b[i] - offdiag[i]*x[i_prev]) * diag_recip[i], forward (backward = 0)
+ * or backward (1), with the reference's `lanes`-chunk affine composition
+ * (_chain_scaled, ntd_solve.py:20-64); bitwise.  work >=
+ * ntd_chain_work_doubles(n, chains). */
+int64_t ntd_chain_work_doubles(int64_t n, int64_t chains);
+int ntd_chain_solve(const double *diag_recip, const double *offdiag,
+                    const double *b, double *x, double *work, int64_t n,
+                    int64_t chains, int64_t backward, int64_t lanes,
+                    void *stream);
+
 /* -------- PCG building blocks (precond_pcg.py:68-122) ------------------
  * Per-system scalar state lives on the device: state (double[B][NTD_ST_N])
  * and flags (int32[B][NTD_FL_N]).  history: double[B][max_iters]. */
@@ -177,6 +194,14 @@ int ntd_apply_ex(const double *pre, const double *solve, const double *b,
                  int64_t batch, const int32_t *active, int64_t ctas_per_system,
                  void *stream);
 
+/* The direct-load apply on the reference band layout (the path every grid
+ * without slot-layout records takes: nx > 352, or misaligned buffers),
+ * exported so it can be checked against the slot-layout path on any grid.
+ * work: >= ntd_apply_work_doubles.  Same result to rounding (<= 1e-10). */
+int ntd_apply_direct(const double *pre, const double *b, double *x,
+                     double *work, int64_t nx, int64_t ny, int64_t nz,
+                     int64_t batch, const int32_t *active, void *stream);
+
 /* Fused combined-preconditioner stages around the NTD apply (the middle of
  * precond_pcg.py:57-65), working on the apply's slot-layout buffers in
  * `work` (>= ntd_apply_work_doubles; zero-filled once by the caller) so the
@@ -201,10 +226,6 @@ int ntd_apply_slot_ex(const double *solve, double *work, int64_t nx,
                       int64_t ny, int64_t nz, int64_t batch,
                       const int32_t *active, int64_t ctas_per_system,
                       void *stream);
-/* Measurement switch: 0 disables the split sweep's shared-memory plane
- * buffers (the solver then reads neighbour and lower-sweep lines from global
- * memory, as the one-CTA sweep does).  Results are bitwise the same. */
-int ntd_set_smb(int on);
 int ntd_residual_from_slot(const double *a, int64_t bands, const double *work,
                            const double *r, const double *w, double *z_out,
                            double *t, int64_t nx, int64_t ny, int64_t nz,

@@ -11,8 +11,6 @@ import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libntdgpu.so")
-# experiments only: load a variant build instead (must be a libntdgpu built from this tree)
-LIB_PATH = os.environ.get("NTD_LIB_OVERRIDE", LIB_PATH)
 
 NTD_ST = dict(RZ=0, PAP=1, ALPHA=2, BETA=3, BNORM=4, RELRES=5, TOL=6, N=8)
 NTD_FL = dict(ACTIVE=0, STATUS=1, ITERS=2, N=4)
@@ -34,6 +32,9 @@ _SIGS = {
     "ntd_residual_sym": (_INT, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_dot_work_doubles": (_I, [_I]),
     "ntd_dot": (_INT, [_P, _P, _P, _INT, _I, _I, _P, _P, _P]),
+    "ntd_axpy": (_INT, [ctypes.c_double, _P, _P, _P, _I, _P]),
+    "ntd_chain_work_doubles": (_I, [_I, _I]),
+    "ntd_chain_solve": (_INT, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P]),
     "ntd_pcg_init": (_INT, [_P, _P, _P, _P, _P, _P, ctypes.c_double, _I, _I, _P, _P]),
     "ntd_pcg_start": (_INT, [_P, _P, _P, _P, _P, _I, _I, _P, _P]),
     "ntd_pcg_spmv_alpha": (_INT, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
@@ -50,10 +51,10 @@ _SIGS = {
     "ntd_solve_bands": (_INT, [_P, _P, _I, _I, _I, _I, _P]),
     "ntd_apply": (_INT, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_apply_ex": (_INT, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _I, _P]),
+    "ntd_apply_direct": (_INT, [_P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_residual_to_slot": (_INT, [_P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_apply_slot": (_INT, [_P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_apply_slot_ex": (_INT, [_P, _P, _I, _I, _I, _I, _P, _I, _P]),
-    "ntd_set_smb": (_INT, [ctypes.c_int]),
     "ntd_residual_from_slot": (_INT, [_P, _I, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
     "ntd_ilu0_factor": (_INT, [_P, _P, _I, _P, _I, _I, _I, _I, _P]),
     "ntd_ilu0_apply": (_INT, [_P, _I, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
@@ -69,9 +70,9 @@ EXPORTED = tuple(_SIGS)
 # kernels launched by one successful call of each entry point (counted for
 # bench.py's gpu_launches; see the launch sites in csrc/)
 KERNELS_PER_CALL = {
-    "ntd_assemble": 1, "ntd_spmv": 1, "ntd_residual": 1, "ntd_dot": 2, "ntd_pcg_init": 3, "ntd_pcg_start": 3,
+    "ntd_assemble": 1, "ntd_spmv": 1, "ntd_residual": 1, "ntd_axpy": 1, "ntd_chain_solve": 1, "ntd_dot": 2, "ntd_pcg_init": 3, "ntd_pcg_start": 3,
     "ntd_pcg_spmv_alpha": 2, "ntd_pcg_update_residual": 3, "ntd_pcg_direction": 3, "ntd_factor": 1,
-    "ntd_apply": 3, "ntd_apply_ex": 3, "ntd_solve_bands": 1, "ntd_ilu0_factor": 2, "ntd_ilu0_apply": 1, "ntd_ilu0_skew_build": 1,
+    "ntd_apply": 3, "ntd_apply_ex": 3, "ntd_apply_direct": 1, "ntd_solve_bands": 1, "ntd_ilu0_factor": 2, "ntd_ilu0_apply": 1, "ntd_ilu0_skew_build": 1,
     "ntd_ilu0_skew_apply": 1, "ntd_ilu0_skew_apply_ex": 1, "ntd_sym_pack": 1, "ntd_residual_sym": 1, "ntd_pcg_spmv_alpha_sym": 2,
     "ntd_pcg_update_residual_sym": 3, "ntd_residual_to_slot": 1, "ntd_apply_slot": 1, "ntd_apply_slot_ex": 1,
     "ntd_residual_from_slot": 1,

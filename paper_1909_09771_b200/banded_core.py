@@ -66,7 +66,14 @@ class BandedMatrix:
     """Matrix on an nx*ny*nz grid stored as seven length-N diagonals
     (banded_core.py:36-92).  Row order of ``data``: -nx*ny, -nx, -1, 0, +1,
     +nx, +nx*ny.  ``data`` may be a numpy array (host) or a CUDA tensor; the
-    GPU kernels read a device copy (``device_data()``)."""
+    GPU kernels read a device copy (``device_data()``).
+
+    Host-backed matrices keep that device copy cached, so repeated spmv / pcg
+    calls upload A once.  The cache is dropped whenever ``data`` is assigned
+    or read through the ``data`` attribute or ``band()`` (the ways the
+    reference's users modify A in place), and by ``invalidate()``; a caller
+    that writes through an array reference it kept from before must call
+    ``invalidate()`` itself."""
 
     def __init__(self, nx, ny, nz, data=None):
         if nx < 1 or ny < 1 or nz < 1:
@@ -85,7 +92,24 @@ class BandedMatrix:
             data = np.ascontiguousarray(data, dtype=np.float64)
             if data.shape != (N_BANDS, n):
                 raise ValueError(f"band data must have shape ({N_BANDS}, {n}), got {data.shape}")
-        self.data = data
+        self._data = data
+        self._dev = None
+
+    @property
+    def data(self):
+        # the caller may write through the returned array: drop the device copy
+        self._dev = None
+        return self._data
+
+    @data.setter
+    def data(self, value):
+        self._data = value
+        self._dev = None
+
+    def invalidate(self):
+        """Drop the cached device copy (after writing to host band data
+        through a reference taken earlier)."""
+        self._dev = None
 
     @property
     def n_rows(self):
@@ -104,19 +128,25 @@ class BandedMatrix:
         return self.data[idx]
 
     def copy(self):
-        d = self.data.clone() if isinstance(self.data, torch.Tensor) else self.data.copy()
+        d = self._data.clone() if isinstance(self._data, torch.Tensor) else self._data.copy()
         return BandedMatrix(self.nx, self.ny, self.nz, d)
 
     def cuda(self):
         """A BandedMatrix whose data lives on the GPU (zero-copy for kernels)."""
-        return BandedMatrix(self.nx, self.ny, self.nz, as_device(self.data).clone())
+        return BandedMatrix(self.nx, self.ny, self.nz, as_device(self._data).clone())
 
     def device_data(self):
-        """(7, N) fp64 CUDA tensor of the bands (uploaded from host data)."""
-        return as_device(self.data)
+        """(7, N) fp64 CUDA tensor of the bands: the data itself when it is a
+        CUDA tensor, else the cached upload of the host bands."""
+        d = self._data
+        if isinstance(d, torch.Tensor) and d.is_cuda:
+            return as_device(d)
+        if self._dev is None:
+            self._dev = as_device(d)
+        return self._dev
 
     def host_data(self):
-        d = self.data
+        d = self._data
         return d.cpu().numpy() if isinstance(d, torch.Tensor) else d
 
     def to_dense(self):
@@ -161,20 +191,29 @@ def dot(x, y):
     """banded_core.py:133-136 (deterministic tree reduction on the GPU)."""
     if _shape(x) != _shape(y):
         raise ValueError("dot operands must have equal length")
-    return float(dot_device(as_device(x), as_device(y))[0].item())
+    xd, yd = as_device(x).reshape(-1), as_device(y).reshape(-1)
+    if xd.numel() == 0:
+        return 0.0
+    return float(dot_device(xd, yd)[0].item())
 
 
 def axpy(alpha, x, y):
-    """alpha*x + y as a new vector (banded_core.py:139-143)."""
+    """alpha*x + y as a new vector (banded_core.py:139-143): one kernel
+    (ntd_axpy), the product rounded and then the sum, bitwise numpy's."""
     if _shape(x) != _shape(y):
         raise ValueError("axpy operands must have equal length")
-    out = alpha * as_device(x) + as_device(y)  # two roundings, as numpy
-    return like_input(out, x if isinstance(x, torch.Tensor) else y)
+    xd, yd = as_device(x).reshape(-1), as_device(y).reshape(-1)
+    out = torch.empty_like(xd)
+    if xd.numel():
+        _lib.call("ntd_axpy", float(alpha), _lib.ptr(xd), _lib.ptr(yd), _lib.ptr(out), xd.numel(), _lib.stream())
+    return like_input(out.reshape(_shape(x)), x if isinstance(x, torch.Tensor) else y)
 
 
 def norm2(x):
     """banded_core.py:146-147"""
-    xd = as_device(x)
+    xd = as_device(x).reshape(-1)
+    if xd.numel() == 0:
+        return 0.0
     return float(dot_device(xd, xd, sqrt=True)[0].item())
 
 

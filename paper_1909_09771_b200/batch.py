@@ -87,9 +87,6 @@ def default_groups(batch):
     """Stream groups for a batch: the NTD apply and the ILU0 sweeps are
     latency-bound (one CTA per system / half), so while one group sweeps, the
     bandwidth-bound stencil/CG kernels of the other run on the idle SMs."""
-    env = os.environ.get("NTD_STREAM_GROUPS")
-    if env:
-        return max(1, min(int(env), batch))
     # CUDA multiplexes streams over CUDA_DEVICE_MAX_CONNECTIONS hardware queues
     # (default 8; the package raises the default to 32 before CUDA starts):
     # more groups than queues serialise (16 groups on 8 queues: 1.5x slower).
@@ -123,7 +120,8 @@ class BatchSolver:
     one iteration late (converged systems are masked on the device, so the
     extra enqueued iteration does no work for them)."""
 
-    def __init__(self, a_dev, nx, ny, nz, kind="ntd+ilu0", max_iters=200, groups=None):
+    def __init__(self, a_dev, nx, ny, nz, kind="ntd+ilu0", max_iters=200, groups=None, sweep_priority="hi",
+                 dynamic_ctas=True):
         if kind not in ("ntd+ilu0", "ntd", "none"):
             raise ValueError("BatchSolver supports 'ntd+ilu0', 'ntd' and 'none'")
         self.a = as_device(a_dev)
@@ -132,8 +130,15 @@ class BatchSolver:
         self.n = nx * ny * nz
         if tuple(self.a.shape) != (self.batch, 7, self.n):
             raise ValueError("a_dev must have shape (B, 7, nx*ny*nz)")
+        if sweep_priority not in ("hi", "lo", "off"):
+            raise ValueError("sweep_priority must be 'hi', 'lo' or 'off'")
         self.kind = kind
         self.max_iters = max_iters
+        # sweep_priority: stream priority of the latency-bound sweeps (see
+        # setup); dynamic_ctas: re-map the ILU0 CTAs to the systems still
+        # iterating (bitwise neutral).  Both exist for measurements.
+        self.sweep_priority = sweep_priority
+        self.dynamic_ctas = dynamic_ctas
         self.setup_seconds = 0.0
         G = default_groups(self.batch) if groups is None else max(1, min(int(groups), self.batch))
         self.x = torch.empty((self.batch, self.n), dtype=torch.float64, device=self.a.device)
@@ -179,10 +184,10 @@ class BatchSolver:
         # The latency-bound sweeps (ILU0, NTD) of every group run on a
         # high-priority stream of their own, so an SM freed by a short stencil
         # kernel goes to a waiting sweep CTA first: +1.8% on the 64-system
-        # batch (8 alternating runs).  NTD_SWEEP_PRIO=off / lo for experiments.
-        # Two streams per group: only while they all get a hardware queue of
-        # their own (32 groups -> 64 streams on 32 queues: 20% slower).
-        prio = os.environ.get("NTD_SWEEP_PRIO", "hi")
+        # batch (8 alternating runs).  Two streams per group: only while they
+        # all get a hardware queue of their own (32 groups -> 64 streams on 32
+        # queues: 20% slower).
+        prio = self.sweep_priority
         if 2 * len(self.groups) > int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8")):
             prio = "off"
         for grp in self.groups:
@@ -294,7 +299,7 @@ class BatchSolver:
             grp.stream.wait_stream(cur)
         self.reserve(K)
         hist, flags_out, state_out = (v[:K] for v in self._pipe_bufs)
-        self._dynamic_ctas = os.environ.get("NTD_DYNAMIC_CTAS", "1") != "0"
+        self._dynamic_ctas = self.dynamic_ctas
         self._map_ctas(self.batch)
 
         def begin(grp, it):
@@ -459,7 +464,7 @@ class BatchSolver:
 
     def _run_groups(self, b, tol, on_start, on_done, done):
         groups = self.groups
-        self._dynamic_ctas = os.environ.get("NTD_DYNAMIC_CTAS", "1") != "0"
+        self._dynamic_ctas = self.dynamic_ctas
         self._map_ctas(self.batch)
         for grp in groups:
             with torch.cuda.stream(grp.stream):

@@ -30,40 +30,27 @@ int check_launch(const char *where)
     return NTD_OK;
 }
 
-static i64 env_int(const char *name, i64 dflt)
-{
-    const char *v = getenv(name);
-    if (!v || !*v) return dflt;
-    i64 x = atoll(v);
-    return x > 0 ? x : dflt;
-}
-i64 rows_block_cap()
-{
-    static const i64 cap = env_int("NTD_ROWS_BLOCKS", 148 * 8);
-    return cap;
-}
-int stn_grid(int full)
-{
-    static const i64 g = env_int("NTD_STN_GRID", 1 << 30);
-    return (int)(g < full ? g : full);
-}
+i64 rows_block_cap() { return 148 * 8; }
 }  // namespace ntd
 
-static constexpr int RED_BLOCKS = 148;   // partials per system (one per SM)
 static constexpr int RED_THREADS = 256;
-// the stencil reductions (A p . p, ||b - A x||^2) keep one partial per warp
+// Reductions (dot products, A p . p, ||b - A x||^2) keep one partial per warp
 // (warp-shuffle tree, no block barriers that would idle the SM at the end of
-// each block): RED_BLOCKS * 8 partials per system, summed in fixed order
-#ifndef NTD_STN_BLOCKS
-#define NTD_STN_BLOCKS 148
-#endif
-static constexpr int STN_BLOCKS = NTD_STN_BLOCKS;  // blocks per system of the stencil reductions
-static constexpr int STN_PARTS = STN_BLOCKS * (RED_THREADS / 32);
-#ifndef NTD_STN_UNROLL
-#define NTD_STN_UNROLL 2  // measured: 1 -> 68%, 2 -> 76%, 4 -> 56% of HBM for spmv+dot (64 systems)
-#endif
-static constexpr int STN_UNROLL = NTD_STN_UNROLL;
-static constexpr int MAX_PARTS = STN_PARTS > RED_BLOCKS ? STN_PARTS : RED_BLOCKS;
+// each block) over VB(n) virtual blocks per system, summed in fixed order by
+// one block per system.  VB depends on n only -- not on the batch, the stream
+// or the grid -- so the reduction tree, and every PCG iterate, is the same
+// for a system solved alone or in any batch.  VB grows with n (about 8 rows
+// per thread) up to 8 blocks per SM, so one large system keeps every SM's
+// memory pipeline busy (a fixed 148 blocks per system held a single 350^3
+// system at 13% of HBM).
+static constexpr int MAX_VB = 148 * 8;
+static constexpr int MAX_PARTS = MAX_VB * (RED_THREADS / 32);
+static constexpr int STN_UNROLL = 2;  // measured: 1 -> 68%, 2 -> 76%, 4 -> 56% of HBM for spmv+dot (64 systems)
+__host__ __device__ __forceinline__ int red_vblocks(i64 n)
+{
+    const i64 v = (n + 8 * RED_THREADS - 1) / (8 * RED_THREADS);
+    return (int)(v < 1 ? 1 : (v > MAX_VB ? MAX_VB : v));
+}
 
 __device__ __forceinline__ double warp_sum(double v)
 {
@@ -223,37 +210,42 @@ extern "C" int ntd_sym_pack(const double *a, double *a4, int32_t *sym_ok, int64_
 }
 
 // ----------------------------------------------------------------- dot
-// Stage 1: partial[s][blk] = sum over rows blk*T+tid, step RED_BLOCKS*T.
+// Stage 1: one partial per warp of every virtual block; thread t of virtual
+// block vb sums rows vb*T + t, step VB*T (VB = red_vblocks(n)).
 __global__ void __launch_bounds__(RED_THREADS) k_dot_partial(const double *__restrict__ x,
                                                              const double *__restrict__ y, double *__restrict__ part,
                                                              i64 n, const int32_t *__restrict__ active)
 {
-    __shared__ double sh[RED_THREADS];
     i64 s = blockIdx.y;
     if (active && !active[s]) return;
+    const int VB = red_vblocks(n);
     const double *xs = x + s * n, *ys = y + s * n;
-    double acc = 0.0;
-    for (i64 i = blockIdx.x * (i64)RED_THREADS + threadIdx.x; i < n; i += (i64)RED_BLOCKS * RED_THREADS)
-        acc = add_rn(acc, mul_rn(xs[i], ys[i]));
-    double b = block_sum(acc, sh);
-    if (threadIdx.x == 0) part[s * MAX_PARTS + blockIdx.x] = b;
+    for (int vb = blockIdx.x; vb < VB; vb += gridDim.x) {
+        double acc = 0.0;
+#pragma unroll STN_UNROLL
+        for (i64 i = vb * (i64)RED_THREADS + threadIdx.x; i < n; i += (i64)VB * RED_THREADS)
+            acc = add_rn(acc, mul_rn(xs[i], ys[i]));
+        const double wsum = warp_sum(acc);
+        if ((threadIdx.x & 31) == 0) part[s * MAX_PARTS + vb * (RED_THREADS / 32) + (threadIdx.x >> 5)] = wsum;
+    }
 }
 
-// partials of system s: part[s * MAX_PARTS + 0 .. nparts), fixed-order sum
-__device__ __forceinline__ double sum_partials(const double *part, i64 s, double *sh, int nparts = RED_BLOCKS)
+// partials of system s (n rows): part[s * MAX_PARTS + 0 .. parts), fixed-order sum
+__device__ __forceinline__ double sum_partials(const double *part, i64 s, double *sh, i64 n)
 {
+    const int nparts = red_vblocks(n) * (RED_THREADS / 32);
     double v = 0.0;
     for (int k = threadIdx.x; k < nparts; k += blockDim.x) v = add_rn(v, part[s * MAX_PARTS + k]);
     return block_sum(v, sh);
 }
 
 __global__ void __launch_bounds__(RED_THREADS) k_dot_final(const double *__restrict__ part, double *__restrict__ out,
-                                                           int sqrt_out, const int32_t *__restrict__ active)
+                                                           int sqrt_out, i64 n, const int32_t *__restrict__ active)
 {
     __shared__ double sh[RED_THREADS];
     i64 s = blockIdx.x;
     if (active && !active[s]) return;
-    double v = sum_partials(part, s, sh);
+    double v = sum_partials(part, s, sh, n);
     if (threadIdx.x == 0) out[s] = sqrt_out ? sqrt(v) : v;
 }
 
@@ -262,7 +254,7 @@ extern "C" int64_t ntd_dot_work_doubles(int64_t batch) { return batch * MAX_PART
 static int launch_dot(const double *x, const double *y, double *work, i64 n, i64 batch, const int32_t *active,
                       cudaStream_t st)
 {
-    dim3 grid(RED_BLOCKS, (unsigned)batch);
+    dim3 grid(red_vblocks(n), (unsigned)batch);
     k_dot_partial<<<grid, RED_THREADS, 0, st>>>(x, y, work, n, active);
     return ntd::check_launch("dot_partial");
 }
@@ -274,7 +266,7 @@ extern "C" int ntd_dot(const double *x, const double *y, double *out, int sqrt_o
     cudaStream_t st = (cudaStream_t)stream;
     int rc = launch_dot(x, y, work, n, batch, active, st);
     if (rc) return rc;
-    k_dot_final<<<(unsigned)batch, RED_THREADS, 0, st>>>(work, out, sqrt_out, active);
+    k_dot_final<<<(unsigned)batch, RED_THREADS, 0, st>>>(work, out, sqrt_out, n, active);
     NTD_CHECK_LAUNCH("ntd_dot");
 }
 
@@ -294,11 +286,11 @@ __global__ void k_pcg_init_vec(const double *__restrict__ b, double *__restrict_
 
 // bnorm = sqrt(b.b); zero rhs short-circuits (precond_pcg.py:86-90)
 __global__ void k_pcg_init_final(const double *__restrict__ part, double *__restrict__ state,
-                                 int32_t *__restrict__ flags, int32_t *__restrict__ active, double tol)
+                                 int32_t *__restrict__ flags, int32_t *__restrict__ active, double tol, i64 n)
 {
     __shared__ double sh[RED_THREADS];
     i64 s = blockIdx.x;
-    double v = sum_partials(part, s, sh);
+    double v = sum_partials(part, s, sh, n);
     if (threadIdx.x == 0) {
         double bn = sqrt(v);
         for (int k = 0; k < NTD_ST_N; k++) ST(s, k) = 0.0;
@@ -325,7 +317,7 @@ extern "C" int ntd_pcg_init(const double *b, double *x, double *r, double *state
     k_pcg_init_vec<<<grid, 256, 0, st>>>(b, x, r, n);
     int rc = launch_dot(b, b, work, n, batch, nullptr, st);
     if (rc) return rc;
-    k_pcg_init_final<<<(unsigned)batch, RED_THREADS, 0, st>>>(work, state, flags, active, tol);
+    k_pcg_init_final<<<(unsigned)batch, RED_THREADS, 0, st>>>(work, state, flags, active, tol, n);
     NTD_CHECK_LAUNCH("ntd_pcg_init");
 }
 
@@ -339,13 +331,13 @@ __global__ void k_copy(const double *__restrict__ src, double *__restrict__ dst,
         dst[s * n + i] = src[s * n + i];
 }
 
-__global__ void k_set_scalar(const double *__restrict__ part, double *__restrict__ state, int which,
+__global__ void k_set_scalar(const double *__restrict__ part, double *__restrict__ state, int which, i64 n,
                              const int32_t *__restrict__ active)
 {
     __shared__ double sh[RED_THREADS];
     i64 s = blockIdx.x;
     if (active && !active[s]) return;
-    double v = sum_partials(part, s, sh);
+    double v = sum_partials(part, s, sh, n);
     if (threadIdx.x == 0) ST(s, which) = v;
 }
 
@@ -358,7 +350,7 @@ extern "C" int ntd_pcg_start(const double *r, const double *z, double *p, double
     k_copy<<<grid, 256, 0, st>>>(z, p, n, active);
     int rc = launch_dot(r, z, work, n, batch, active, st);
     if (rc) return rc;
-    k_set_scalar<<<(unsigned)batch, RED_THREADS, 0, st>>>(work, state, NTD_ST_RZ, active);
+    k_set_scalar<<<(unsigned)batch, RED_THREADS, 0, st>>>(work, state, NTD_ST_RZ, n, active);
     NTD_CHECK_LAUNCH("ntd_pcg_start");
 }
 
@@ -374,11 +366,12 @@ __global__ void __launch_bounds__(RED_THREADS) k_spmv_dot(const double *__restri
     const double *as = a + s * NB * n, *ps = p + s * n;
     double *aps = ap + s * n;
     // virtual blocks vb = the partials' owners, so the reduction tree (and the
-    // result) is the same for any grid of at most STN_BLOCKS blocks
-    for (int vb = blockIdx.x; vb < STN_BLOCKS; vb += gridDim.x) {
+    // result) depends on n only, not on the launched grid
+    const int VB = red_vblocks(n);
+    for (int vb = blockIdx.x; vb < VB; vb += gridDim.x) {
         double acc = 0.0;
 #pragma unroll STN_UNROLL
-        for (i64 i = vb * (i64)RED_THREADS + threadIdx.x; i < n; i += (i64)STN_BLOCKS * RED_THREADS) {
+        for (i64 i = vb * (i64)RED_THREADS + threadIdx.x; i < n; i += (i64)VB * RED_THREADS) {
             double y = row_of<NB>(as, ps, i, n, nx, nxy);
             aps[i] = y;
             acc = add_rn(acc, mul_rn(ps[i], y));
@@ -391,12 +384,12 @@ __global__ void __launch_bounds__(RED_THREADS) k_spmv_dot(const double *__restri
 
 // pap, breakdown check, alpha (precond_pcg.py:99-102)
 __global__ void k_alpha(const double *__restrict__ part, double *__restrict__ state, int32_t *__restrict__ flags,
-                        int32_t *__restrict__ active)
+                        int32_t *__restrict__ active, i64 n)
 {
     __shared__ double sh[RED_THREADS];
     i64 s = blockIdx.x;
     if (!active[s]) return;
-    double pap = sum_partials(part, s, sh, STN_PARTS);
+    double pap = sum_partials(part, s, sh, n);
     if (threadIdx.x == 0) {
         ST(s, NTD_ST_PAP) = pap;
         if (pap <= 0.0 || !isfinite(pap)) {
@@ -417,11 +410,11 @@ static int spmv_alpha_nb(const double *a, const double *p, double *ap, double *s
     if (!a || !p || !ap || !state || !flags || !active || !work || batch < 1) return NTD_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     i64 n = nx * ny * nz;
-    dim3 grid(ntd::stn_grid(STN_BLOCKS), (unsigned)batch);
+    dim3 grid(red_vblocks(n), (unsigned)batch);
     k_spmv_dot<NB><<<grid, RED_THREADS, 0, st>>>(a, p, ap, work, n, nx, nx * ny, active);
     int rc = ntd::check_launch("spmv_dot");
     if (rc) return rc;
-    k_alpha<<<(unsigned)batch, RED_THREADS, 0, st>>>(work, state, flags, active);
+    k_alpha<<<(unsigned)batch, RED_THREADS, 0, st>>>(work, state, flags, active, n);
     NTD_CHECK_LAUNCH("ntd_pcg_spmv_alpha");
 }
 extern "C" int ntd_pcg_spmv_alpha(const double *a, const double *p, double *ap, double *state, int32_t *flags,
@@ -463,10 +456,11 @@ __global__ void __launch_bounds__(RED_THREADS) k_true_res(const double *__restri
     i64 s = blockIdx.y;
     if (!active[s]) return;
     const double *as = a + s * NB * n, *xs = x + s * n, *bs = b + s * n;
-    for (int vb = blockIdx.x; vb < STN_BLOCKS; vb += gridDim.x) {  // virtual blocks, as in k_spmv_dot
+    const int VB = red_vblocks(n);
+    for (int vb = blockIdx.x; vb < VB; vb += gridDim.x) {  // virtual blocks, as in k_spmv_dot
         double acc = 0.0;
 #pragma unroll STN_UNROLL
-        for (i64 i = vb * (i64)RED_THREADS + threadIdx.x; i < n; i += (i64)STN_BLOCKS * RED_THREADS) {
+        for (i64 i = vb * (i64)RED_THREADS + threadIdx.x; i < n; i += (i64)VB * RED_THREADS) {
             double res = add_rn(-row_of<NB>(as, xs, i, n, nx, nxy), bs[i]);
             acc = add_rn(acc, mul_rn(res, res));
         }
@@ -478,12 +472,12 @@ __global__ void __launch_bounds__(RED_THREADS) k_true_res(const double *__restri
 
 // relres, history, convergence (precond_pcg.py:106-114)
 __global__ void k_relres(const double *__restrict__ part, double *__restrict__ state, int32_t *__restrict__ flags,
-                         int32_t *__restrict__ active, double *__restrict__ history, i64 max_iters)
+                         int32_t *__restrict__ active, double *__restrict__ history, i64 max_iters, i64 n)
 {
     __shared__ double sh[RED_THREADS];
     i64 s = blockIdx.x;
     if (!active[s]) return;
-    double v = sum_partials(part, s, sh, STN_PARTS);
+    double v = sum_partials(part, s, sh, n);
     if (threadIdx.x == 0) {
         double rel = sqrt(v) / ST(s, NTD_ST_BNORM);
         int it = FL(s, NTD_FL_ITERS);
@@ -515,11 +509,11 @@ static int update_residual_nb(const double *a, const double *b, double *x, doubl
     k_update_xr<<<grid, 256, 0, st>>>(x, r, p, ap, state, n, active);
     int rc = ntd::check_launch("update_xr");
     if (rc) return rc;
-    dim3 g2(ntd::stn_grid(STN_BLOCKS), (unsigned)batch);
+    dim3 g2(red_vblocks(n), (unsigned)batch);
     k_true_res<NB><<<g2, RED_THREADS, 0, st>>>(a, b, x, work, n, nx, nx * ny, active);
     rc = ntd::check_launch("true_res");
     if (rc) return rc;
-    k_relres<<<(unsigned)batch, RED_THREADS, 0, st>>>(work, state, flags, active, history, max_iters);
+    k_relres<<<(unsigned)batch, RED_THREADS, 0, st>>>(work, state, flags, active, history, max_iters, n);
     NTD_CHECK_LAUNCH("ntd_pcg_update_residual");
 }
 extern "C" int ntd_pcg_update_residual(const double *a, const double *b, double *x, double *r, const double *p,
@@ -540,12 +534,13 @@ extern "C" int ntd_pcg_update_residual_sym(const double *a4, const double *b, do
 }
 
 // beta = rz_new / rz ; rz = rz_new  (precond_pcg.py:116-118)
-__global__ void k_beta(const double *__restrict__ part, double *__restrict__ state, const int32_t *__restrict__ active)
+__global__ void k_beta(const double *__restrict__ part, double *__restrict__ state, const int32_t *__restrict__ active,
+                       i64 n)
 {
     __shared__ double sh[RED_THREADS];
     i64 s = blockIdx.x;
     if (!active[s]) return;
-    double rzn = sum_partials(part, s, sh);
+    double rzn = sum_partials(part, s, sh, n);
     if (threadIdx.x == 0) {
         ST(s, NTD_ST_BETA) = rzn / ST(s, NTD_ST_RZ);
         ST(s, NTD_ST_RZ) = rzn;
@@ -572,7 +567,7 @@ extern "C" int ntd_pcg_direction(const double *r, const double *z, double *p, do
     cudaStream_t st = (cudaStream_t)stream;
     int rc = launch_dot(r, z, work, n, batch, active, st);
     if (rc) return rc;
-    k_beta<<<(unsigned)batch, RED_THREADS, 0, st>>>(work, state, active);
+    k_beta<<<(unsigned)batch, RED_THREADS, 0, st>>>(work, state, active, n);
     rc = ntd::check_launch("beta");
     if (rc) return rc;
     dim3 grid(grid_rows(n), (unsigned)batch);

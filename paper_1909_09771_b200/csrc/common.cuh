@@ -36,11 +36,8 @@ __device__ __forceinline__ void prefetch_l2(const void *p)
 namespace ntd {
 void set_error(const char *where, cudaError_t e);
 int check_launch(const char *where);
-// Per-system block caps of the bandwidth-bound stencil/CG kernels, read once
-// from NTD_ROWS_BLOCKS / NTD_STN_GRID (experiments: a smaller footprint leaves
-// SMs free for the concurrent sweeps).  Results do not depend on them.
+// Per-system block cap of the bandwidth-bound row kernels (8 blocks per SM).
 i64 rows_block_cap();
-int stn_grid(int full);
 }  // namespace ntd
 
 #define NTD_CHECK_LAUNCH(name) return ntd::check_launch(name)

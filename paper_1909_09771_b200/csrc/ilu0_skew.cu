@@ -558,14 +558,15 @@ extern "C" int ntd_ilu0_skew_apply_ex(const double *coef, int64_t split, const d
     const i64 per = g.skew_size();
     double *zf = work, *zb = work + per * batch;
     const int smem = skew::ring_doubles() * 8;
-    static bool attr_set = false;  // per process; the attribute is per function
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(skew::k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    // the attribute is per function and per device: set it on every call (a
+    // host-side driver call, cheap next to the sweep), as the NTD launchers do
+    {
+        cudaError_t e = cudaFuncSetAttribute(skew::k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem > 120 * 1024 ? smem : 120 * 1024);
         if (e != cudaSuccess) {
             ntd::set_error("ilu0 skew apply smem", e);
             return NTD_ELAUNCH;
         }
-        attr_set = true;
     }
     const int nc = (int)ctas_per_half, nw = (int)warps_per_cta;
     if (nc == 1) {

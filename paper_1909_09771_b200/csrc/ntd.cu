@@ -1,8 +1,6 @@
 // ntd.cu -- C-ABI entry points of the NTD setup / apply kernels
 // (ntd_kernels.cuh); per-K instantiations live in ntd_k<K>.cu so they
 // compile in parallel.  K = ceil(nx/32) cells per lane per chain.
-#include <stdlib.h>
-
 #include <algorithm>
 
 #include "ntd_kernels.cuh"
@@ -109,18 +107,17 @@ extern "C" int ntd_apply(const double *pre, const double *solve, const double *b
     return ntd_apply_ex(pre, solve, b, x, work, nx, ny, nz, batch, active, 1, stream);
 }
 
-extern "C" int ntd_apply_ex(const double *pre, const double *solve, const double *b, double *x, double *work,
-                            int64_t nx, int64_t ny, int64_t nz, int64_t batch, const int32_t *active,
-                            int64_t ctas_per_system, void *stream)
+static int apply_impl(const double *pre, const double *solve, const double *b, double *x, double *work, int64_t nx,
+                      int64_t ny, int64_t nz, int64_t batch, const int32_t *active, int64_t ctas_per_system,
+                      bool direct, void *stream)
 {
     if (!pre || !b || !x || !work || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
     if (ctas_per_system != 1 && ctas_per_system != 2) return NTD_EINVAL;
     const int K = pick_k(nx);
-    const char *force = getenv("NTD_APPLY_PATH");
     const int depth = K > 0 ? sl_depth(K) : 0;
     const bool aligned = ((uintptr_t)work % 16 == 0) && (!solve || (uintptr_t)solve % 16 == 0);
     cudaStream_t st = (cudaStream_t)stream;
-    if (depth && aligned && !(force && force[0] == 'd')) {
+    if (depth && aligned && !direct) {
         const i64 lines = ny * nz, s = sl_doubles(nx, ny, nz) * batch;
         double *bsl = work, *xsl = work + s, *xssl = work + 2 * s, *zpl = work + 3 * s;
         const i64 zn = ny * (i64)sl::lr_of(K);
@@ -150,6 +147,19 @@ extern "C" int ntd_apply_ex(const double *pre, const double *solve, const double
         return ntd::check_launch("ntd_apply from_sl");
     }
     NTD_DISPATCH(launch_apply_k, pre, b, x, work, (int)nx, (int)ny, (int)nz, batch, active, st);
+}
+
+extern "C" int ntd_apply_ex(const double *pre, const double *solve, const double *b, double *x, double *work,
+                            int64_t nx, int64_t ny, int64_t nz, int64_t batch, const int32_t *active,
+                            int64_t ctas_per_system, void *stream)
+{
+    return apply_impl(pre, solve, b, x, work, nx, ny, nz, batch, active, ctas_per_system, false, stream);
+}
+
+extern "C" int ntd_apply_direct(const double *pre, const double *b, double *x, double *work, int64_t nx, int64_t ny,
+                                int64_t nz, int64_t batch, const int32_t *active, void *stream)
+{
+    return apply_impl(pre, nullptr, b, x, work, nx, ny, nz, batch, active, 1, true, stream);
 }
 
 // ------------------------------------------------------------------ fused
@@ -313,9 +323,3 @@ extern "C" int ntd_factor(const double *a, double *pre, double *work, int64_t *s
     NTD_DISPATCH(launch_factor_k, a, pre, work, status, (int)nx, (int)ny, (int)nz, batch, (cudaStream_t)stream);
 }
 
-// A/B switch for the split sweep's shared-memory plane buffers (experiments)
-extern "C" int ntd_set_smb(int on)
-{
-    sl::g_ntd_smb = on != 0;
-    return 0;
-}

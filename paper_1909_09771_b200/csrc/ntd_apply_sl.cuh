@@ -991,11 +991,6 @@ template <int K>
 int launch_apply_sl_k(const double *solve, const double *bsl, double *xsl, double *xssl, const double *zpl, int nx,
                       int ny, int nz, i64 batch, const int32_t *active, cudaStream_t st, int ctas_per_system = 1);
 
-namespace sl {
-// host switch for A/B measurements (ntd_set_smb); on by default
-inline bool g_ntd_smb = true;
-}
-
 template <int K>
 int launch_apply_smb(const double *solve, const double *bsl, double *xsl, double *xssl, const double *zpl, int nx,
                      int ny, int nz, i64 batch, const int32_t *active, cudaStream_t st, int bl)
@@ -1043,7 +1038,7 @@ int launch_apply_smb(const double *solve, const double *bsl, double *xsl, double
     {                                                                                                              \
         const int bl_ = (ny - 1) / 2 + 1 > ny - (ny - 1) / 2 ? (ny - 1) / 2 + 1 : ny - (ny - 1) / 2;             \
         if constexpr (sl::depth_smb_of(K) >= 2) {                                                                  \
-            if (ctas_per_system == 2 && bl_ <= 16 * K + 1 && sl::g_ntd_smb)                                        \
+            if (ctas_per_system == 2 && bl_ <= 16 * K + 1)                                                            \
                 return launch_apply_smb<K>(solve, bsl, xsl, xssl, zpl, nx, ny, nz, batch, active, st, bl_);        \
         }                                                                                                          \
         if (ctas_per_system == 2) {                                                                                \

@@ -8,7 +8,6 @@ solver both sit on top of these functions.
 """
 
 import contextlib
-import os
 
 import torch
 
@@ -81,6 +80,19 @@ def ntd_apply(pre_dev, b_dev, nx, ny, nz, batch, x=None, work=None, active=None,
     return x
 
 
+def ntd_apply_direct(pre_dev, b_dev, nx, ny, nz, batch, x=None, work=None, active=None):
+    """x = M_NTD^{-1} b by the direct-load kernel on the reference band layout
+    (the path of grids without slot-layout records, e.g. nx > 352)."""
+    lib = _lib.load()
+    if x is None:
+        x = torch.empty_like(b_dev)
+    if work is None or work.numel() < lib.ntd_apply_work_doubles(nx, ny, nz, batch):
+        work = torch.empty(lib.ntd_apply_work_doubles(nx, ny, nz, batch), dtype=torch.float64, device=_dev())
+    _lib.call("ntd_apply_direct", _lib.ptr(pre_dev), _lib.ptr(b_dev), _lib.ptr(x), _lib.ptr(work), nx, ny, nz, batch,
+              _lib.ptr(active), _lib.stream())
+    return x
+
+
 def check_grid_pattern(a_dev, nx, ny, nz):
     """True when no band couples across a line or plane boundary
     (BandedMatrix invariant, banded_core.py:39-42); required by the ILU0
@@ -121,11 +133,7 @@ def ilu0_ctas(systems_on_gpu):
     """(CTAs per system half, warps per CTA) for the skewed ILU0 sweep: a
     cluster of up to 8 CTAs on separate SMs when the GPU's whole load (all
     systems, every stream group) leaves SMs idle, else one 24-warp CTA per
-    half.  NTD_ILU0_CTAS="c,w" overrides (experiments)."""
-    env = os.environ.get("NTD_ILU0_CTAS")
-    if env:
-        c, w = (int(v) for v in env.split(","))
-        return c, w
+    half."""
     # measured (tools/ilu0_ctas_scan.py, 96^3, ms per apply at 1 / 8 / 16
     # systems): 1x24 1.25/1.27/1.28, 2x24 1.10/1.12/1.15, 4x12 0.95/0.99/1.03;
     # 8x6 0.84 at 1 system.  Whole solves (bench.py): 8x6 instead of 4x12 is
@@ -142,11 +150,7 @@ def ntd_ctas(systems_on_gpu):
     """CTAs per system for the NTD apply sweep: 2 (one level-3 half per SM,
     a cluster of two) while the GPU's systems fit one CTA per SM, else 1.
     Measured on the config-4 batch: 2 is faster at every size up to 64
-    systems per GPU (4327 -> 4747 Munk-iter/s at 64, 1795 -> 1947 at 16).
-    NTD_APPLY_CTAS=1|2 overrides (experiments)."""
-    env = os.environ.get("NTD_APPLY_CTAS")
-    if env:
-        return int(env)
+    systems per GPU (4327 -> 4747 Munk-iter/s at 64, 1795 -> 1947 at 16)."""
     return 2 if 2 * systems_on_gpu <= SMS else 1
 
 
@@ -396,4 +400,63 @@ class PcgDevice:
             if precond_apply is not None:
                 z = precond_apply(self.r, self.z, self.active)
             self.direction(z)
+        return it
+
+    # ------------------------------------------------------------ graphed loop
+    def _iteration(self, precond_apply):
+        """One PCG iteration: update (ap, alpha, x, r, true residual, flags),
+        preconditioner, new direction -- every kernel masked by `active`."""
+        self.step_update()
+        z = self.r if precond_apply is None else precond_apply(self.r, self.z, self.active)
+        self.direction(z)
+
+    def solve_graph(self, b, tol, precond_apply=None, graph_key=None):
+        """PCG to completion with one iteration replayed as a CUDA graph.
+
+        The host neither launches the ~15 kernels of an iteration nor waits
+        for each one: it replays the captured iteration and reads the
+        convergence flags of iteration i-1 while iteration i runs (converged
+        systems are masked on the device, so the one extra replay does no
+        work).  Captured once per (PcgDevice, graph_key); precond_apply must
+        only enqueue device work on the current stream.  Returns the number
+        of host-side iterations (the per-system count is in the flags)."""
+        if getattr(self, "_b_buf", None) is None:
+            self._b_buf = torch.empty((self.batch, self.n), dtype=torch.float64, device=self.r.device)
+            self._flag_slots = [torch.zeros((self.batch, _lib.NTD_FL["N"]), dtype=torch.int32).pin_memory()
+                                for _ in range(2)]
+            self._flag_events = [torch.cuda.Event() for _ in range(2)]
+        self._b_buf.copy_(b.reshape(self.batch, self.n))
+        self.init(self._b_buf, tol)
+        z = self.r if precond_apply is None else precond_apply(self.r, self.z, self.active)
+        self.start(z)
+        if getattr(self, "_graph", None) is None or self._graph_key != graph_key:
+            # one eager iteration first: it allocates every lazily sized
+            # buffer, so the capture below allocates nothing
+            self._iteration(precond_apply)
+            done = 1
+            self._flag_slots[1].copy_(self.flags, non_blocking=True)
+            self._flag_events[1].record()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side):
+                    self._iteration(precond_apply)
+            torch.cuda.current_stream().wait_stream(side)
+            self._graph, self._graph_key = g, graph_key
+        else:
+            done = 0
+        act = _lib.NTD_FL["ACTIVE"]
+        it = done
+        while it < self.max_iters:
+            self._graph.replay()
+            it += 1
+            slot = it & 1
+            self._flag_slots[slot].copy_(self.flags, non_blocking=True)
+            self._flag_events[slot].record()
+            if it >= 2:
+                prev = 1 - slot
+                self._flag_events[prev].synchronize()
+                if not bool(self._flag_slots[prev][:, act].any()):
+                    break
         return it

@@ -10,7 +10,6 @@ and ignored; results match the reference to rounding (<= 1e-10 relative is
 the parity bar, typically ~1e-15).
 """
 
-import numpy as np
 import torch
 
 from . import _lib
@@ -36,26 +35,30 @@ class SolveWorkspace:
 
 
 def chain_bidiagonal_solve(diag_recip, offdiag, b, direction="forward", lanes=CHAIN_LANES):
-    """Public bidiagonal chain helper (ntd_solve.py:272-300).  Reference
-    utility, not on the solve path: evaluated as the plain sequential
-    recurrence (the reference's lanes == 1 form)."""
-    dr = np.ascontiguousarray(diag_recip, dtype=np.float64)
-    off = np.ascontiguousarray(offdiag, dtype=np.float64)
-    rhs = np.ascontiguousarray(b, dtype=np.float64)
-    n = dr.shape[0]
-    if off.shape[0] != n or rhs.shape[0] != n:
+    """Bidiagonal chain x[i] = (b[i] - offdiag[i]*x[i_prev]) * diag_recip[i]
+    (ntd_solve.py:272-300), on the GPU (libntdgpu ``ntd_chain_solve``) with
+    the reference's lane composition: ``lanes`` equal chunks composed as
+    affine maps, carries stitched in order, remainder walked sequentially,
+    the plain recurrence when lanes == 1 or the chain is shorter than
+    2*lanes (_chain_scaled, ntd_solve.py:20-64).  Bitwise the reference's
+    result for every ``lanes``."""
+    dr = as_device(diag_recip).reshape(-1)
+    off = as_device(offdiag).reshape(-1)
+    rhs = as_device(b).reshape(-1)
+    n = dr.numel()
+    if off.numel() != n or rhs.numel() != n:
         raise ValueError("chain solve operands must have equal length")
     if lanes < 1:
         raise ValueError("lanes must be >= 1")
+    x = torch.empty_like(rhs)
+    if n == 0:
+        return like_input(x, b)
     if direction not in ("forward", "backward"):
         raise ValueError(f"unknown direction {direction!r}")
-    x = np.empty(n)
-    order = range(n) if direction == "forward" else range(n - 1, -1, -1)
-    xp = 0.0
-    for p in order:
-        xp = (rhs[p] - off[p] * xp) * dr[p]
-        x[p] = xp
-    return x
+    work = torch.empty(_lib.load().ntd_chain_work_doubles(n, 1), dtype=torch.float64, device=rhs.device)
+    _lib.call("ntd_chain_solve", _lib.ptr(dr), _lib.ptr(off), _lib.ptr(rhs), _lib.ptr(x), _lib.ptr(work), n, 1,
+              0 if direction == "forward" else 1, int(lanes), _lib.stream())
+    return like_input(x, b)
 
 
 def ntd_apply(pre, b, workers=1, lanes=CHAIN_LANES, workspace=None):

@@ -90,7 +90,6 @@ def pcg(a, b, precond=None, tol=1e-7, max_iters=200, workers=1, callback=None):
     t0 = perf_counter()
     ad = a.device_data()
     bd = as_device(b).reshape(1, n)
-    solver = D.PcgDevice(ad, a.nx, a.ny, a.nz, 1, max_iters)
 
     if precond is None:
         papply = None
@@ -104,6 +103,25 @@ def pcg(a, b, precond=None, tol=1e-7, max_iters=200, workers=1, callback=None):
             z_dev.copy_(as_device(zv).reshape(z_dev.shape))
             return z_dev
 
+    if callback is None and (precond is None or hasattr(precond, "device_apply")):
+        # device-only iteration: replayed as a CUDA graph, no per-iteration
+        # host round trip (PcgDevice.solve_graph)
+        solver = _graphed_solver(precond, ad, a, max_iters)
+        solver.solve_graph(bd, tol, papply, graph_key=id(precond))
+        fl, st = solver.read_flags()
+        iters = int(fl[0, _lib.NTD_FL["ITERS"]])
+        status = int(fl[0, _lib.NTD_FL["STATUS"]])
+        history = solver.history[0, :iters].cpu().tolist()
+        if status == _lib.PCG_BREAKDOWN:
+            pap = float(st[0, _lib.NTD_ST["PAP"]])
+            raise DivergenceError(f"breakdown at iteration {iters + 1}: p.A.p = {pap}")
+        if status == _lib.PCG_NONFINITE:
+            raise DivergenceError(f"non-finite residual at iteration {iters}")
+        x = like_input(solver.x.reshape(-1).clone(), b)
+        final = history[-1] if history else 0.0
+        return x, SolveStats(iters, status == _lib.PCG_CONVERGED, history, final, perf_counter() - t0)
+
+    solver = D.PcgDevice(ad, a.nx, a.ny, a.nz, 1, max_iters)
     history = []
     err = []
 
@@ -126,6 +144,23 @@ def pcg(a, b, precond=None, tol=1e-7, max_iters=200, workers=1, callback=None):
     x = like_input(solver.x.reshape(-1), b)
     final = history[-1] if history else 0.0
     return x, SolveStats(it, converged, history, final, perf_counter() - t0)
+
+
+def _graphed_solver(precond, ad, a, max_iters):
+    """The PcgDevice (with its captured iteration) for this operator and
+    preconditioner, cached on the preconditioner object so repeated solves
+    reuse the graph."""
+    key = (ad.data_ptr(), a.nx, a.ny, a.nz, max_iters)
+    cache = getattr(precond, "_pcg_devices", None) if precond is not None else None
+    if cache is not None and key in cache:
+        return cache[key]
+    solver = D.PcgDevice(ad, a.nx, a.ny, a.nz, 1, max_iters)
+    if precond is not None:
+        try:
+            precond._pcg_devices = {key: solver}  # one operator at a time
+        except AttributeError:
+            pass
+    return solver
 
 
 __all__ = ["CombinedPrecond", "DivergenceError", "SolveStats", "combined_apply", "pcg"]

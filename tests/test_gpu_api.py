@@ -142,19 +142,15 @@ def test_apply_does_not_clobber_input_and_is_deterministic(ntd, rng):
 
 
 def test_direct_and_slot_layout_paths_agree(ntd, rng):
-    """The slot-layout TMA kernel and the direct-load kernel compute the same
-    operator (forced with NTD_APPLY_PATH=direct)."""
+    """The slot-layout TMA kernel and the direct-load kernel (ntd_apply_direct,
+    the path of grids without slot-layout records) compute the same operator."""
     import torch
     from paper_1909_09771_b200 import device as D
     a = ntd.assemble(ntd.GridSpec(24, 20, 18), 2)
     pre = ntd.factor_level3(a)
     b = torch.from_numpy(rng.standard_normal(a.n_rows)).cuda()
     x_sl = D.ntd_apply(pre.bands, b, 24, 20, 18, 1, solve=pre.solve)
-    os.environ["NTD_APPLY_PATH"] = "direct"
-    try:
-        x_d = D.ntd_apply(pre.bands, b, 24, 20, 18, 1)
-    finally:
-        del os.environ["NTD_APPLY_PATH"]
+    x_d = D.ntd_apply_direct(pre.bands, b, 24, 20, 18, 1)
     assert rel(x_sl.cpu().numpy(), x_d.cpu().numpy()) <= 1e-13
 
 

@@ -28,9 +28,11 @@ def test_reference_name_surface():
                  "CHAIN_LANES", "SolveWorkspace", "chain_bidiagonal_solve", "ntd_apply", "LineBands", "PlaneBands",
                  "PreconBands", "compute_beta", "dump_precon_bands", "factor_level1", "factor_level2",
                  "factor_level3", "load_precon_bands", "twist_index", "ILU0Factors", "build_block_ilu0",
-                 "ilu0_apply", "CombinedPrecond", "DivergenceError", "SolveStats", "combined_apply", "pcg"]
+                 "ilu0_apply", "CombinedPrecond", "DivergenceError", "SolveStats", "combined_apply", "pcg",
+                 "BenchConfig", "BenchReport", "run_benchmark", "speedup_probe"]
     for n in ref_names:
         assert hasattr(ntd, n), n
+        assert n in ntd.__all__, n
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-device behaviour")
