@@ -323,11 +323,13 @@ def run_ntd(args):
     R = 5
     has_ilu = args.precond == "ntd+ilu0"
     for _ in range(2 if has_ilu else 0):
-        D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, Bg, z=xa, skew=P.skew, work=P.skew_work, ctas=P.ilu_ctas)
+        D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, Bg, z=xa, skew=P.skew, work=P.skew_work, ctas=P.ilu_ctas,
+                     hp=P.ilu_hp)
     e4 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     e4[0].record()
     for _ in range(R if has_ilu else 0):
-        D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, Bg, z=xa, skew=P.skew, work=P.skew_work, ctas=P.ilu_ctas)
+        D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, Bg, z=xa, skew=P.skew, work=P.skew_work, ctas=P.ilu_ctas,
+                     hp=P.ilu_hp)
     e4[1].record()
     e5 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     e5[0].record()
@@ -526,7 +528,7 @@ def single_configs(peak, cfgs=(1, 2, 3, 5), cpu=True):
                                           work=cp.workspace.work(nx, ny, nz), solve=pre.solve), R)
         t_comb = timed(lambda: dv.apply(v, z), R)
         t_ilu = timed(lambda: D.ilu0_apply(dv.ilu, dv.split, v, nx, ny, nz, 1, z=z, skew=dv.skew,
-                                           work=dv.skew_work, ctas=dv.ilu_ctas), R)
+                                           work=dv.skew_work, ctas=dv.ilu_ctas, hp=dv.ilu_hp), R)
         # parity against the oracle on the same vector (the GPU factor is
         # bitwise the reference's: tests/test_gpu_api.py)
         vh = v[0].cpu().numpy()

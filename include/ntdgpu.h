@@ -274,6 +274,23 @@ int ntd_ilu0_skew_apply_ex(const double *coef, int64_t split, const double *r,
                            const int32_t *active, int64_t ctas_per_half,
                            int64_t warps_per_cta, void *stream);
 
+/* Hyperplane-synchronous ILU0 solves (same records and arithmetic as the
+ * skewed kernels, bitwise equal): every 32-line unit of a half advances one
+ * skewed step per barrier, neighbour rows passed through shared memory, so
+ * the critical path is the wavefront length instead of progress-word chains.
+ * A half runs on ctas_per_half CTAs (1..16; > 1: a thread-block cluster
+ * splitting its planes, boundary rows through distributed shared memory) of
+ * warps_per_cta warps.  ntd_ilu0_hp_units returns the units of the larger
+ * half (0: split is not a plane boundary); a CTA's share must be <= 380
+ * units and <= 8 units per warp (1 unit per warp: <= 24 warps; 2-8:
+ * <= 16 warps).  Two launches (forward, backward). */
+int64_t ntd_ilu0_hp_units(int64_t nx, int64_t ny, int64_t nz, int64_t split);
+int ntd_ilu0_hp_apply(const double *coef, int64_t split, const double *r,
+                      double *z, double *acc, double *work, int64_t nx,
+                      int64_t ny, int64_t nz, int64_t batch,
+                      const int32_t *active, int64_t ctas_per_half,
+                      int64_t warps_per_cta, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

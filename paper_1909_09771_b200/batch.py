@@ -199,7 +199,8 @@ class BatchSolver:
             else:
                 grp.precond = D.CombinedDevice(grp.a, self.nx, self.ny, self.nz, hi - lo, pre=pre[lo:hi],
                                                ilu=f[lo:hi], split=split, a4=grp.pcg.a4,
-                                               ilu_ctas=D.ilu0_ctas(self.batch), ntd_ctas_=D.ntd_ctas(self.batch))
+                                               ilu_ctas=D.ilu0_ctas(self.batch), ntd_ctas_=D.ntd_ctas(self.batch),
+                                               ilu_hp=D.ilu0_hp_config(self.nx, self.ny, self.nz, split, self.batch))
             if prio in ("hi", "lo") and len(self.groups) > 1:
                 lo_p, hi_p = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") \
                     else (0, -1)
@@ -442,9 +443,11 @@ class BatchSolver:
         if not self._dynamic_ctas:
             return
         ctas = D.ilu0_ctas(max(1, systems))
+        hp = D.ilu0_hp_config(self.nx, self.ny, self.nz, self.n // 2, max(1, systems))
         for grp in self.groups:
             if isinstance(grp.precond, D.CombinedDevice):
                 grp.precond.ilu_ctas = ctas
+                grp.precond.ilu_hp = hp
 
     def _run(self, b, tol, on_start=None, on_done=None):
         """PCG (precond_pcg.py:84-119) on every group, enqueued round-robin.

@@ -146,6 +146,43 @@ def ilu0_ctas(systems_on_gpu):
     return (2, ILU0_WARPS) if c >= 2 else (1, ILU0_WARPS)
 
 
+def _hp_warps(umax):
+    """(warps per CTA, units per warp) for a CTA share of umax units, within
+    the kernels' register budgets (1 unit per warp: <= 24 warps; 2-8: <= 16)."""
+    if umax <= 24:
+        return max(1, umax), 1
+    if umax <= 128:
+        return 16, -(-umax // 16)
+    return None
+
+
+def ilu0_hp_config(nx, ny, nz, split, systems_on_gpu):
+    """(CTAs per half, warps per CTA) of the hyperplane ILU0 kernel
+    (ntd_ilu0_hp_apply) for this grid, or None when the batch leaves it no
+    room (then the skewed progress-word kernel, which needs one SM per half,
+    is used: at 64 systems per GPU it is 1.8x faster).  One CTA per half when
+    it holds the half at one unit per warp (the CTA barrier is cheaper than
+    the cluster barrier: 32^3 0.079 ms vs 0.13-0.15 ms on 2-16 CTAs), else
+    the largest cluster the batch leaves room for (148 / (2 systems) SMs per
+    half, at most 16): the step time grows with the units per CTA (64^3:
+    0.27 ms on 16 CTAs, 0.41 ms on one; 128^3 0.83 ms on 16)."""
+    units = _lib.load().ntd_ilu0_hp_units(nx, ny, nz, split)
+    if units <= 0:
+        return None
+    g = (ny + 31) // 32
+    nk = units // g
+    budget = max(1, SMS // (2 * max(1, systems_on_gpu)))
+    if units <= 24:
+        return 1, max(1, units)
+    nc = min(16, budget, nk)
+    while nc >= 2:
+        wu = _hp_warps(-(-nk // nc) * g)
+        if wu is not None:
+            return nc, wu[0]
+        nc -= 1
+    return None
+
+
 def ntd_ctas(systems_on_gpu):
     """CTAs per system for the NTD apply sweep: 2 (one level-3 half per SM,
     a cluster of two) while the GPU's systems fit one CTA per SM, else 1.
@@ -155,17 +192,25 @@ def ntd_ctas(systems_on_gpu):
 
 
 def ilu0_apply(f_dev, split, r_dev, nx, ny, nz, batch, z=None, acc=None, active=None, skew=None, work=None,
-               ctas=None):
+               ctas=None, hp="auto"):
     """z = (LU)^-1 r (and/or acc += z).  skew: coefficient records from
-    ilu0_skew_build (fast path); work: scratch for it; ctas: (CTAs per
-    system half, warps per CTA) (default: sized for this batch alone,
-    ilu0_ctas)."""
+    ilu0_skew_build (fast paths); work: scratch for them; hp: (CTAs per half,
+    warps per CTA) of the hyperplane kernel, None for the skewed kernel, or
+    "auto" (ilu0_hp_config for this batch alone); ctas: (CTAs per system
+    half, warps per CTA) of the skewed kernel (default ilu0_ctas).  Every
+    path gives bitwise the same result."""
     if z is None and acc is None:
         z = torch.empty_like(r_dev)
     if skew is not None:
         need = _lib.load().ntd_ilu0_skew_work_doubles(nx, ny, nz, batch)
         if work is None or work.numel() < need:
             work = torch.empty(need, dtype=torch.float64, device=_dev())
+        if isinstance(hp, str):
+            hp = ilu0_hp_config(nx, ny, nz, split, batch)
+        if hp is not None:
+            _lib.call("ntd_ilu0_hp_apply", _lib.ptr(skew), split, _lib.ptr(r_dev), _lib.ptr(z), _lib.ptr(acc),
+                      _lib.ptr(work), nx, ny, nz, batch, _lib.ptr(active), hp[0], hp[1], _lib.stream())
+            return z
         nc, nw = ilu0_ctas(batch) if ctas is None else ctas
         _lib.call("ntd_ilu0_skew_apply_ex", _lib.ptr(skew), split, _lib.ptr(r_dev), _lib.ptr(z), _lib.ptr(acc),
                   _lib.ptr(work), nx, ny, nz, batch, _lib.ptr(active), nc, nw, _lib.stream())
@@ -204,9 +249,11 @@ class CombinedDevice:
     (precond_pcg.py:28-65), all buffers preallocated on the device."""
 
     def __init__(self, a_dev, nx, ny, nz, batch, pre=None, ilu=None, split=None, solve=None, skew=None,
-                 a4="auto", ilu_ctas=None, ntd_ctas_=None):
+                 a4="auto", ilu_ctas=None, ntd_ctas_=None, ilu_hp="auto"):
         self.a, self.nx, self.ny, self.nz, self.batch = a_dev, nx, ny, nz, batch
         self.ilu_ctas = ilu0_ctas(batch) if ilu_ctas is None else ilu_ctas
+        self.split = (nx * ny * nz) // 2 if split is None else split
+        self.ilu_hp = ilu0_hp_config(nx, ny, nz, self.split, batch) if isinstance(ilu_hp, str) else ilu_hp
         self.ntd_ctas = ntd_ctas(batch) if ntd_ctas_ is None else ntd_ctas_
         self.a4 = sym_pack(a_dev, nx, ny, nz, batch) if isinstance(a4, str) else a4
         n = nx * ny * nz
@@ -214,7 +261,6 @@ class CombinedDevice:
         self.pre = pre
         self.solve = solve if solve is not None else solve_bands(pre, nx, ny, nz, batch)
         self.ilu = ilu
-        self.split = n // 2 if split is None else split
         self.skew = skew if skew is not None else ilu0_skew_build(ilu, self.split, nx, ny, nz, batch)
         self.skew_work = None
         shape = (batch, n)
@@ -252,7 +298,7 @@ class CombinedDevice:
                                          device=_dev())
         with self._sweep():
             ilu0_apply(self.ilu, self.split, r, *g, z=self.w, active=active, skew=self.skew, work=self.skew_work,
-                       ctas=self.ilu_ctas)
+                       ctas=self.ilu_ctas, hp=self.ilu_hp)
         op, nb = (self.a, 7) if self.a4 is None else (self.a4, 4)
         if self.fused:
             _lib.call("ntd_residual_to_slot", _lib.ptr(op), nb, _lib.ptr(self.pre), _lib.ptr(r), _lib.ptr(self.w),
@@ -279,7 +325,7 @@ class CombinedDevice:
         with self._sweep():
             if self.skew is not None:
                 ilu0_apply(self.ilu, self.split, self.t, *g, z=None, acc=z, active=active, skew=self.skew,
-                           work=self.skew_work, ctas=self.ilu_ctas)
+                           work=self.skew_work, ctas=self.ilu_ctas, hp=self.ilu_hp)
             else:
                 ilu0_apply(self.ilu, self.split, self.t, *g, z=self.xn, acc=z, active=active)
         return z

@@ -239,8 +239,28 @@ def test_sm_mappings_bitwise(ntd):
             # the sweep never reads the empty (padding) slots of its skewed
             # work arrays: NaN there must not reach the result
             work = torch.full((need,), float("nan"), dtype=torch.float64, device=v.device)
-            D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, 2, z=z, skew=P.skew, work=work, ctas=ctas)
+            D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, 2, z=z, skew=P.skew, work=work, ctas=ctas, hp=None)
             outs.append(z)
+        # the hyperplane kernel: one CTA or a cluster of CTAs per half, 1..8
+        # units per warp, z and / or acc outputs
+        g = (ny + 31) // 32
+        nk = max(P.split // (nx * ny), nz - P.split // (nx * ny))
+        for nc in (1, 2, 4, 8, 16):
+            if nc > nk:
+                continue
+            umax = -(-nk // nc) * g
+            for w in sorted({max(1, -(-umax // 8)), min(16, umax), min(24, umax)}):
+                if -(-umax // w) > 8 or (w > 16 and -(-umax // w) > 1) or umax > 380:
+                    continue
+                z = torch.empty_like(v)
+                acc = torch.full_like(v, 0.5)
+                work = torch.full((need,), float("nan"), dtype=torch.float64, device=v.device)
+                D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, 2, z=z, acc=acc, skew=P.skew, work=work, hp=(nc, w))
+                assert torch.equal(z, z_ref), (nx, ny, nz, nc, w)
+                assert torch.equal(acc, z_ref + 0.5), (nx, ny, nz, nc, w)
+                z2 = torch.empty_like(v)
+                D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, 2, z=z2, skew=P.skew, work=work, hp=(nc, w))
+                assert torch.equal(z2, z_ref), (nx, ny, nz, nc, w)
         assert all(torch.equal(z_ref, o) for o in outs), (nx, ny, nz)
         if P.fused:
             xs = []
