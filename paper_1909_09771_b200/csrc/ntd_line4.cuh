@@ -75,24 +75,36 @@ __device__ __forceinline__ LinePrep line_prep(int s, const double (&aL)[K], cons
 
 // Solve one line.  cr[k] = rhs[k]*mr[k] (the chain constants of the lower
 // phase); twist row xt = bt*mrt + nlt*xa + nut*xd.
+//
+// The per-lane chain pieces are composed as prefix maps: slot k's value is
+// PA_k * carry + PC_k with PC_k the composed constant after slot k (the
+// compose's own intermediates) and PA_k the prefix product of the slot
+// coefficients (factor-only, off the critical path), so once the scan has
+// delivered the lane's carry every slot takes one FMA instead of a K-long
+// re-walk; the compose starts from the first constant (fma(a, 0, c) == c).
+// Same operator as the sequential form, rounded differently (<= 1e-15
+// relative, far inside the 1e-10 apply bar).
 template <int K>
 __device__ __forceinline__ void line_solve4(const LinePrep &P, int n, int t, const double (&aL)[K],
                                             const double (&cr)[K], const double (&aU)[K], double btm, double nlt,
                                             double nut, double (&x)[K], double &xt)
 {
     // ---- lower chain
-    double C0 = 0.0;
+    double pc[K], pa[K];
+    pc[0] = cr[0];
+    pa[0] = aL[0];
 #pragma unroll
-    for (int k = 0; k < K; k++) C0 = fma(aL[k], C0, cr[k]);
+    for (int k = 1; k < K; k++) {
+        pc[k] = fma(aL[k], pc[k - 1], cr[k]);
+        pa[k] = aL[k] * pa[k - 1];
+    }
+    const double C0 = pc[K - 1];
     const double t1 = shup(C0, 1), t2 = shup(C0, 2), t3 = shup(C0, 3);
     const double C1 = fma(P.p1, t1, C0) + fma(P.p2, t2, P.p3 * t3);
     const double u1 = shup(C1, 1), u5 = shup(C1, 5), u9 = shup(C1, 9), u13 = shup(C1, 13);
-    double xc = fma(P.e0, u1, P.e1 * u5) + fma(P.e2, u9, P.e3 * u13);
+    const double xl = fma(P.e0, u1, P.e1 * u5) + fma(P.e2, u9, P.e3 * u13);
 #pragma unroll
-    for (int k = 0; k < K; k++) {
-        xc = fma(aL[k], xc, cr[k]);
-        x[k] = xc;
-    }
+    for (int k = 0; k < K; k++) x[k] = fma(pa[k], xl, pc[k]);
     // ---- twist row
     const double xa = __shfl_sync(FULL_MASK, x[K - 1], 15);
     const double xd = __shfl_sync(FULL_MASK, x[K - 1], 31);
@@ -101,17 +113,20 @@ __device__ __forceinline__ void line_solve4(const LinePrep &P, int n, int t, con
     if (t < n - 1) acc = fma(nut, xd, acc);
     xt = acc;
     // ---- upper chain (independent of xt until the carry)
-    double D0 = 0.0;
+    double qc[K], qa[K];
+    qc[K - 1] = x[K - 1];
+    qa[K - 1] = aU[K - 1];
 #pragma unroll
-    for (int k = K - 1; k >= 0; k--) D0 = fma(aU[k], D0, x[k]);
+    for (int k = K - 2; k >= 0; k--) {
+        qc[k] = fma(aU[k], qc[k + 1], x[k]);
+        qa[k] = aU[k] * qa[k + 1];
+    }
+    const double D0 = qc[0];
     const double v1 = shdn(D0, 1), v2 = shdn(D0, 2), v3 = shdn(D0, 3);
     const double D1 = fma(P.q1, v1, D0) + fma(P.q2, v2, P.q3 * v3);
     const double w1 = shdn(D1, 1), w5 = shdn(D1, 5), w9 = shdn(D1, 9), w13 = shdn(D1, 13);
     const double dex = fma(P.f0, w1, P.f1 * w5) + fma(P.f2, w9, P.f3 * w13);
-    xc = fma(P.bex, xt, dex);
+    const double xu = fma(P.bex, xt, dex);
 #pragma unroll
-    for (int k = K - 1; k >= 0; k--) {
-        xc = fma(aU[k], xc, x[k]);
-        x[k] = xc;
-    }
+    for (int k = 0; k < K; k++) x[k] = fma(qa[k], xu, qc[k]);
 }

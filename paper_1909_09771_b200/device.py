@@ -160,18 +160,20 @@ def ilu0_hp_config(nx, ny, nz, split, systems_on_gpu):
     """(CTAs per half, warps per CTA) of the hyperplane ILU0 kernel
     (ntd_ilu0_hp_apply) for this grid, or None when the batch leaves it no
     room (then the skewed progress-word kernel, which needs one SM per half,
-    is used: at 64 systems per GPU it is 1.8x faster).  One CTA per half when
+    is used: at 64 systems per GPU it is 1.8x faster alone and the whole
+    batched solve runs 3-25% faster with it; at 8 systems the hyperplane
+    kernel on 16-CTA clusters gives +14%).  One CTA per half when
     it holds the half at one unit per warp (the CTA barrier is cheaper than
     the cluster barrier: 32^3 0.079 ms vs 0.13-0.15 ms on 2-16 CTAs), else
-    the largest cluster the batch leaves room for (148 / (2 systems) SMs per
-    half, at most 16): the step time grows with the units per CTA (64^3:
+    the largest cluster the batch leaves room for (148 / systems SMs per
+    half, at most 16; the halves of a batch do not all sweep at once): the step time grows with the units per CTA (64^3:
     0.27 ms on 16 CTAs, 0.41 ms on one; 128^3 0.83 ms on 16)."""
     units = _lib.load().ntd_ilu0_hp_units(nx, ny, nz, split)
-    if units <= 0:
+    if units <= 0 or systems_on_gpu > 16:
         return None
     g = (ny + 31) // 32
     nk = units // g
-    budget = max(1, SMS // (2 * max(1, systems_on_gpu)))
+    budget = max(1, SMS // max(1, systems_on_gpu))
     if units <= 24:
         return 1, max(1, units)
     nc = min(16, budget, nk)
