@@ -278,9 +278,11 @@ int ntd_ilu0_skew_apply_ex(const double *coef, int64_t split, const double *r,
  * skewed kernels, bitwise equal): every 32-line unit of a half advances one
  * skewed step per barrier, neighbour rows passed through shared memory, so
  * the critical path is the wavefront length instead of progress-word chains.
- * A half runs on ctas_per_half CTAs (1..16; > 1: a thread-block cluster
- * splitting its planes, boundary rows through distributed shared memory) of
- * warps_per_cta warps.  ntd_ilu0_hp_units returns the units of the larger
+ * A half runs on ctas_per_half CTAs splitting its planes: 1; 2..16 form a
+ * thread-block cluster (boundary rows through distributed shared memory);
+ * 17..74 are linked through global memory (boundary-row rings and progress
+ * words, a cooperative launch: 2 * batch * ctas_per_half <= 148).  Each CTA
+ * has warps_per_cta warps.  ntd_ilu0_hp_units returns the units of the larger
  * half (0: split is not a plane boundary); a CTA's share must be <= 380
  * units and <= 8 units per warp (1 unit per warp: <= 24 warps; 2-8:
  * <= 16 warps).  Two launches (forward, backward). */

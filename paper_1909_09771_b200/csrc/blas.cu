@@ -42,21 +42,22 @@ static constexpr int RED_THREADS = 256;
 // for a system solved alone or in any batch.  VB grows with n (about 8 rows
 // per thread) up to 8 blocks per SM, so one large system keeps every SM's
 // memory pipeline busy (a fixed 148 blocks per system held a single 350^3
-// system at 13% of HBM).
+// system at 13% of HBM); about 24 rows per thread (144 blocks per 96^3
+// system: 8 rows per thread gave 67% instead of 80% of HBM on the batch).
 static constexpr int MAX_VB = 148 * 8;
 static constexpr int MAX_PARTS = MAX_VB * (RED_THREADS / 32);
 static constexpr int STN_UNROLL = 2;  // measured: 1 -> 68%, 2 -> 76%, 4 -> 56% of HBM for spmv+dot (64 systems)
 __host__ __device__ __forceinline__ int red_vblocks(i64 n)
 {
-    const i64 v = (n + 8 * RED_THREADS - 1) / (8 * RED_THREADS);
+    const i64 v = (n + 24 * RED_THREADS - 1) / (24 * RED_THREADS);
     return (int)(v < 1 ? 1 : (v > MAX_VB ? MAX_VB : v));
 }
 // Launched blocks per system: every virtual block for a lone system (its
 // rows need the whole GPU's memory pipelines), at most 148 per system in a
 // batch (each block then walks several virtual blocks in order; the partials
 // -- hence the result -- do not change).  Measured on the 64-system batch:
-// one block per virtual block (432 per 96^3 system) 67% of HBM for
-// spmv+dot, 148 per system 80%.
+// 148 blocks per system walking 432 virtual blocks of 8 rows each 65% of
+// HBM for spmv+dot, one block per 24-row virtual block 80%.
 static unsigned red_grid(i64 n, i64 batch)
 {
     const i64 v = red_vblocks(n);

@@ -51,17 +51,61 @@ __device__ __forceinline__ void st_remote(double *local_addr, int rank, double v
     asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
 }
 
+// Global-memory link between the CTAs of a half that do not form a cluster
+// (more than 16 CTAs, one lone large system).  The boundary plane's row goes
+// through a ring of RING slots in global memory whose empty state is a
+// sentinel NaN (all bits set; the host fills the rings with it): the value
+// is its own signal, so a consumer lane spins on its 8-byte slot until it is
+// not the sentinel, uses it and resets the slot -- no fences or flags on the
+// critical path.  The only flag is the consumer's progress (published with
+// release every few steps), which the producer checks before it reuses a
+// slot (RING steps of slack).  The next step's halo is loaded speculatively
+// with the operands and re-polled only if it was still empty.  All CTAs of
+// the launch are co-resident (a cooperative launch), so the waits resolve.
+constexpr int RING = 16;
+constexpr int PUBLISH = 4;  // consumer progress published every PUBLISH steps
+struct Link {
+    double *halo_in;          // ring this CTA reads (RING x G x 32), nullptr: no predecessor
+    double *halo_out;         // ring this CTA writes, nullptr: no successor
+    unsigned *flag_self;      // this CTA's progress (read by its predecessor)
+    const unsigned *flag_succ;
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p)
+{
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned *p, unsigned v)
+{
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ double ld_relaxed(const double *p)
+{
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(double *p, double v)
+{
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ bool is_empty_slot(double v) { return __double_as_longlong(v) == -1ll; }
+
 // One sweep of one half.  buf: [2][rows][32] (rows 0..G-1: halo = the
 // previous plane in sweep order, owned by the neighbour CTA; row rows-1:
 // zeros; rows is the same in every CTA of the cluster, so a row has the same
 // offset in every CTA's buffer).
-template <bool FWD, int UPW, int OUT, int PF>
+template <bool FWD, int UPW, int OUT, int PF, bool GL>
 __device__ __forceinline__ void sweep(const Sweep &w, const double *__restrict__ coef, const double *__restrict__ in,
-                                      double *zf, double *zout, double *accio, double *buf, int nc, int crank)
+                                      double *zf, double *zout, double *accio, double *buf, int nc, int crank,
+                                      const Link &lk)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
     constexpr int NCF = FWD ? 3 : 4;
-    constexpr int NO = FWD ? 4 : ((OUT & 2) ? 6 : 5);  // operands per unit and step
+    constexpr int NOP = FWD ? 4 : ((OUT & 2) ? 6 : 5);  // operands per unit and step
+    constexpr int NO = NOP + (GL ? 1 : 0);             // (+ the speculative halo value)
     const int G = w.G, Tu = w.T, U = w.U;
     const int rows = w.rows, zrow = w.rows - 1;
     // sweep-order index of this CTA's first plane; the CTA that receives our
@@ -109,11 +153,28 @@ __device__ __forceinline__ void sweep(const Sweep &w, const double *__restrict__
             d[4] = __ldcg(zf + (uu[j] * Tu + t) * 32 + lane);         // forward result
             if constexpr (has_ao) d[5] = ok ? accio[rb[j] + t] : 0.0;
         }
+        if constexpr (GL) {
+            // the halo this step will read (produced at its global step - 1)
+            if (lk.halo_in && mm[j] < G)
+                d[NOP] = ld_relaxed(lk.halo_in + ((tau + sm[j] - 1) % RING) * G * 32 + mm[j] * 32 + lane);
+        }
     };
+    unsigned seen_succ = 0;  // (thread 0) last observed successor progress
     for (int T = -PF; T < w.S; T++) {
         const int cur = T & 1, prv = cur ^ 1;
         double *bc = buf + (size_t)cur * rows * 32, *bp = buf + (size_t)prv * rows * 32;
         // step tau of unit j with operand set op, then the loads of step tau + PF into op
+        if (GL && T >= 0 && lk.halo_out) {
+            // before slot T % RING is reused: the successor has completed the
+            // last step that read it (T - RING + 1)
+            const int need = T - RING + 2;
+            if (threadIdx.x == 0 && need > 0 && seen_succ < (unsigned)need) {
+                long long spins = 0;  // (a protocol error must not hang the GPU: fail the launch)
+                while ((seen_succ = ld_acquire(lk.flag_succ)) < (unsigned)need)
+                    if (++spins > (1ll << 28)) __trap();
+            }
+            __syncthreads();
+        }
         auto unit_step = [&](int j, int tau, double *op) {
             if (tau >= 0) {
                 const int m = mm[j], h = m % G;
@@ -123,7 +184,26 @@ __device__ __forceinline__ void sweep(const Sweep &w, const double *__restrict__
                 const double zn = FWD ? __shfl_up_sync(FULL_MASK, zprev[j], 1) : __shfl_down_sync(FULL_MASK, zprev[j], 1);
                 const double ze = bp[(h > 0 ? m + G - 1 : zrow) * 32 + (FWD ? 31 : 0)];
                 const double zy = (FWD ? lane == 0 : lane == 31) ? ze : zn;
-                const double zz = bp[m * 32 + lane];  // previous plane (row m = halo or unit m - G)
+                // previous plane: row m (the halo rows 0..G-1, or unit m - G); in the
+                // global-link mode the halo comes from the predecessor's ring
+                double zz;
+                if (GL && m < G) {
+                    zz = 0.0;
+                    if constexpr (GL) {
+                        if (lk.halo_in) {
+                            double *slot = lk.halo_in + ((T - 1) % RING) * G * 32 + h * 32 + lane;
+                            zz = op[NOP];
+                            long long spins = 0;
+                            while (is_empty_slot(zz)) {
+                                zz = ld_relaxed(slot);
+                                if (++spins > (1ll << 28)) __trap();
+                            }
+                            st_relaxed(slot, __longlong_as_double(-1ll));  // empty again
+                        }
+                    }
+                } else {
+                    zz = bp[m * 32 + lane];
+                }
                 double acc = FWD ? op[3] : op[4];
                 acc = sub_rn(acc, mul_rn(op[0], zprev[j]));
                 acc = sub_rn(acc, mul_rn(op[1], zy));
@@ -146,7 +226,12 @@ __device__ __forceinline__ void sweep(const Sweep &w, const double *__restrict__
                 }
                 zprev[j] = zv;
                 bc[(m + G) * 32 + lane] = zv;
-                if (next >= 0 && m >= U - G) st_remote(&bc[(m - (U - G)) * 32 + lane], next, zv);
+                if (GL) {
+                    if (lk.halo_out && m >= U - G)
+                        st_relaxed(lk.halo_out + (T % RING) * G * 32 + (m - (U - G)) * 32 + lane, zv);
+                } else if (next >= 0 && m >= U - G) {
+                    st_remote(&bc[(m - (U - G)) * 32 + lane], next, zv);
+                }
             }
             if (tau + PF < Tu) load(j, tau + PF, op);
         };
@@ -167,8 +252,12 @@ __device__ __forceinline__ void sweep(const Sweep &w, const double *__restrict__
                 else unit_step(j, tau, o[2][j]);
             }
         }
-        if (nc == 1) {
+        if (GL || nc == 1) {
             __syncthreads();
+            // progress for the predecessor's slot reuse (our slot resets are
+            // ordered before it: CTA barrier, then a release by thread 0)
+            if (GL && lk.halo_in && threadIdx.x == 0 && T >= 0 && (T % PUBLISH == PUBLISH - 1 || T == w.S - 1))
+                st_release(lk.flag_self, (unsigned)T + 1);
         } else {
             cluster_arrive();
             cluster_wait();
@@ -184,10 +273,10 @@ struct HpTraits {
     static constexpr int MAXT = UPW <= 1 ? 768 : 512;     // threads per CTA (register budget)
 };
 
-template <bool FWD, int UPW, int OUT>
+template <bool FWD, int UPW, int OUT, bool GL>
 __global__ void __launch_bounds__(HpTraits<UPW>::MAXT, 1)
     k_sweep(const double *__restrict__ coef, const double *__restrict__ r, double *zf, double *z, double *acc,
-            i64 split, int nx, int ny, int nz, const int32_t *__restrict__ active, int nc)
+            i64 split, int nx, int ny, int nz, const int32_t *__restrict__ active, int nc, double *glbuf)
 {
     extern __shared__ __align__(16) double hp_buf[];
     const int hb = blockIdx.x / nc, crank = blockIdx.x % nc;
@@ -211,14 +300,31 @@ __global__ void __launch_bounds__(HpTraits<UPW>::MAXT, 1)
     w.S = 32 * (w.G - 1) + w.nk - 1 + w.T;
     const i64 n = w.nxy * nz, per = (i64)nz * w.G * w.T * 32;
     for (int e = threadIdx.x; e < 2 * w.rows * 32; e += blockDim.x) hp_buf[e] = 0.0;
-    if (nc == 1) {
+    Link lk = {nullptr, nullptr, nullptr, nullptr};
+    if (GL) {
+        // glbuf: [batch][2 halves][nc boundaries][RING][G][32] rings (filled
+        // with the empty sentinel by the host), then the [batch][2][nc]
+        // progress words (zeroed)
+        const size_t ring = (size_t)RING * w.G * 32;
+        const i64 hs = sys * 2 + half;  // this system half
+        double *rings = glbuf + (size_t)hs * nc * ring;
+        unsigned *flags = (unsigned *)(glbuf + (size_t)gridDim.x / nc * nc * ring) + hs * nc;
+        const int pred = FWD ? crank - 1 : crank + 1, succ = FWD ? crank + 1 : crank - 1;
+        // boundary b lies between CTAs b and b + 1
+        if (pred >= 0 && pred < nc) lk.halo_in = rings + (size_t)(FWD ? pred : crank) * ring;
+        if (succ >= 0 && succ < nc) lk.halo_out = rings + (size_t)(FWD ? crank : succ) * ring;
+        lk.flag_self = flags + crank;
+        lk.flag_succ = flags + (succ >= 0 && succ < nc ? succ : crank);
+    }
+    if (GL || nc == 1) {
         __syncthreads();
     } else {
         cluster_arrive();
         cluster_wait();
     }
-    sweep<FWD, UPW, OUT, HpTraits<UPW>::PF>(w, coef + sys * per * (FWD ? 3 : 4), FWD ? r + sys * n : nullptr, zf + sys * per,
-                         (OUT & 1) ? z + sys * n : nullptr, (OUT & 2) ? acc + sys * n : nullptr, hp_buf, nc, crank);
+    sweep<FWD, UPW, OUT, HpTraits<UPW>::PF, GL>(w, coef + sys * per * (FWD ? 3 : 4), FWD ? r + sys * n : nullptr,
+                                               zf + sys * per, (OUT & 1) ? z + sys * n : nullptr,
+                                               (OUT & 2) ? acc + sys * n : nullptr, hp_buf, nc, crank, lk);
 }
 
 }  // namespace hp
@@ -242,7 +348,11 @@ extern "C" int ntd_ilu0_hp_apply(const double *coef, int64_t split, const double
 {
     if (!coef || !r || !work || (!z && !acc) || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
     const int nc = (int)ctas_per_half, W = (int)warps_per_cta;
-    if (nc < 1 || nc > 16 || W < 1 || W > 24) return NTD_EINVAL;
+    if (nc < 1 || nc > 74 || W < 1 || W > 24) return NTD_EINVAL;
+    // more than 16 CTAs per half: global-memory links, every CTA on its own
+    // SM (cooperative launch)
+    const bool gl = nc > 16;
+    if (gl && 2 * batch * nc > 148) return NTD_EINVAL;
     const i64 nxy = nx * ny, G = (ny + 31) / 32, T = nx + 31;
     if (split % nxy != 0) return NTD_ENOTSUP;
     const i64 ks = split / nxy, nk = ks > nz - ks ? ks : nz - ks;
@@ -253,17 +363,27 @@ extern "C" int ntd_ilu0_hp_apply(const double *coef, int64_t split, const double
     const int upw = (int)((umax + W - 1) / W);
     const size_t smem = (size_t)2 * (umax + G + 1) * 32 * 8;
     const i64 per = nz * G * T * 32;
+    // global-link scratch (rings + progress words) in the second half of the
+    // work buffer (the skewed kernel's backward array, unused here)
+    double *glbuf = work + per * batch;
+    const size_t ring_doubles = (size_t)2 * batch * nc * hp::RING * G * 32;
     const int out = (z ? 1 : 0) | (acc ? 2 : 0);
     typedef void (*Kern)(const double *, const double *, double *, double *, double *, i64, int, int, int,
-                         const int32_t *, int);
+                         const int32_t *, int, double *);
     Kern kf = nullptr, kb = nullptr;
     int maxt = 0;
-#define HP_CASE(U_)                                                                             \
-    case U_:                                                                                    \
-        kf = hp::k_sweep<true, U_, 0>;                                                          \
-        kb = out == 1 ? hp::k_sweep<false, U_, 1> : (out == 2 ? hp::k_sweep<false, U_, 2>     \
-                                                              : hp::k_sweep<false, U_, 3>);    \
-        maxt = hp::HpTraits<U_>::MAXT;                                                          \
+#define HP_CASE2(U_, GL_)                                                                                  \
+    kf = hp::k_sweep<true, U_, 0, GL_>;                                                                    \
+    kb = out == 1 ? hp::k_sweep<false, U_, 1, GL_>                                                         \
+                  : (out == 2 ? hp::k_sweep<false, U_, 2, GL_> : hp::k_sweep<false, U_, 3, GL_>);          \
+    maxt = hp::HpTraits<U_>::MAXT;
+#define HP_CASE(U_)                  \
+    case U_:                         \
+        if (gl) {                    \
+            HP_CASE2(U_, true)       \
+        } else {                     \
+            HP_CASE2(U_, false)      \
+        }                            \
         break;
     switch (upw) {
         HP_CASE(1)
@@ -277,12 +397,17 @@ extern "C" int ntd_ilu0_hp_apply(const double *coef, int64_t split, const double
     default: return NTD_ENOTSUP;
     }
 #undef HP_CASE
+#undef HP_CASE2
     if (W * 32 > maxt) return NTD_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     for (int pass = 0; pass < 2; pass++) {
         Kern k = pass == 0 ? kf : kb;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess && nc > 8) e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e == cudaSuccess && !gl && nc > 8)
+            e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e == cudaSuccess && gl) e = cudaMemsetAsync(glbuf, 0xff, sizeof(double) * ring_doubles, st);
+        if (e == cudaSuccess && gl)
+            e = cudaMemsetAsync(glbuf + ring_doubles, 0, sizeof(unsigned) * 2 * batch * nc, st);
         if (e != cudaSuccess) {
             ntd::set_error("ilu0 hp apply attributes", e);
             return NTD_ELAUNCH;
@@ -293,14 +418,20 @@ extern "C" int ntd_ilu0_hp_apply(const double *coef, int64_t split, const double
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = nc;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
+        if (gl) {
+            attr[0].id = cudaLaunchAttributeCooperative;
+            attr[0].val.cooperative = 1;
+        } else {
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = nc;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+        }
         cfg.attrs = attr;
-        cfg.numAttrs = nc > 1 ? 1 : 0;
+        cfg.numAttrs = (gl || nc > 1) ? 1 : 0;
         const double *cf = pass == 0 ? coef : coef + per * batch * 3;
-        e = cudaLaunchKernelEx(&cfg, k, cf, r, work, z, acc, (i64)split, (int)nx, (int)ny, (int)nz, active, nc);
+        e = cudaLaunchKernelEx(&cfg, k, cf, r, work, z, acc, (i64)split, (int)nx, (int)ny, (int)nz, active, nc,
+                               glbuf);
         if (e != cudaSuccess) {
             ntd::set_error("ilu0 hp apply", e);
             return NTD_ELAUNCH;

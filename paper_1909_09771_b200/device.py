@@ -168,7 +168,7 @@ def ilu0_hp_config(nx, ny, nz, split, systems_on_gpu):
     the largest cluster the batch leaves room for (148 / systems SMs per
     half, at most 16; the halves of a batch do not all sweep at once): the step time grows with the units per CTA (64^3:
     0.27 ms on 16 CTAs, 0.41 ms on one; 128^3 0.83 ms on 16)."""
-    units = _lib.load().ntd_ilu0_hp_units(nx, ny, nz, split)
+    units = _lib.load(require_device=False).ntd_ilu0_hp_units(nx, ny, nz, split)
     if units <= 0 or systems_on_gpu > 16:
         return None
     g = (ny + 31) // 32
@@ -177,6 +177,16 @@ def ilu0_hp_config(nx, ny, nz, split, systems_on_gpu):
     if units <= 24:
         return 1, max(1, units)
     nc = min(16, budget, nk)
+    if systems_on_gpu == 1 and nk > 32:
+        # a lone large system: up to 74 CTAs per half (one per SM) linked
+        # through global memory (cooperative launch) beat a 16-CTA cluster
+        # (measured per apply: 96^3 0.50 vs 0.53 ms, 128^3 0.76 vs 0.85 ms,
+        # 350^3 2.95 ms on 74 CTAs vs 15.7 ms on 16 at 8 units per warp);
+        # 48 CTAs when that keeps one unit per warp
+        for ncg in (min(48, nk), min(74, nk)):
+            wu = _hp_warps(-(-nk // ncg) * g)
+            if wu is not None and (wu[1] == 1 or ncg == min(74, nk)):
+                return ncg, wu[0]
     while nc >= 2:
         wu = _hp_warps(-(-nk // nc) * g)
         if wu is not None:

@@ -245,8 +245,8 @@ def test_sm_mappings_bitwise(ntd):
         # units per warp, z and / or acc outputs
         g = (ny + 31) // 32
         nk = max(P.split // (nx * ny), nz - P.split // (nx * ny))
-        for nc in (1, 2, 4, 8, 16):
-            if nc > nk:
+        for nc in (1, 2, 4, 8, 16, 24, 32):  # > 16: CTAs linked through global memory
+            if nc > nk or 2 * 2 * nc > 148:
                 continue
             umax = -(-nk // nc) * g
             for w in sorted({max(1, -(-umax // 8)), min(16, umax), min(24, umax)}):

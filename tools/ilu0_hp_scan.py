@@ -61,8 +61,8 @@ for ctas in ((1, 24), (2, 24), (4, 12), (8, 6)):
     print(f"  skew {ctas}: {t:.3f} ms  bitwise={torch.equal(z, z_ref)}", flush=True)
 g = (ny + 31) // 32
 nk = nz - split // (nx * ny)
-for nc in (1, 2, 4, 8, 16):
-    if nc > nk:
+for nc in (1, 2, 4, 8, 16, 24, 37, 48, 74):
+    if nc > nk or (nc > 16 and S > 1):
         continue
     umax = -(-nk // nc) * g
     for w in (4, 8, 12, 16, 24):
