@@ -45,6 +45,26 @@ CFG4_REF_ITERS = [21, 21, 24, 21, 22, 22, 20, 20, 20, 24, 22, 23, 20, 21, 19, 21
                   22, 22, 22, 23, 21, 23, 21, 20, 21, 25, 21, 24, 21, 22, 21, 21, 19, 20, 23, 20, 25, 21, 25, 21,
                   20, 22, 23, 21, 20, 21, 21, 21, 20, 21, 21, 21, 23, 20, 23, 22]
 
+# Dependent-instruction latencies measured on this pool's B200s (tools/micro_lat.cu,
+# profiles/r02e_micro_lat.txt): a dependent DFMA/DMUL/DADD ~25 cycles, a 64-bit
+# warp shuffle ~23.  The NTD line solve (ntd_line4.cuh) has 2K + 14 dependent
+# fp64 operations and 4 dependent shuffle rounds per line step, and one apply
+# is (nz + 1)(ny + 1) dependent line steps: its latency roofline.
+FP64_DEP_CYCLES = 25.1
+SHFL64_CYCLES = 23.0
+
+
+def ntd_latency_roofline(nx, ny, nz, apply_s, sm_mhz):
+    K = next(k for k in (1, 2, 3, 4, 5, 6, 8, 11, 12, 16) if 32 * k >= nx)
+    chain = (2 * K + 14) * FP64_DEP_CYCLES + 4 * SHFL64_CYCLES
+    steps = (nz + 1) * (ny + 1)
+    measured = apply_s * sm_mhz * 1e6 / steps
+    return {"bound": "latency (dependent fp64 chain of the line solves)", "line_steps_per_apply": steps,
+            "chain_cycles_per_step": round(chain, 1), "measured_cycles_per_step": round(measured, 1),
+            "sm_mhz": sm_mhz, "frac": round(chain / measured, 3),
+            "source": "tools/micro_lat.cu latencies, profiles/r02e_micro_lat.txt"}
+
+
 METRIC = "pcg_munknowns_per_s"
 UNIT = "Munknown-iterations/s"
 NTD_APPLY_BYTES_PER_UNKNOWN = 48  # canonical algorithmic bytes
@@ -339,7 +359,7 @@ def run_ntd(args):
     torch.cuda.synchronize()
     t_ilu = e4[0].elapsed_time(e4[1]) / 1e3 / R
     t_spmv = e5[0].elapsed_time(e5[1]) / 1e3 / R
-    stencil = stencil_roofline(solver, B, n, nx, ny, nz)
+    stencil = stencil_roofline(solver.a, B, n, nx, ny, nz)
 
     # ---- reductions over ranks (NCCL: max of timings, sum of work, one all_gather of stats)
     from paper_1909_09771_b200 import dist as pdist
@@ -382,6 +402,7 @@ def run_ntd(args):
                          "concurrent_launches": len(solver.groups),
                          "aggregate_gbs": NTD_APPLY_BYTES_PER_UNKNOWN * work[0] / t_dev / 1e9,
                          "launches_timed": len(evs)},
+            "latency_roofline": ntd_latency_roofline(nx, ny, nz, t_apply, clk.summary()["sm_mhz"] or 1965.0),
             "kernels_ms": {"ntd_apply": 1e3 * t_apply, "ilu0_apply": 1e3 * t_ilu if has_ilu else None,
                            "spmv": 1e3 * t_spmv},
             "stencil_roofline": stencil,
@@ -397,20 +418,25 @@ def run_ntd(args):
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(args)
         if world == 1 and cfg == 4 and not args.no_configs:
-            out["configs"] = single_configs(peak[0], cpu=not args.no_cpu_baseline)
+            out["configs"] = single_configs(peak[0], cpu=not args.no_cpu_baseline,
+                                            sm_mhz=out["clocks"]["sm_mhz"] or 1965.0)
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def stencil_roofline(solver, B, n, nx, ny, nz):
-    """The bandwidth-bound stencil / CG kernels on the whole shard in one
-    launch each (CUDA events, median of 5): algorithmic bytes per unknown
-    (SURVEY.md 8(d), A as its 4 symmetric bands) / time, against the HBM
-    peak.  north_star asks >= 70% for these."""
+def stencil_roofline(a_dev, B, n, nx, ny, nz):
+    """The bandwidth-bound stencil / CG kernels on B systems (a_dev (B,7,N))
+    in one launch each (CUDA events, median of 5): algorithmic bytes per
+    unknown (SURVEY.md 8(d), A as its 4 symmetric bands) / time, against
+    the HBM peak.  north_star asks >= 70% for these."""
     import torch
     from paper_1909_09771_b200 import _lib
     from paper_1909_09771_b200 import device as D
+
+    class _S:
+        a = a_dev
+    solver = _S()
     a4 = D.sym_pack(solver.a, nx, ny, nz, B)
     if a4 is None:
         return None
@@ -469,7 +495,7 @@ COMBINED_APPLY_BYTES_PER_UNKNOWN = 304
 PCG_ITER_BYTES = 488
 
 
-def single_configs(peak, cfgs=(1, 2, 3, 5), cpu=True):
+def single_configs(peak, cfgs=(1, 2, 3, 5), cpu=True, sm_mhz=1965.0):
     """BASELINE configs 1, 2, 3, 5 (one system each) through the public API on
     device-resident inputs: PCG (ntd+ilu0, tol 1e-8) solve rate and
     iterations against the reference's, the NTD and combined applies alone
@@ -542,11 +568,15 @@ def single_configs(peak, cfgs=(1, 2, 3, 5), cpu=True):
                        "solve_ms": 1e3 * solve_s, "value": rate, "unit": UNIT,
                        "hbm_frac_canonical": PCG_ITER_BYTES * rate * 1e6 / 1e9 / peak},
                "ntd_apply": {"ms": 1e3 * t_ntd, "munknowns_per_s": n / t_ntd / 1e6,
-                             "hbm_frac": NTD_APPLY_BYTES_PER_UNKNOWN * n / t_ntd / 1e9 / peak},
+                             "hbm_frac": NTD_APPLY_BYTES_PER_UNKNOWN * n / t_ntd / 1e9 / peak,
+                             "latency_roofline": ntd_latency_roofline(nx, ny, nz, t_ntd, sm_mhz)},
                "combined_apply": {"ms": 1e3 * t_comb, "munknowns_per_s": n / t_comb / 1e6,
                                   "hbm_frac": COMBINED_APPLY_BYTES_PER_UNKNOWN * n / t_comb / 1e9 / peak},
                "ilu0_apply_ms": 1e3 * t_ilu,
                "ntd_apply_rel_err_vs_oracle": err}
+        if cfg in (3, 5):  # the stencil / CG kernels on one system (north_star: >= 70% of HBM)
+            rec["stencil_roofline"] = {k: {"frac": round(v["frac"], 3), "ms": round(v["ms"], 3)}
+                                       for k, v in stencil_roofline(a_dev.reshape(1, 7, n), 1, n, nx, ny, nz).items()}
         if cfg != 5:
             data = a.host_data()
             fo, split = oracle.build_block_ilu0(data, nx, ny, nz)

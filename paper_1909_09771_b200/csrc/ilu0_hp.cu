@@ -30,6 +30,17 @@
 
 namespace hp {
 
+#ifdef HP_TIMING
+// per-warp cycle accounting of CTA 0 (experiments): [warp][0 work, 1 loads, 2 barrier, 3 steps]
+__device__ unsigned long long g_hp_timing[32][4];
+#define HPT_NOW(v) const long long v = clock64()
+#define HPT_ADD(k, val) \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) g_hp_timing[threadIdx.x >> 5][k] += (unsigned long long)(val)
+#else
+#define HPT_NOW(v)
+#define HPT_ADD(k, val)
+#endif
+
 struct Sweep {
     int G, T, nk, kb;   // groups per plane, steps per unit, planes in the half, first plane (absolute)
     int nx, ny;
@@ -235,6 +246,7 @@ __device__ __forceinline__ void sweep(const Sweep &w, const double *__restrict__
             }
             if (tau + PF < Tu) load(j, tau + PF, op);
         };
+        HPT_NOW(t_w0);
 #pragma unroll
         for (int j = 0; j < UPW; j++) {
             const int tau = T - sm[j];
@@ -252,8 +264,13 @@ __device__ __forceinline__ void sweep(const Sweep &w, const double *__restrict__
                 else unit_step(j, tau, o[2][j]);
             }
         }
+        HPT_NOW(t_w1);
+        HPT_ADD(0, t_w1 - t_w0);
         if (GL || nc == 1) {
             __syncthreads();
+#ifdef HP_TIMING
+            { HPT_NOW(t_w2); HPT_ADD(2, t_w2 - t_w1); HPT_ADD(3, 1); }
+#endif
             // progress for the predecessor's slot reuse (our slot resets are
             // ordered before it: CTA barrier, then a release by thread 0)
             if (GL && lk.halo_in && threadIdx.x == 0 && T >= 0 && (T % PUBLISH == PUBLISH - 1 || T == w.S - 1))
@@ -441,3 +458,16 @@ extern "C" int ntd_ilu0_hp_apply(const double *coef, int64_t split, const double
     }
     return NTD_OK;
 }
+
+#ifdef HP_TIMING
+extern "C" int ntd_hp_timing(unsigned long long *out, int reset)
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, hp::g_hp_timing, sizeof(unsigned long long) * 32 * 4);
+    if (reset) {
+        static unsigned long long z[32 * 4] = {};
+        cudaMemcpyToSymbol(hp::g_hp_timing, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

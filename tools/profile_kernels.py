@@ -32,7 +32,8 @@ for _ in range(2):
     # the NTD sweep as the solver launches it (slot layout, ctas per system)
     _lib.call("ntd_apply_slot_ex", _lib.ptr(P.solve), _lib.ptr(P.work), nx, ny, nz, B, None, ntd_ctas,
               _lib.stream())
-    D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, B, z=x, skew=P.skew, ctas=ilu_ctas)
+    D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, B, z=x, skew=P.skew, ctas=ilu_ctas,
+                 hp=D.ilu0_hp_config(nx, ny, nz, P.split, full))
     D.residual(a, v, x, nx, ny, nz, B, a4=s.precond.a4)
 torch.cuda.synchronize()
 print("ok")
