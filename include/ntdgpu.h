@@ -16,6 +16,8 @@
  *    factor: l1,u1,l2,u2,l3,u3,m_recip (ntd_factor.py:461).
  *  - `active` (int32[B], device, may be NULL = all active): systems with
  *    active[s]==0 are skipped by the kernel (their outputs are untouched).
+ *  - Output arrays must not alias input arrays of the same call (the kernels
+ *    are compiled with restrict-qualified pointers).
  *  - `stream` is a cudaStream_t; every call only enqueues work on it (no host
  *    synchronisation).  Results are bitwise run-to-run deterministic.
  *  - Return value: 0 on success, NTD_EINVAL for bad arguments, NTD_ENOTSUP for

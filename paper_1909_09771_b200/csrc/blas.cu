@@ -30,7 +30,6 @@ int check_launch(const char *where)
     return NTD_OK;
 }
 
-i64 rows_block_cap() { return 148 * 8; }
 }  // namespace ntd
 
 static constexpr int RED_THREADS = 256;
@@ -42,14 +41,17 @@ static constexpr int RED_THREADS = 256;
 // for a system solved alone or in any batch.  VB grows with n (about 8 rows
 // per thread) up to 8 blocks per SM, so one large system keeps every SM's
 // memory pipeline busy (a fixed 148 blocks per system held a single 350^3
-// system at 13% of HBM); about 24 rows per thread (144 blocks per 96^3
-// system: 8 rows per thread gave 67% instead of 80% of HBM on the batch).
-static constexpr int MAX_VB = 148 * 8;
+// system at 13% of HBM); at least 8 rows per thread, so a mid-size system
+// (128^3: 820 blocks) still fills the GPU.
+// at most one wave of the heaviest reduction kernel (k_spmv_dot: 40 registers,
+// 6 resident 256-thread blocks per SM), so a lone system's reduction never
+// runs a partial second wave (148 * 8 virtual blocks: 52% warps active)
+static constexpr int MAX_VB = 148 * 6;
 static constexpr int MAX_PARTS = MAX_VB * (RED_THREADS / 32);
 static constexpr int STN_UNROLL = 2;  // measured: 1 -> 68%, 2 -> 76%, 4 -> 56% of HBM for spmv+dot (64 systems)
 __host__ __device__ __forceinline__ int red_vblocks(i64 n)
 {
-    const i64 v = (n + 24 * RED_THREADS - 1) / (24 * RED_THREADS);
+    const i64 v = (n + 8 * RED_THREADS - 1) / (8 * RED_THREADS);
     return (int)(v < 1 ? 1 : (v > MAX_VB ? MAX_VB : v));
 }
 // Launched blocks per system: every virtual block for a lone system (its
@@ -93,26 +95,20 @@ __global__ void __launch_bounds__(256) k_spmv(const double *__restrict__ a, cons
 {
     i64 s = blockIdx.y;
     if (active && !active[s]) return;
-    const double *as = a + s * 7 * n;
-    const double *xs = x + s * n;
-    double *ys = y + s * n;
+    const double *__restrict__ as = a + s * 7 * n;
+    const double *__restrict__ xs = x + s * n;
+    double *__restrict__ ys = y + s * n;
     for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < n; r += (i64)gridDim.x * blockDim.x)
         ys[r] = spmv_row(as, xs, r, n, nx, nxy);
 }
 
-static unsigned grid_rows(i64 n)
-{
-    i64 b = (n + 255) / 256;
-    i64 cap = ntd::rows_block_cap();
-    return (unsigned)(b < cap ? (b > 0 ? b : 1) : cap);
-}
 
 extern "C" int ntd_spmv(const double *a, const double *x, double *y, int64_t nx, int64_t ny,
                         int64_t nz, int64_t batch, const int32_t *active, void *stream)
 {
     if (!a || !x || !y || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
     i64 n = nx * ny * nz;
-    dim3 grid(grid_rows(n), (unsigned)batch);
+    dim3 grid(ntd::fill_grid<k_spmv>(n), (unsigned)batch);
     k_spmv<<<grid, 256, 0, (cudaStream_t)stream>>>(a, x, y, n, nx, nx * ny, active);
     NTD_CHECK_LAUNCH("ntd_spmv");
 }
@@ -128,17 +124,17 @@ __global__ void __launch_bounds__(256) k_residual(const double *__restrict__ a, 
 {
     i64 s = blockIdx.y;
     if (active && !active[s]) return;
-    const double *as = a + s * NB * n;
-    const double *ws = w + s * n;
-    const double *rs = r + s * n;
-    double *ts = t + s * n;
+    const double *__restrict__ as = a + s * NB * n;
+    const double *__restrict__ ws = w + s * n;
+    const double *__restrict__ rs = r + s * n;
+    double *__restrict__ ts = t + s * n;
     if (!v) {
         for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
             ts[i] = sub_rn(rs[i], row_of<NB>(as, ws, i, n, nx, nxy));
         return;
     }
-    const double *vs = v + s * n;
-    double *zs = z_out + s * n;
+    const double *__restrict__ vs = v + s * n;
+    double *__restrict__ zs = z_out + s * n;
     for (i64 r0 = blockIdx.x * (i64)blockDim.x + threadIdx.x; r0 < n; r0 += (i64)gridDim.x * blockDim.x) {
         // spmv of z = v + w, z formed on the fly at the 7 taps (bitwise).
 #define ZV(idx) add_rn(vs[idx], ws[idx])
@@ -170,7 +166,7 @@ static int residual_nb(const double *a, const double *r, const double *w, const 
     if (!a || !r || !w || !t || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
     if ((v == nullptr) != (z_out == nullptr)) return NTD_EINVAL;
     i64 n = nx * ny * nz;
-    dim3 grid(grid_rows(n), (unsigned)batch);
+    dim3 grid(ntd::fill_grid<k_residual<NB>>(n), (unsigned)batch);
     k_residual<NB><<<grid, 256, 0, (cudaStream_t)stream>>>(a, r, w, v, z_out, t, n, nx, nx * ny, active);
     NTD_CHECK_LAUNCH("ntd_residual");
 }
@@ -195,8 +191,8 @@ __global__ void k_sym_pack(const double *__restrict__ a, double *__restrict__ a4
                            i64 nx, i64 nxy)
 {
     const i64 s = blockIdx.y;
-    const double *as = a + s * 7 * n;
-    double *o = a4 + s * 4 * n;
+    const double *__restrict__ as = a + s * 7 * n;
+    double *__restrict__ o = a4 + s * 4 * n;
     bool good = true;
     for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < n; r += (i64)gridDim.x * blockDim.x) {
         o[r] = as[3 * n + r];
@@ -216,7 +212,7 @@ extern "C" int ntd_sym_pack(const double *a, double *a4, int32_t *sym_ok, int64_
 {
     if (!a || !a4 || !sym_ok || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
     i64 n = nx * ny * nz;
-    dim3 grid(grid_rows(n), (unsigned)batch);
+    dim3 grid(ntd::fill_grid<k_sym_pack>(n), (unsigned)batch);
     k_sym_pack<<<grid, 256, 0, (cudaStream_t)stream>>>(a, a4, sym_ok, n, nx, nx * ny);
     NTD_CHECK_LAUNCH("ntd_sym_pack");
 }
@@ -231,7 +227,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_dot_partial(const double *__res
     i64 s = blockIdx.y;
     if (active && !active[s]) return;
     const int VB = red_vblocks(n);
-    const double *xs = x + s * n, *ys = y + s * n;
+    const double *__restrict__ xs = x + s * n, *__restrict__ ys = y + s * n;
     for (int vb = blockIdx.x; vb < VB; vb += gridDim.x) {
         double acc = 0.0;
 #pragma unroll STN_UNROLL
@@ -325,7 +321,7 @@ extern "C" int ntd_pcg_init(const double *b, double *x, double *r, double *state
 {
     if (!b || !x || !r || !state || !flags || !active || !work || n < 1 || batch < 1) return NTD_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
-    dim3 grid(grid_rows(n), (unsigned)batch);
+    dim3 grid(ntd::fill_grid<k_pcg_init_vec>(n), (unsigned)batch);
     k_pcg_init_vec<<<grid, 256, 0, st>>>(b, x, r, n);
     int rc = launch_dot(b, b, work, n, batch, nullptr, st);
     if (rc) return rc;
@@ -358,7 +354,7 @@ extern "C" int ntd_pcg_start(const double *r, const double *z, double *p, double
 {
     if (!r || !z || !p || !state || !work || n < 1 || batch < 1) return NTD_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
-    dim3 grid(grid_rows(n), (unsigned)batch);
+    dim3 grid(ntd::fill_grid<k_copy>(n), (unsigned)batch);
     k_copy<<<grid, 256, 0, st>>>(z, p, n, active);
     int rc = launch_dot(r, z, work, n, batch, active, st);
     if (rc) return rc;
@@ -375,8 +371,8 @@ __global__ void __launch_bounds__(RED_THREADS) k_spmv_dot(const double *__restri
     __shared__ double sh[RED_THREADS];
     i64 s = blockIdx.y;
     if (active && !active[s]) return;
-    const double *as = a + s * NB * n, *ps = p + s * n;
-    double *aps = ap + s * n;
+    const double *__restrict__ as = a + s * NB * n, *__restrict__ ps = p + s * n;
+    double *__restrict__ aps = ap + s * n;
     // virtual blocks vb = the partials' owners, so the reduction tree (and the
     // result) depends on n only, not on the launched grid
     const int VB = red_vblocks(n);
@@ -467,7 +463,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_true_res(const double *__restri
     __shared__ double sh[RED_THREADS];
     i64 s = blockIdx.y;
     if (!active[s]) return;
-    const double *as = a + s * NB * n, *xs = x + s * n, *bs = b + s * n;
+    const double *__restrict__ as = a + s * NB * n, *__restrict__ xs = x + s * n, *__restrict__ bs = b + s * n;
     const int VB = red_vblocks(n);
     for (int vb = blockIdx.x; vb < VB; vb += gridDim.x) {  // virtual blocks, as in k_spmv_dot
         double acc = 0.0;
@@ -517,7 +513,7 @@ static int update_residual_nb(const double *a, const double *b, double *x, doubl
     if (!a || !b || !x || !r || !p || !ap || !state || !flags || !active || !history || !work) return NTD_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     i64 n = nx * ny * nz;
-    dim3 grid(grid_rows(n), (unsigned)batch);
+    dim3 grid(ntd::fill_grid<k_update_xr>(n), (unsigned)batch);
     k_update_xr<<<grid, 256, 0, st>>>(x, r, p, ap, state, n, active);
     int rc = ntd::check_launch("update_xr");
     if (rc) return rc;
@@ -582,7 +578,7 @@ extern "C" int ntd_pcg_direction(const double *r, const double *z, double *p, do
     k_beta<<<(unsigned)batch, RED_THREADS, 0, st>>>(work, state, active, n);
     rc = ntd::check_launch("beta");
     if (rc) return rc;
-    dim3 grid(grid_rows(n), (unsigned)batch);
+    dim3 grid(ntd::fill_grid<k_update_p>(n), (unsigned)batch);
     k_update_p<<<grid, 256, 0, st>>>(p, z, state, n, active);
     NTD_CHECK_LAUNCH("ntd_pcg_direction");
 }

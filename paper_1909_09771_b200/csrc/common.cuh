@@ -36,8 +36,28 @@ __device__ __forceinline__ void prefetch_l2(const void *p)
 namespace ntd {
 void set_error(const char *where, cudaError_t e);
 int check_launch(const char *where);
-// Per-system block cap of the bandwidth-bound row kernels (8 blocks per SM).
-i64 rows_block_cap();
 }  // namespace ntd
 
 #define NTD_CHECK_LAUNCH(name) return ntd::check_launch(name)
+
+namespace ntd {
+// Blocks of 256 threads per system for a grid-stride kernel over `rows`
+// rows: one full wave of the kernel on the GPU (SMs x resident blocks per SM,
+// from the occupancy of this kernel instantiation), fewer for small systems.
+// A fixed 8 blocks per SM left a partial second wave for kernels whose
+// register count allows only 5-6 resident blocks.
+template <auto K>
+unsigned fill_grid(i64 rows)
+{
+    static int wave = 0;  // per kernel instantiation (same on every B200)
+    if (wave == 0) {
+        int occ = 0, sms = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K, 256, 0);
+        wave = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 148);
+    }
+    const i64 b = (rows + 255) / 256;
+    return (unsigned)(b < wave ? (b > 0 ? b : 1) : wave);
+}
+}  // namespace ntd

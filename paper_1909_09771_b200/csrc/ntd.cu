@@ -180,8 +180,8 @@ __global__ void __launch_bounds__(256) k_residual_to_sl(const double *__restrict
     if (active && !active[s]) return;
     const int LR = sl::lr_of(K);
     const i64 lines = n / nx;
-    const double *as = a + s * NB * n, *ws = w + s * n, *rs = r + s * n, *ms = pre + s * 7 * n + 6 * n;
-    double *bs = bsl + s * lines * LR;
+    const double *__restrict__ as = a + s * NB * n, *__restrict__ ws = w + s * n, *__restrict__ rs = r + s * n, *__restrict__ ms = pre + s * 7 * n + 6 * n;
+    double *__restrict__ bs = bsl + s * lines * LR;
     for (i64 r0 = blockIdx.x * (i64)blockDim.x + threadIdx.x; r0 < n; r0 += (i64)gridDim.x * blockDim.x) {
         const double t = sub_rn(rs[r0], row_of<NB>(as, ws, r0, n, nx, nxy));
         const unsigned line = (unsigned)r0 / (unsigned)nx;
@@ -201,8 +201,8 @@ __global__ void __launch_bounds__(256) k_residual_from_sl(const double *__restri
     if (active && !active[s]) return;
     const int LR = sl::lr_of(K);
     const i64 lines = n / nx, plr = (i64)ny * LR;
-    const double *as = a + s * NB * n, *ws = w + s * n, *rs = r + s * n, *xs = xsl + s * lines * LR;
-    double *zs = z_out + s * n, *ts = t + s * n;
+    const double *__restrict__ as = a + s * NB * n, *__restrict__ ws = w + s * n, *__restrict__ rs = r + s * n, *__restrict__ xs = xsl + s * lines * LR;
+    double *__restrict__ zs = z_out + s * n, *__restrict__ ts = t + s * n;
     const double *d0 = as + (NB == 4 ? 0 : 3 * n);
     const double *lm1 = NB == 4 ? as + n - 1 : as + 2 * n, *lmx = NB == 4 ? as + 2 * n - nx : as + n;
     const double *lmz = NB == 4 ? as + 3 * n - nxy : as;
@@ -249,7 +249,8 @@ extern "C" int ntd_residual_to_slot(const double *a, int64_t bands, const double
     const int K = pick_k(nx);
     if (K <= 0 || !sl_depth(K) || nx * ny * nz >= (1ll << 31)) return NTD_ENOTSUP;
     const i64 n = nx * ny * nz;
-    dim3 grid((unsigned)std::min<i64>((n + 255) / 256, ntd::rows_block_cap()), (unsigned)batch);
+    dim3 grid(bands == 4 ? ntd::fill_grid<k_residual_to_sl<4>>(n) : ntd::fill_grid<k_residual_to_sl<7>>(n),
+              (unsigned)batch);
     if (bands == 4)
         k_residual_to_sl<4><<<grid, 256, 0, (cudaStream_t)stream>>>(a, pre, r, w, work, n, (int)nx, nx * ny, K, active);
     else
@@ -299,7 +300,8 @@ extern "C" int ntd_residual_from_slot(const double *a, int64_t bands, const doub
     if (K <= 0 || !sl_depth(K) || nx * ny * nz >= (1ll << 31)) return NTD_ENOTSUP;
     const i64 n = nx * ny * nz, s = sl_doubles(nx, ny, nz) * batch;
     const double *xsl = work + s;
-    dim3 grid((unsigned)std::min<i64>((n + 255) / 256, ntd::rows_block_cap()), (unsigned)batch);
+    dim3 grid(bands == 4 ? ntd::fill_grid<k_residual_from_sl<4>>(n) : ntd::fill_grid<k_residual_from_sl<7>>(n),
+              (unsigned)batch);
     if (bands == 4)
         k_residual_from_sl<4><<<grid, 256, 0, (cudaStream_t)stream>>>(a, r, w, xsl, z_out, t, n, (int)nx, nx * ny,
                                                                       (int)ny, K, active);
