@@ -210,11 +210,12 @@ int ntd_apply_direct(const double *pre, const double *b, double *x,
  * apply needs no layout conversions.  a: the 7-band operator (bands == 7) or
  * the ntd_sym_pack operator (bands == 4).  Available when ntd_solve_doubles
  * is non-zero (NTD_ENOTSUP otherwise).
- *   ntd_residual_to_slot:   b' = (r - A w) * m_recip into the apply's input
+ *   ntd_residual_to_slot:   b' = (r - A w) * mu into the apply's input (mu: the
+ *                           per-cell pivot reciprocals kept in `solve`)
  *   ntd_apply_slot:         the NTD apply of b' (ntd_solve.py:303-322)
  *   ntd_residual_from_slot: z_out = x + w, t = r - A z_out (x: the apply's
  *                           result), bitwise equal to ntd_residual(v = x). */
-int ntd_residual_to_slot(const double *a, int64_t bands, const double *pre,
+int ntd_residual_to_slot(const double *a, int64_t bands, const double *solve,
                          const double *r, const double *w, double *work,
                          int64_t nx, int64_t ny, int64_t nz, int64_t batch,
                          const int32_t *active, void *stream);

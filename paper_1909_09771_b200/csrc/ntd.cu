@@ -4,7 +4,7 @@
 #include <algorithm>
 
 #include "ntd_kernels.cuh"
-#include "ntd_apply_sl.cuh"
+#include "ntd_apply_ts.cuh"
 #include "stencil.cuh"
 
 // instantiated K values (ntd_k<K>.cu); a line of nx cells uses the
@@ -37,25 +37,25 @@ static int pick_k(i64 nx)
 
 extern "C" int64_t ntd_max_nx(void) { return 32 * MAX_K; }
 
-// Slot-layout (SL) path: K values with an instantiated SL kernel and a ring
+// Lane-layout (TS) path: K values with an instantiated ring kernel and a ring
 // that fits in shared memory.
 static int sl_depth(int K)
 {
     if (K > 11) return 0;
-    return sl::depth_of(K) >= 2 ? sl::depth_of(K) : 0;
+    return ts::depth_of(K) >= 2 ? ts::depth_of(K) : 0;
 }
 
 static i64 sl_doubles(i64 nx, i64 ny, i64 nz)
 {
     const int K = pick_k(nx);
-    return K > 0 ? ny * nz * (i64)sl::lr_of(K) : 0;
+    return K > 0 ? ny * nz * (i64)ts::lr_of(K) : 0;
 }
 
 extern "C" int64_t ntd_solve_doubles(int64_t nx, int64_t ny, int64_t nz, int64_t batch)
 {
     const int K = pick_k(nx);
     if (K <= 0 || !sl_depth(K)) return 0;
-    return (int64_t)sl::recd_of(K) * ny * nz * batch;
+    return (int64_t)(ts::recd_of(K) + ts::lr_of(K)) * ny * nz * batch;  // records, then mu of every cell
 }
 
 extern "C" int64_t ntd_apply_work_doubles(int64_t nx, int64_t ny, int64_t nz, int64_t batch)
@@ -64,7 +64,7 @@ extern "C" int64_t ntd_apply_work_doubles(int64_t nx, int64_t ny, int64_t nz, in
     const i64 s = sl_doubles(nx, ny, nz) * batch;
     const int K = pick_k(nx);
     // b, x, xs in SL, a zero plane (+ solve records when the caller has none)
-    const i64 w = K > 0 ? 3 * s + ny * (i64)sl::lr_of(K) + (i64)sl::recd_of(K) * ny * nz * batch : 0;
+    const i64 w = K > 0 ? 3 * s + ny * (i64)ts::lr_of(K) + (i64)(ts::recd_of(K) + ts::lr_of(K)) * ny * nz * batch : 0;
     return w > n ? w : n;
 }
 
@@ -75,15 +75,17 @@ extern "C" int ntd_solve_bands(const double *pre, double *solve, int64_t nx, int
     const int K = pick_k(nx);
     if (K <= 0 || !sl_depth(K)) return NTD_ENOTSUP;
     const i64 lines = ny * nz;
-    i64 total = lines * sl::lr_of(K) * batch;
-    i64 blocks = (total + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    sl::k_solve_sl<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(pre, solve, (int)nx, lines, K, batch);
+    cudaStream_t st_ = (cudaStream_t)stream;
+    double *mu = solve + (i64)ts::recd_of(K) * lines * batch;
+    // padding elements of every record array are exact zeros
+    if (cudaMemsetAsync(solve, 0, sizeof(double) * (size_t)ntd_solve_doubles(nx, ny, nz, batch), st_) != cudaSuccess)
+        return ntd::check_launch("memset");
+    ts::k_solve_ts<<<(unsigned)((lines * batch + 127) / 128), 128, 0, st_>>>(pre, solve, mu, (int)nx, lines, K, batch);
     int rc = ntd::check_launch("ntd_solve_bands");
     if (rc) return rc;
     switch (K) {
 #define PREPCASE(KK) \
-    case KK: return launch_prep_sl_k<KK>(solve, lines * batch, (cudaStream_t)stream);
+    case KK: return launch_prep_ts_k<KK>(solve, lines * batch, (cudaStream_t)stream);
         PREPCASE(1) PREPCASE(2) PREPCASE(3) PREPCASE(4) PREPCASE(5) PREPCASE(6) PREPCASE(8) PREPCASE(11)
 #undef PREPCASE
     default: return NTD_ENOTSUP;
@@ -120,7 +122,7 @@ static int apply_impl(const double *pre, const double *solve, const double *b, d
     if (depth && aligned && !direct) {
         const i64 lines = ny * nz, s = sl_doubles(nx, ny, nz) * batch;
         double *bsl = work, *xsl = work + s, *xssl = work + 2 * s, *zpl = work + 3 * s;
-        const i64 zn = ny * (i64)sl::lr_of(K);
+        const i64 zn = ny * (i64)ts::lr_of(K);
         if (!solve) {
             double *sv = zpl + zn;
             int rc = ntd_solve_bands(pre, sv, nx, ny, nz, batch, stream);
@@ -129,13 +131,14 @@ static int apply_impl(const double *pre, const double *solve, const double *b, d
         }
         // the missing level-3 neighbour of the first/last plane reads zeros
         if (cudaMemsetAsync(zpl, 0, sizeof(double) * zn, st) != cudaSuccess) return ntd::check_launch("memset");
-        sl::k_to_sl<<<grid_for(s), 256, 0, st>>>(b, pre, bsl, (int)nx, lines, K, batch);
+        ts::k_to_ts<<<grid_for(s), 256, 0, st>>>(b, solve + (i64)ts::recd_of(K) * lines * batch, bsl, (int)nx, lines, K,
+                                                 batch);
         int rc = ntd::check_launch("ntd_apply to_sl");
         if (rc) return rc;
         switch (K) {
 #define SLCASE(KK)                                                                                                \
     case KK:                                                                                                       \
-        rc = launch_apply_sl_k<KK>(solve, bsl, xsl, xssl, zpl, (int)nx, (int)ny, (int)nz, batch, active, st,     \
+        rc = launch_apply_ts_k<KK>(solve, bsl, xsl, xssl, zpl, (int)nx, (int)ny, (int)nz, batch, active, st,     \
                                    (int)ctas_per_system);                                                          \
         break;
             SLCASE(1) SLCASE(2) SLCASE(3) SLCASE(4) SLCASE(5) SLCASE(6) SLCASE(8) SLCASE(11)
@@ -143,7 +146,7 @@ static int apply_impl(const double *pre, const double *solve, const double *b, d
         default: return NTD_ENOTSUP;
         }
         if (rc) return rc;
-        sl::k_from_sl<<<grid_for(nx * lines * batch), 256, 0, st>>>(xsl, x, (int)nx, lines, K, batch, active);
+        ts::k_from_ts<<<grid_for(nx * lines * batch), 256, 0, st>>>(xsl, x, (int)nx, lines, K, batch, active);
         return ntd::check_launch("ntd_apply from_sl");
     }
     NTD_DISPATCH(launch_apply_k, pre, b, x, work, (int)nx, (int)ny, (int)nz, batch, active, st);
@@ -171,22 +174,24 @@ extern "C" int ntd_apply_direct(const double *pre, const double *b, double *x, d
 // Both keep the reference summation order (bitwise equal to ntd_residual on
 // the natural-layout vectors).
 template <int NB>
-__global__ void __launch_bounds__(256) k_residual_to_sl(const double *__restrict__ a, const double *__restrict__ pre,
+__global__ void __launch_bounds__(256) k_residual_to_sl(const double *__restrict__ a, const double *__restrict__ mu,
                                                         const double *__restrict__ r, const double *__restrict__ w,
                                                         double *__restrict__ bsl, i64 n, int nx, i64 nxy, int K,
                                                         const int32_t *__restrict__ active)
 {
     const i64 s = blockIdx.y;
     if (active && !active[s]) return;
-    const int LR = sl::lr_of(K);
+    const int LR = ts::lr_of(K);
     const i64 lines = n / nx;
-    const double *__restrict__ as = a + s * NB * n, *__restrict__ ws = w + s * n, *__restrict__ rs = r + s * n, *__restrict__ ms = pre + s * 7 * n + 6 * n;
+    const double *__restrict__ as = a + s * NB * n, *__restrict__ ws = w + s * n, *__restrict__ rs = r + s * n;
+    const double *__restrict__ ms = mu + s * lines * LR;
     double *__restrict__ bs = bsl + s * lines * LR;
     for (i64 r0 = blockIdx.x * (i64)blockDim.x + threadIdx.x; r0 < n; r0 += (i64)gridDim.x * blockDim.x) {
         const double t = sub_rn(rs[r0], row_of<NB>(as, ws, r0, n, nx, nxy));
         const unsigned line = (unsigned)r0 / (unsigned)nx;
         const int i = (int)(r0 - (i64)line * nx);
-        bs[(i64)line * LR + sl::sl_index(i, nx, K)] = t * ms[r0];
+        const i64 e = (i64)line * LR + ts::ts_index(i, K);
+        bs[e] = t * ms[e];
     }
 }
 
@@ -199,7 +204,7 @@ __global__ void __launch_bounds__(256) k_residual_from_sl(const double *__restri
 {
     const i64 s = blockIdx.y;
     if (active && !active[s]) return;
-    const int LR = sl::lr_of(K);
+    const int LR = ts::lr_of(K);
     const i64 lines = n / nx, plr = (i64)ny * LR;
     const double *__restrict__ as = a + s * NB * n, *__restrict__ ws = w + s * n, *__restrict__ rs = r + s * n, *__restrict__ xs = xsl + s * lines * LR;
     double *__restrict__ zs = z_out + s * n, *__restrict__ ts = t + s * n;
@@ -212,11 +217,11 @@ __global__ void __launch_bounds__(256) k_residual_from_sl(const double *__restri
         const unsigned line = (unsigned)r0 / (unsigned)nx;
         const int i = (int)(r0 - (i64)line * nx);
         const i64 lb = (i64)line * LR;
-        const int sc = sl::sl_index(i, nx, K);
+        const int sc = ts::ts_index(i, K);
         // x at the 7 taps (cell i-1 / i+1 wrap to the neighbouring line, where
         // the band value is an exact zero: same operands as the natural layout)
-        const i64 pm1 = i > 0 ? lb + sl::sl_index(i - 1, nx, K) : lb - LR + sl::sl_index(nx - 1, nx, K);
-        const i64 pp1 = i < nx - 1 ? lb + sl::sl_index(i + 1, nx, K) : lb + LR + sl::sl_index(0, nx, K);
+        const i64 pm1 = i > 0 ? lb + ts::ts_index(i - 1, K) : lb - LR + ts::ts_index(nx - 1, K);
+        const i64 pp1 = i < nx - 1 ? lb + ts::ts_index(i + 1, K) : lb + LR + ts::ts_index(0, K);
 #define ZV(idx, pos) add_rn(xs[pos], ws[idx])
         const double zc = ZV(r0, lb + sc);
         double sacc = mul_rn(d0[r0], zc);
@@ -240,15 +245,16 @@ static bool slot_path(i64 nx, const double *work, const double *solve, int *K_ou
     return K > 0 && sl_depth(K) && aligned && solve;
 }
 
-extern "C" int ntd_residual_to_slot(const double *a, int64_t bands, const double *pre, const double *r,
+extern "C" int ntd_residual_to_slot(const double *a, int64_t bands, const double *solve, const double *r,
                                     const double *w, double *work, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
                                     const int32_t *active, void *stream)
 {
-    if (!a || !pre || !r || !w || !work || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
+    if (!a || !solve || !r || !w || !work || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
     if (bands != 4 && bands != 7) return NTD_EINVAL;
     const int K = pick_k(nx);
     if (K <= 0 || !sl_depth(K) || nx * ny * nz >= (1ll << 31)) return NTD_ENOTSUP;
     const i64 n = nx * ny * nz;
+    const double *pre = solve + (i64)ts::recd_of(K) * ny * nz * batch;  // mu of every cell (lane layout)
     dim3 grid(bands == 4 ? ntd::fill_grid<k_residual_to_sl<4>>(n) : ntd::fill_grid<k_residual_to_sl<7>>(n),
               (unsigned)batch);
     if (bands == 4)
@@ -277,12 +283,12 @@ extern "C" int ntd_apply_slot_ex(const double *solve, double *work, int64_t nx, 
     cudaStream_t st = (cudaStream_t)stream;
     const i64 s = sl_doubles(nx, ny, nz) * batch;
     double *bsl = work, *xsl = work + s, *xssl = work + 2 * s, *zpl = work + 3 * s;
-    const i64 zn = ny * (i64)sl::lr_of(K);
+    const i64 zn = ny * (i64)ts::lr_of(K);
     if (cudaMemsetAsync(zpl, 0, sizeof(double) * zn, st) != cudaSuccess) return ntd::check_launch("memset");
     switch (K) {
 #define SLCASE(KK) \
     case KK:                                                                                                       \
-        return launch_apply_sl_k<KK>(solve, bsl, xsl, xssl, zpl, (int)nx, (int)ny, (int)nz, batch, active, st,    \
+        return launch_apply_ts_k<KK>(solve, bsl, xsl, xssl, zpl, (int)nx, (int)ny, (int)nz, batch, active, st,    \
                                      (int)ctas_per_system);
         SLCASE(1) SLCASE(2) SLCASE(3) SLCASE(4) SLCASE(5) SLCASE(6) SLCASE(8) SLCASE(11)
 #undef SLCASE

@@ -1,5 +1,5 @@
 // instantiation of the NTD kernels for K=11 cells per lane (see ntd.cu)
 #include "ntd_kernels.cuh"
-#include "ntd_apply_sl.cuh"
+#include "ntd_apply_ts.cuh"
 NTD_INSTANTIATE(11)
-NTD_INSTANTIATE_SL(11)
+NTD_INSTANTIATE_TS(11)

@@ -1,4 +1,4 @@
 // instantiation of the NTD kernels for K=16 cells per lane (see ntd.cu)
 #include "ntd_kernels.cuh"
-#include "ntd_apply_sl.cuh"
+#include "ntd_apply_ts.cuh"
 NTD_INSTANTIATE(16)

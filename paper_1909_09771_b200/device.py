@@ -313,7 +313,7 @@ class CombinedDevice:
                        ctas=self.ilu_ctas, hp=self.ilu_hp)
         op, nb = (self.a, 7) if self.a4 is None else (self.a4, 4)
         if self.fused:
-            _lib.call("ntd_residual_to_slot", _lib.ptr(op), nb, _lib.ptr(self.pre), _lib.ptr(r), _lib.ptr(self.w),
+            _lib.call("ntd_residual_to_slot", _lib.ptr(op), nb, _lib.ptr(self.solve), _lib.ptr(r), _lib.ptr(self.w),
                       _lib.ptr(self.work), *g, _lib.ptr(active), _lib.stream())
         else:
             residual(self.a, r, self.w, *g, t=self.t, active=active, a4=self.a4)

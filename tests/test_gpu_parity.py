@@ -266,13 +266,13 @@ def test_sm_mappings_bitwise(ntd):
             xs = []
             for c in (1, 2):
                 P.work.zero_()
-                _lib.call("ntd_residual_to_slot", _lib.ptr(P.a4), 4, _lib.ptr(P.pre), _lib.ptr(v), _lib.ptr(outs[0]),
+                _lib.call("ntd_residual_to_slot", _lib.ptr(P.a4), 4, _lib.ptr(P.solve), _lib.ptr(v), _lib.ptr(outs[0]),
                           _lib.ptr(P.work), nx, ny, nz, 2, None, _lib.stream())
                 _lib.call("ntd_apply_slot_ex", _lib.ptr(P.solve), _lib.ptr(P.work), nx, ny, nz, 2, None, c,
                           _lib.stream())
                 # the apply's result x in the slot layout: work[s:2s]
                 kk = next(k for k in (1, 2, 3, 4, 5, 6, 8, 11, 12, 16) if 32 * k >= nx)
-                s_ = ny * nz * (32 * kk + 2) * 2
+                s_ = ny * nz * (32 * kk) * 2
                 xs.append(P.work[s_:2 * s_].clone())
             assert torch.equal(xs[0], xs[1]), (nx, ny, nz)
 
