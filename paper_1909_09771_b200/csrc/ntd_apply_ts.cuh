@@ -14,7 +14,7 @@
 //
 // Solve record of one line (record-major, [system][line][RECD]), derived once
 // at setup from the factor (ntd_solve_bands):
-//   [ EFB (eF, eB pairs, 2 LR) | PREP (NPREP x 32, pairs) | L2' | U2' | L3' | U3' ]
+//   [ L2' | L3' | EFB (eF, eB pairs, 2 LR) | PREP (NPREP x 32, pairs) | U3' | U2' ]
 // eF / eB are the scaled elimination multipliers of the two-sided solve,
 // PREP the factor-only scan coefficients, and the couplings are pre-multiplied
 // by mu (the twisted pivot reciprocal at the cell): c' = c mu, as is the
@@ -23,26 +23,23 @@
 #pragma once
 #include "ntd_kernels.cuh"
 #include "ntd_line_ts.cuh"
+#include <type_traits>
 
 namespace ts {
 
-constexpr int NPREP = 12;  // stored PrepTS coefficients per lane; p1 and q1 are rebuilt
+constexpr int NPREP = 8;  // stored PrepTS coefficients per lane (m2 m4 m8 e, n2 n4 n8 f); m1 and n1 are rebuilt
 __host__ __device__ constexpr int lr_of(int K) { return 32 * K; }
-__host__ __device__ constexpr int o_efb(int K) { return 0; }
-__host__ __device__ constexpr int o_prep(int K) { return 2 * lr_of(K); }
-__host__ __device__ constexpr int blk_of(int K) { return 2 * lr_of(K) + NPREP * 32; }  // [EFB|PREP]
-__host__ __device__ constexpr int o_l2(int K) { return blk_of(K); }
-__host__ __device__ constexpr int o_u2(int K) { return blk_of(K) + lr_of(K); }
-__host__ __device__ constexpr int o_l3(int K) { return blk_of(K) + 2 * lr_of(K); }
-__host__ __device__ constexpr int o_u3(int K) { return blk_of(K) + 3 * lr_of(K); }
-__host__ __device__ constexpr int recd_of(int K) { return blk_of(K) + 4 * lr_of(K); }
-// ring stage: [block | S0: in-plane coupling | S1: C1 | S2: C2 | X: b' or xo | S4: second in-plane coupling (twist line)]
-__host__ __device__ constexpr int rs0_of(int K) { return blk_of(K); }
-__host__ __device__ constexpr int rs1_of(int K) { return blk_of(K) + lr_of(K); }
-__host__ __device__ constexpr int rs2_of(int K) { return blk_of(K) + 2 * lr_of(K); }
-__host__ __device__ constexpr int rx_of(int K) { return blk_of(K) + 3 * lr_of(K); }
-__host__ __device__ constexpr int rs4_of(int K) { return blk_of(K) + 4 * lr_of(K); }
-__host__ __device__ constexpr int stage_of(int K) { return blk_of(K) + 5 * lr_of(K); }
+// record: [ L2' | L3' | EFB | PREP | U3' | U2' ] -- whatever a line step reads is one contiguous range
+__host__ __device__ constexpr int o_l2(int K) { return 0; }
+__host__ __device__ constexpr int o_l3(int K) { return lr_of(K); }
+__host__ __device__ constexpr int o_efb(int K) { return 2 * lr_of(K); }
+__host__ __device__ constexpr int o_prep(int K) { return 4 * lr_of(K); }
+__host__ __device__ constexpr int o_u3(int K) { return 4 * lr_of(K) + NPREP * 32; }
+__host__ __device__ constexpr int o_u2(int K) { return 5 * lr_of(K) + NPREP * 32; }
+__host__ __device__ constexpr int recd_of(int K) { return 6 * lr_of(K) + NPREP * 32; }
+// ring stage: [ record | X: b' or xo ]
+__host__ __device__ constexpr int rx_of(int K) { return recd_of(K); }
+__host__ __device__ constexpr int stage_of(int K) { return recd_of(K) + lr_of(K); }
 
 constexpr int SMEM_MAX = 232448 - 1024;
 __host__ __device__ constexpr int clamp8(int d) { return d > 8 ? 8 : d; }
@@ -54,7 +51,7 @@ __host__ __device__ constexpr int depth2_of(int K) { return clamp8((SMEM_MAX - s
 // split kernel with plane buffers sized for ny <= 32K+1 (a half-plane of 16K+1 lines per solver warp); < 2: none
 __host__ __device__ constexpr int depth_smb_of(int K)
 {
-    return clamp8((SMEM_MAX - static_smem_of(K, 1) - 2 * (16 * K + 1) * lr_of(K) * 8) / (2 * stage_of(K) * 8));
+    return clamp8((SMEM_MAX - static_smem_of(K, 1) - (2 * (16 * K + 1) + 1) * lr_of(K) * 8) / (2 * stage_of(K) * 8));
 }
 
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
@@ -174,19 +171,6 @@ struct TsArrays {  // one system, TS
     const double *zero;   // one plane of zero records: the missing level-3 neighbour
 };
 
-template <int K>
-__device__ __forceinline__ void ld_rec(const double *rec, int lane, double (&v)[K])
-{
-#pragma unroll
-    for (int k = 0; k < K; k++) v[k] = rec[k * 32 + lane];
-}
-template <int K>
-__device__ __forceinline__ void st_rec(double *rec, int lane, const double (&v)[K])
-{
-#pragma unroll
-    for (int k = 0; k < K; k++) rec[k * 32 + lane] = v[k];
-}
-
 // ring of D stages per solver warp
 template <int K, int D>
 struct Ring {
@@ -229,7 +213,7 @@ __global__ void k_prep_ts(double *__restrict__ solve, i64 lines_total)
     }
     const PrepTS P = line_prep<K>(lane, eF, eB);
     double *pp = rec + o_prep(K);
-    const double v[NPREP] = {P.p2, P.p3, P.s1, P.s2, P.s3, P.e1, P.q2, P.q3, P.t1, P.t2, P.t3, P.f1};
+    const double v[NPREP] = {P.m2, P.m4, P.m8, P.e, P.n2, P.n4, P.n8, P.f};
 #pragma unroll
     for (int c = 0; c < NPREP; c++) pp[(c >> 1) * 64 + 2 * lane + (c & 1)] = v[c];
 }
@@ -251,89 +235,212 @@ __device__ __forceinline__ void mbar_wait_producer(void *bar, unsigned parity)
     }
 }
 
+__device__ __forceinline__ void mbar_wait_a(unsigned bar, unsigned parity);
+__device__ __forceinline__ void mbar_expect_tx_a(unsigned bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// The bulk copies of one record, issued by ONE lane.  A record costs that
+// lane several hundred cycles (barrier wait, byte count, 4-5 copy
+// instructions), more than a line step of the solver, so a producer warp
+// works on NB consecutive records at a time, one per lane (produce_range).
+__device__ __forceinline__ void tma_load_a(unsigned dst, const void *src, unsigned bytes, unsigned bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
 template <int K>
-__device__ __forceinline__ void rec_copy(const TsArrays &S, const PlaneDesc &P, const Seq &Q, int k, double *dst,
-                                         unsigned long long *bar)
+__device__ __forceinline__ void rec_copy(const TsArrays &S, const PlaneDesc &P, const Seq &Q, int k, unsigned dst,
+                                         unsigned bar)
 {
     constexpr int LR = lr_of(K);
-    constexpr unsigned lb = LR * 8u, bb = blk_of(K) * 8u;
+    constexpr unsigned lb = LR * 8u;
     const bool lower3 = P.mode == M_LOWER3;
     const int ph = k < Q.cnt ? 0 : k == Q.cnt ? 1 : 2;
     const i64 line = P.prec + Q.qrec(k);
     const double *src = S.solve + line * (i64)recd_of(K);
-    const int cpl = ph == 1 ? o_l2(K) : ((ph == 0) == (Q.w2 == 0) ? o_l2(K) : o_u2(K));
-    const unsigned nc = ph < 2 ? (P.two ? 2u : 1u) : 0u;
+    // what the step reads: the in-plane coupling of its sweep (both for the twist line), the level-3
+    // coupling(s) of a lower-sweep / twist line, the block; the record orders them so that this is
+    // one range [lo, hi) (at most one unused coupling inside it)
+    const bool l2 = ph == 1 || ((ph == 0) == (Q.w2 == 0)), u2 = ph == 1 || !l2;
+    const bool l3 = ph < 2 && (P.two || P.c1 == o_l3(K)), u3 = ph < 2 && (P.two || P.c1 == o_u3(K));
+    const int lo = l2 ? o_l2(K) : l3 ? o_l3(K) : o_efb(K);
+    const int hi = u2 ? recd_of(K) : u3 ? o_u2(K) : o_u3(K);
     const bool extra = ph == 0 ? lower3 : ph == 1 ? true : !lower3;
     const double *xsrc = (lower3 ? S.b : S.x) + line * (i64)LR;
-    mbar_expect_tx(bar, bb + lb + nc * lb + (extra ? lb : 0u) + (ph == 1 ? lb : 0u));
-    tma_load_1d(dst, src, bb, bar);
-    tma_load_1d(dst + rs0_of(K), src + cpl, lb, bar);
-    if (nc) tma_load_1d(dst + rs1_of(K), src + P.c1, nc * lb, bar);
-    if (extra) tma_load_1d(dst + rx_of(K), xsrc, lb, bar);
-    if (ph == 1) tma_load_1d(dst + rs4_of(K), src + o_u2(K), lb, bar);
+    mbar_expect_tx_a(bar, (unsigned)(hi - lo) * 8u + (extra ? lb : 0u));
+    tma_load_a(dst + (unsigned)lo * 8u, src + lo, (unsigned)(hi - lo) * 8u, bar);
+    if (extra) tma_load_a(dst + rx_of(K) * 8u, xsrc, lb, bar);
 }
 
-template <int K, int D>
-__device__ void produce_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q, const Ring<K, D> &R, unsigned &rec)
+// records of planes idx0 .. idx1-1 of this warp's schedule (one level-3 phase)
+template <int K, int D, class DescF>
+__device__ void produce_range(const TsArrays &S, DescF &&desc, int idx0, int idx1, const Seq &Q, unsigned ring_a,
+                              unsigned bars_a, unsigned &rec)
 {
+    constexpr int NB = D >= 8 ? 4 : D >= 4 ? 2 : 1;  // records in flight per step: half the ring at most
+    constexpr unsigned SB = stage_of(K) * 8;
     const int lane = threadIdx.x & 31;
-    const int n = 2 * Q.cnt + 1;
-    if (lane == 0) {
-        for (int k = 0; k < n; k++, rec++) {
-            const unsigned st = rec % D;
-            if (rec >= (unsigned)D) mbar_wait_producer(&R.empty[st], ((rec / D) + 1) & 1);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            rec_copy<K>(S, P, Q, k, R.stage(st), &R.full[st]);
+    const int n = 2 * Q.cnt + 1, total = (idx1 - idx0) * n;
+    for (int g = 0; g < total; g += NB) {
+        const int my = g + lane;
+        if (lane < NB && my < total) {
+            const int pl = my / n, k = my - pl * n;
+            const PlaneDesc P = desc(idx0 + pl);
+            const unsigned r = rec + (unsigned)my, st = r % D;
+            // (no proxy fence: the solver only read the stage, and its release of the stage's
+            // empty barrier orders those reads before the copies issued after this wait)
+            if (r >= (unsigned)D) mbar_wait_a(bars_a + (D + st) * 8, ((r / D) + 1) & 1);
+            rec_copy<K>(S, P, Q, k, ring_a + st * SB, bars_a + st * 8);
         }
-    } else {
-        rec += n;
+        __syncwarp();
     }
-    __syncwarp();
+    rec += (unsigned)total;
 }
 
-__device__ __forceinline__ bool mbar_test(void *bar, unsigned parity)
+// ---- explicit accesses of the solver.  volatile: kept in program order among
+// themselves and with the mbarrier operations, so the next line's operands
+// are requested at chosen points of the current line's scans (the warp issues
+// in order: a load placed early delays the chain, placed late it stalls the
+// next line), and addressed with 32-bit shared addresses + immediates.
+__device__ __forceinline__ double lds(unsigned a)
+{
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double2 lds2(unsigned a)
+{
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts(unsigned a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v)); }
+__device__ __forceinline__ double ldg(const double *p)
+{
+    double v;
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void stg(double *p, double v) { asm volatile("st.global.f64 [%0], %1;" ::"l"(p), "d"(v)); }
+// a line of the plane buffer (shared address) or of a global plane; byte offsets
+__device__ __forceinline__ double ldb(unsigned a) { return lds(a); }
+__device__ __forceinline__ double ldb(double *p) { return ldg(p); }
+__device__ __forceinline__ void stb(unsigned a, double v) { sts(a, v); }
+__device__ __forceinline__ void stb(double *p, double v) { stg(p, v); }
+__device__ __forceinline__ unsigned adv(unsigned a, int bytes) { return a + bytes; }
+__device__ __forceinline__ double *adv(double *p, int bytes) { return (double *)((char *)p + bytes); }
+template <bool SMB>
+struct BufT {
+    typedef unsigned type;
+};
+template <>
+struct BufT<false> {
+    typedef double *type;
+};
+
+__device__ __forceinline__ void mbar_wait_a(unsigned bar, unsigned parity)
+{
+    unsigned ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ bool mbar_test_a(unsigned bar, unsigned parity)
 {
     unsigned ok;
     asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
                  : "=r"(ok)
-                 : "r"(smem_u32(bar)), "r"(parity)
+                 : "r"(bar), "r"(parity)
                  : "memory");
     return ok != 0;
 }
+// one lane releases a stage (barrier count 1): the warp's loads of the stage
+// precede it in program order, and a 32-lane arrive would serialise 32 atomics
+__device__ __forceinline__ void mbar_arrive_if(unsigned bar, bool on)
+{
+    asm volatile("{ .reg .pred p; setp.ne.u32 p, %1, 0; @p mbarrier.arrive.shared::cta.b64 _, [%0]; }" ::"r"(bar),
+                 "r"((unsigned)on)
+                 : "memory");
+}
 
-// Ring operands of one line step.  ld_* only issues the shared-memory loads;
-// the x-independent constants are formed after the current line's solve.
+// Operands of one line step.
 template <int K>
 struct Ops {
     double eF[K], eB[K], cp[K], pt[K];
-    double pr[NPREP];  // p2 p3 s1 s2 s3 e1 q2 q3 t1 t2 t3 f1
+    double pr[NPREP];  // m2 m4 m8 e n2 n4 n8 f
+};
+template <int K>
+struct Raw {  // x-independent inputs of a lower-sweep line: pt = bx - c1 n1 (- c2 n2)  or  c1 n1
+    double bx[K], c1[K], c2[K], n1[K], n2[K];
 };
 
 template <int K>
-__device__ __forceinline__ void ld_common(Ops<K> &o, const double *sg, int lane)
+__device__ __forceinline__ void ld_row(double (&v)[K], unsigned a)
 {
-    const double2 *efb = reinterpret_cast<const double2 *>(sg + o_efb(K));
+#pragma unroll
+    for (int k = 0; k < K; k++) v[k] = lds(a + k * 256);
+}
+template <int K, class BA>
+__device__ __forceinline__ void ld_buf(double (&v)[K], BA a)
+{
+#pragma unroll
+    for (int k = 0; k < K; k++) v[k] = ldb(adv(a, k * 256));
+}
+template <int K, class BA>
+__device__ __forceinline__ void st_buf(BA a, const double (&v)[K])
+{
+#pragma unroll
+    for (int k = 0; k < K; k++) stb(adv(a, k * 256), v[k]);
+}
+// sa16: stage address + lane * 16
+template <int K>
+__device__ __forceinline__ void ld_efb(Ops<K> &o, unsigned sa16)
+{
 #pragma unroll
     for (int k = 0; k < K; k++) {
-        const double2 v = efb[k * 32 + lane];
+        const double2 v = lds2(sa16 + o_efb(K) * 8 + k * 512);
         o.eF[k] = v.x;
         o.eB[k] = v.y;
     }
-    const double2 *pp = reinterpret_cast<const double2 *>(sg + o_prep(K));
+}
+template <int K>
+__device__ __forceinline__ void ld_prep(Ops<K> &o, unsigned sa16)
+{
 #pragma unroll
     for (int c = 0; c < NPREP / 2; c++) {
-        const double2 v = pp[c * 32 + lane];
+        const double2 v = lds2(sa16 + o_prep(K) * 8 + c * 512);
         o.pr[2 * c] = v.x;
         o.pr[2 * c + 1] = v.y;
     }
-    ld_rec(sg + rs0_of(K), lane, o.cp);
 }
 
-// One line: x = T^{-1} r for rho = mu r (SUB: x = y - T^{-1} r, y passed in x).
-template <int K, bool SUB>
-__device__ __forceinline__ void solve_line(const Ops<K> &o, int l, const double (&rho)[K], double (&x)[K])
+template <int A, int B, class F>
+__device__ __forceinline__ void static_for(F &&f)
 {
-    double pf[K], pb[K], pa[K], qa[K];
+    if constexpr (A < B) {
+        f(std::integral_constant<int, A>{});
+        static_for<A + 1, B>(f);
+    }
+}
+constexpr int NHOOK = 5;  // shuffle rounds of a line solve (4 levels + the exclusive level)
+
+// One line: x = T^{-1} r for rho = mu r (SUB: x = y - T^{-1} r, y passed in x).
+// hook(j), j = 0..4, runs right after the shuffles of round j are issued and
+// hook(5) once the carries are formed: the caller requests a share of the
+// next line's operands behind every round, so its loads fill the shuffle
+// latencies instead of queueing in front of the next round's shuffles (a
+// warp's shared-memory loads and shuffles go through the same in-order queue,
+// ~6 cycles each).
+template <int K, bool SUB, class FH>
+__device__ __forceinline__ void solve_line(const Ops<K> &o, int l, const double (&rho)[K], double (&x)[K], FH &&hook)
+{
+    double pf[K], pb[K], pa[K], qa[K], Rr[K];
     pf[0] = rho[0];
     pa[0] = o.eF[0];
     pb[K - 1] = rho[K - 1];
@@ -341,91 +448,208 @@ __device__ __forceinline__ void solve_line(const Ops<K> &o, int l, const double 
 #pragma unroll
     for (int k = 1; k < K; k++) {
         pf[k] = fma(o.eF[k], pf[k - 1], rho[k]);
-        pa[k] = o.eF[k] * pa[k - 1];
         pb[K - 1 - k] = fma(o.eB[K - 1 - k], pb[K - k], rho[K - 1 - k]);
+    }
+    double C = pf[K - 1], D = pb[0];
+    // Kogge-Stone levels at distances 1, 2, 4, 8 (ntd_line_ts.cuh), both directions interleaved
+    const double c1 = up(C, 1), d1 = dn(D, 1);
+    hook(std::integral_constant<int, 0>{});
+#pragma unroll
+    for (int k = 1; k < K; k++) {
+        pa[k] = o.eF[k] * pa[k - 1];
         qa[K - 1 - k] = o.eB[K - 1 - k] * qa[K - k];
     }
-    const double p1 = l >= 1 ? pa[K - 1] : 0.0, q1 = l <= 30 ? qa[0] : 0.0;
-    const double C0 = pf[K - 1], D0 = pb[0];
-    // level 1 (windows of 4 lanes)
-    const double c3 = up(C0, 3), d3 = dn(D0, 3), c2 = up(C0, 2), d2 = dn(D0, 2), c1 = up(C0, 1), d1 = dn(D0, 1);
-    const double C1 = fma(p1, c1, C0) + fma(o.pr[0], c2, o.pr[1] * c3);
-    const double D1 = fma(q1, d1, D0) + fma(o.pr[6], d2, o.pr[7] * d3);
-    // level 2 (windows of 16 lanes)
-    const double c12 = up(C1, 12), d12 = dn(D1, 12), c8 = up(C1, 8), d8 = dn(D1, 8), c4 = up(C1, 4), d4 = dn(D1, 4);
-    const double C2 = fma(o.pr[2], c4, C1) + fma(o.pr[3], c8, o.pr[4] * c12);
-    const double D2 = fma(o.pr[8], d4, D1) + fma(o.pr[9], d8, o.pr[10] * d12);
-    // level 3: exclusive carries
-    const double u17 = up(C2, 17), v17 = dn(D2, 17), u1 = up(C2, 1), v1 = dn(D2, 1);
-    const double cF = fma(o.pr[5], u17, l >= 1 ? u1 : 0.0);
-    const double cB = fma(o.pr[11], v17, l <= 30 ? v1 : 0.0);
+#pragma unroll
+    for (int k = 0; k < K; k++) Rr[k] = k < K - 1 ? fma(o.eB[k], pb[k + 1 < K ? k + 1 : k], pf[k]) : pf[k];
+    const double m1 = l >= 1 ? pa[K - 1] : 0.0, n1 = l <= 30 ? qa[0] : 0.0;
+    C = fma(m1, c1, C);
+    D = fma(n1, d1, D);
+    const double c2 = up(C, 2), d2 = dn(D, 2);
+    hook(std::integral_constant<int, 1>{});
+    C = fma(o.pr[0], c2, C);
+    D = fma(o.pr[4], d2, D);
+    const double c4 = up(C, 4), d4 = dn(D, 4);
+    hook(std::integral_constant<int, 2>{});
+    C = fma(o.pr[1], c4, C);
+    D = fma(o.pr[5], d4, D);
+    const double c8 = up(C, 8), d8 = dn(D, 8);
+    hook(std::integral_constant<int, 3>{});
+    C = fma(o.pr[2], c8, C);
+    D = fma(o.pr[6], d8, D);
+    // exclusive carries
+    const double u17 = up(C, 17), v17 = dn(D, 17), u1 = up(C, 1), v1 = dn(D, 1);
+    hook(std::integral_constant<int, 4>{});
+    const double cF = fma(o.pr[3], u17, l >= 1 ? u1 : 0.0);
+    const double cB = fma(o.pr[7], v17, l <= 30 ? v1 : 0.0);
+    hook(std::integral_constant<int, 5>{});
 #pragma unroll
     for (int k = 0; k < K; k++) {
-        const double R = k < K - 1 ? fma(o.eB[k], pb[k + 1 < K ? k + 1 : k], pf[k]) : pf[k];
         if (SUB)
-            x[k] = fma(-pa[k], cF, fma(-qa[k], cB, x[k] - R));
+            x[k] = fma(-pa[k], cF, fma(-qa[k], cB, x[k] - Rr[k]));
         else
-            x[k] = fma(pa[k], cF, fma(qa[k], cB, R));
+            x[k] = fma(pa[k], cF, fma(qa[k], cB, Rr[k]));
     }
 }
 
 // ---------------- solver: one plane
-// SMB: the warp keeps its half of the plane it processed last in shared
-// memory (pbuf, lines lo_line.. of the half incl. the twist line): each line
-// slot holds the neighbour plane's final x until this plane's lower sweep
-// replaces it with the lower-sweep value, which the upper sweep replaces with
-// this plane's final x.  The solver then issues no global loads per line.
+// Plane buffer (SMB): the warp keeps its half of the plane it processed last
+// in shared memory (lines lo_line.. of the half incl. the twist line): each
+// line slot holds the neighbour plane's final x until this plane's lower
+// sweep replaces it with the lower-sweep value, which the upper sweep
+// replaces with this plane's final x.  Without it (wide or tall planes) the
+// same lines are read from / written to the global planes.
+//
+// A plane is 2 cnt + 1 records (lower lines, twist line, upper lines); step r
+// solves record r while the operands of record r+1 are loaded (hooks of
+// solve_line), so the serial chain per line is rho = pt - cp' xprev and the
+// scans.  full(r+2) is tested during step r and the result consumed in step
+// r+1 (an mbarrier test has a long latency: never wait on it in place).
 template <int K, int D, int MODE, bool TWO, bool SMB>
-__device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q, int bar_id, double *ex, int &parity,
-                            const Ring<K, D> &R, unsigned &rec, double *pbuf)
+__device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q, int bar_id, unsigned ex_a, int &parity,
+                            unsigned ring_a, unsigned bars_a, unsigned &rec, unsigned pbuf_a)
 {
-    constexpr int LR = lr_of(K);
+    typedef typename BufT<SMB>::type BA;
+    constexpr int LR = lr_of(K), LB = LR * 8;
+    constexpr unsigned SB = stage_of(K) * 8;
+    constexpr bool lower3 = MODE == M_LOWER3;
     const int lane = threadIdx.x & 31, w2 = Q.w2;
     const int ny = Q.ny, t2 = Q.t2, cnt = Q.cnt;
+    const unsigned l8 = lane * 8, l16 = lane * 16;
     const i64 plr = (i64)ny * LR;  // plane stride in TS
-    constexpr bool lower3 = MODE == M_LOWER3;
-    constexpr bool PIPE = K <= 5;
-    // Plane bases (line q of a plane at base + q*LR).  A missing level-3
-    // neighbour (first/last plane) has an exactly-zero coupling; it reads the
-    // zero plane instead of branching.
-    double *xpl = S.x + P.prec * LR;
-    const double *y1, *y2 = S.zero;
+    // Plane bases (line q of a plane at base + q*LR), this lane's column.  A
+    // missing level-3 neighbour (first/last plane) has an exactly-zero
+    // coupling; it reads the zero plane instead of branching.
+    double *xpl = S.x + P.prec * LR + lane;
+    const double *y1, *y2 = S.zero + lane;
     if (lower3) {
         if (TWO) {
-            y1 = P.hasM ? xpl - plr : S.zero;
-            y2 = P.hasP ? xpl + plr : S.zero;
+            y1 = P.hasM ? xpl - plr : S.zero + lane;
+            y2 = P.hasP ? xpl + plr : S.zero + lane;
         } else if (P.up) {
-            y1 = P.hasP ? xpl + plr : S.zero;
+            y1 = P.hasP ? xpl + plr : S.zero + lane;
         } else {
-            y1 = P.hasM ? xpl - plr : S.zero;
+            y1 = P.hasM ? xpl - plr : S.zero + lane;
         }
     } else {
         y1 = P.nbrUp ? xpl + plr : xpl - plr;
     }
-    double *xlow = (lower3 ? S.x : S.xs) + P.prec * LR;  // lower-sweep store of this plane
+    // line q of this plane's own values (xl) and of the level-3 neighbour (yn)
+    BA xl, yn;
+    const int q0 = cnt == 0 ? t2 : (w2 == 0 ? 0 : ny - 1), dq = w2 == 0 ? 1 : -1;
     if constexpr (SMB) {
-        double *bq = pbuf - (i64)(w2 == 0 ? 0 : t2) * LR;  // line q of this half at bq + q*LR
-        xlow = bq;
-        if (P.nbuf) y1 = bq;
+        const unsigned bq = pbuf_a - (unsigned)((w2 == 0 ? 0 : t2) * LB) + l8;  // line q at bq + q*LB
+        if (!P.nbuf) {  // prime the buffer with the neighbour plane (a sweep's first plane)
+            constexpr int CH = K <= 4 ? 8 : 2;  // lines in flight
+            const int qa_ = w2 == 0 ? 0 : t2, qb_ = w2 == 0 ? t2 : ny - 1;
+            for (int q = qa_; q <= qb_; q += CH) {
+                double v[CH][K];
+#pragma unroll
+                for (int j = 0; j < CH; j++)
+#pragma unroll
+                    for (int k = 0; k < K; k++) v[j][k] = ldg(y1 + (i64)(q + j <= qb_ ? q + j : qb_) * LR + k * 32);
+#pragma unroll
+                for (int j = 0; j < CH; j++)
+#pragma unroll
+                    for (int k = 0; k < K; k++) sts(bq + (q + j <= qb_ ? q + j : qb_) * LB + k * 256, v[j][k]);
+            }
+        }
+        xl = yn = bq + q0 * LB;
+    } else {
+        xl = (lower3 ? S.x : S.xs) + P.prec * LR + lane + (i64)q0 * LR;
+        yn = const_cast<double *>(y1) + (i64)q0 * LR;
     }
-    auto full = [&](unsigned r) { return &R.full[r % D]; };
+    const double *y2p = y2 + (i64)q0 * LR;
+    const int dqB = dq * LB;
+    auto sa = [&](unsigned r) { return ring_a + (r % D) * SB; };
+    auto full = [&](unsigned r) { return bars_a + (r % D) * 8; };
+    auto empty = [&](unsigned r) { return bars_a + (D + r % D) * 8; };
     auto par = [&](unsigned r) { return (r / D) & 1u; };
-    // raw operands of a lower-sweep line, and its x-independent constants
-    //   LOWER3: pt = b' - C1' y1 (- C2' y2);  UPPER3: pt = C1' y1
-    struct Raw {
-        double bx[K], c1[K], c2[K], n1[K], n2[K];
-    };
-    auto ld_lower = [&](Ops<K> &o, Raw &w, const double *sg, int q) {
-        ld_common(o, sg, lane);
-        if (lower3) ld_rec(sg + rx_of(K), lane, w.bx);
-        ld_rec(sg + rs1_of(K), lane, w.c1);
-        ld_rec(y1 + q * LR, lane, w.n1);
-        if (TWO) {
-            ld_rec(sg + rs2_of(K), lane, w.c2);
-            ld_rec(y2 + q * LR, lane, w.n2);
+    // in-plane coupling of the lower sweep (and of the twist line's first neighbour) / of the upper sweep
+    const unsigned cpL = (unsigned)(w2 == 0 || cnt == 0 ? o_l2(K) : o_u2(K)) * 8 + l8;
+    const unsigned cpU = (unsigned)(w2 == 0 ? o_u2(K) : o_l2(K)) * 8 + l8;
+    const unsigned c1o = (unsigned)P.c1 * 8 + l8;
+    // The operand loads of a record as a list of NL_L / NL_U single loads; share j of NHOOK is issued
+    // behind shuffle round j of the line being solved (share = -1: all of them).
+    //   lower-type record: c1, n1, [bx], [c2, n2], cp, eF|eB pairs, scan coefficient pairs
+    //   upper-type record: cp, y, [xo], eF|eB pairs, scan coefficient pairs
+    constexpr int NL_L = K * (4 + (lower3 ? 1 : 0) + (TWO ? 2 : 0)) + NPREP / 2;
+    constexpr int NL_U = K * (3 + (lower3 ? 0 : 1)) + NPREP / 2;
+    // (WN = false: without the neighbour-plane / lower-sweep values, which the wide-line mode requests
+    // one line ahead through nbr_L / nbr_U)
+    auto item_L = [&](auto I, auto WN, Ops<K> &o, Raw<K> &w, unsigned s, BA ya, const double *y2q, unsigned cpo) {
+        constexpr int i = decltype(I)::value;
+        constexpr bool wn = decltype(WN)::value;
+        constexpr int nb = lower3 ? 1 : 0, nt = TWO ? 2 : 0;
+        if constexpr (i < K) {
+            w.c1[i] = lds(s + c1o + i * 256);
+        } else if constexpr (i < 2 * K) {
+            if constexpr (wn) w.n1[i - K] = ldb(adv(ya, (i - K) * 256));
+        } else if constexpr (i < (2 + nb) * K) {
+            w.bx[i - 2 * K] = lds(s + rx_of(K) * 8 + l8 + (i - 2 * K) * 256);
+        } else if constexpr (i < (2 + nb + nt) * K) {
+            constexpr int j = i - (2 + nb) * K;
+            if constexpr (j < K)
+                w.c2[j] = lds(s + o_u3(K) * 8 + l8 + j * 256);
+            else if constexpr (wn)
+                w.n2[j - K] = ldg(y2q + (j - K) * 32);
+        } else if constexpr (i < (3 + nb + nt) * K) {
+            constexpr int j = i - (2 + nb + nt) * K;
+            o.cp[j] = lds(s + cpo + j * 256);
+        } else if constexpr (i < (4 + nb + nt) * K) {
+            constexpr int j = i - (3 + nb + nt) * K;
+            const double2 v = lds2(s + l16 + o_efb(K) * 8 + j * 512);
+            o.eF[j] = v.x;
+            o.eB[j] = v.y;
+        } else {
+            constexpr int j = i - (4 + nb + nt) * K;
+            const double2 v = lds2(s + l16 + o_prep(K) * 8 + j * 512);
+            o.pr[2 * j] = v.x;
+            o.pr[2 * j + 1] = v.y;
         }
     };
-    auto fin_lower = [&](Ops<K> &o, const Raw &w) {
+    auto item_U = [&](auto I, auto WN, Ops<K> &o, double (&y)[K], double (&xo)[K], unsigned s, BA ya) {
+        constexpr int i = decltype(I)::value;
+        constexpr bool wn = decltype(WN)::value;
+        constexpr int nx_ = lower3 ? 0 : 1;
+        if constexpr (i < K) {
+            o.cp[i] = lds(s + cpU + i * 256);
+        } else if constexpr (i < 2 * K) {
+            if constexpr (wn) y[i - K] = ldb(adv(ya, (i - K) * 256));
+        } else if constexpr (i < (2 + nx_) * K) {
+            xo[i - 2 * K] = lds(s + rx_of(K) * 8 + l8 + (i - 2 * K) * 256);
+        } else if constexpr (i < (3 + nx_) * K) {
+            constexpr int j = i - (2 + nx_) * K;
+            const double2 v = lds2(s + l16 + o_efb(K) * 8 + j * 512);
+            o.eF[j] = v.x;
+            o.eB[j] = v.y;
+        } else {
+            constexpr int j = i - (3 + nx_) * K;
+            const double2 v = lds2(s + l16 + o_prep(K) * 8 + j * 512);
+            o.pr[2 * j] = v.x;
+            o.pr[2 * j + 1] = v.y;
+        }
+    };
+    const std::integral_constant<bool, true> WITH_N{};
+    const std::integral_constant<bool, false> NO_N{};
+    auto load_L = [&](auto J, auto WN, Ops<K> &o, Raw<K> &w, unsigned s, BA ya, const double *y2q, unsigned cpo) {
+        constexpr int j = decltype(J)::value;
+        constexpr int a = j < 0 ? 0 : j * NL_L / NHOOK, b = j < 0 ? NL_L : (j + 1) * NL_L / NHOOK;
+        static_for<a, b>([&](auto I) { item_L(I, WN, o, w, s, ya, y2q, cpo); });
+    };
+    auto load_U = [&](auto J, auto WN, Ops<K> &o, double (&y)[K], double (&xo)[K], unsigned s, BA ya) {
+        constexpr int j = decltype(J)::value;
+        constexpr int a = j < 0 ? 0 : j * NL_U / NHOOK, b = j < 0 ? NL_U : (j + 1) * NL_U / NHOOK;
+        static_for<a, b>([&](auto I) { item_U(I, WN, o, y, xo, s, ya); });
+    };
+    auto nbr_L = [&](Raw<K> &w, BA ya, const double *y2q) {
+        ld_buf(w.n1, ya);
+        if (TWO) {
+#pragma unroll
+            for (int k = 0; k < K; k++) w.n2[k] = ldg(y2q + k * 32);
+        }
+    };
+    const std::integral_constant<int, -1> ALL{};
+    auto fin_L = [&](Ops<K> &o, const Raw<K> &w) {
 #pragma unroll
         for (int k = 0; k < K; k++) {
             double v = lower3 ? fma(-w.c1[k], w.n1[k], w.bx[k]) : w.c1[k] * w.n1[k];
@@ -433,136 +657,171 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
             o.pt[k] = v;
         }
     };
+    // PIPE (narrow lines): step r solves record r while the operands of record r+1 are loaded behind
+    // its shuffle rounds.  Wide lines (K > 5) do not have the registers for two operand sets: a step
+    // loads its own record first, and only the neighbour-plane / lower-sweep values, which may come
+    // from global memory, are requested one line ahead.
+    constexpr bool PIPE = K <= 5;
+    const unsigned cpT = (unsigned)o_l2(K) * 8 + l8;  // the twist record is read with L2' as cp
+    Ops<K> cur;
+    Raw<K> wn;  // wide lines: neighbour values of the next lower-type record
+    bool okn = true;
+    // ---------------- prologue: the plane's first record (a lower line, or the twist line when cnt == 0)
+    if constexpr (PIPE) {
+        Raw<K> w;
+        mbar_wait_a(full(rec), par(rec));
+        load_L(ALL, WITH_N, cur, w, sa(rec), yn, y2p, cpL);
+        mbar_arrive_if(empty(rec), lane == 0 && cnt > 0);  // the twist record releases itself
+        okn = mbar_test_a(full(rec + 1), par(rec + 1));
+        fin_L(cur, w);
+    } else {
+        nbr_L(wn, yn, y2p);
+    }
+    // ---------------- level-2 lower sweep (ntd_solve.py:147-171)
     double xprev[K];
 #pragma unroll
     for (int k = 0; k < K; k++) xprev[k] = 0.0;
-    // ---------------- level-2 lower sweep (ntd_solve.py:147-171)
-    // Software-pipelined (PIPE): the operands of line i+1 are loaded while
-    // line i solves, so the serial chain per line is rho = pt - cp' xprev and
-    // the scans.  The full barrier of record i+2 is tested at the top of step
-    // i and the result consumed after the solve.
-    Ops<K> cur;
-    if (PIPE && cnt > 0) {
-        Raw w;
-        mbar_wait(full(rec), par(rec));
-        ld_lower(cur, w, R.stage(rec % D), Q.qlow(0));
-        fin_lower(cur, w);
-        if (cnt > 1) mbar_wait(full(rec + 1), par(rec + 1));
-    }
-#pragma unroll 2  // ping-pong registers: no copies of in-flight loads
+#pragma unroll 1
     for (int i = 0; i < cnt; i++, rec++) {
-        const unsigned st = rec % D;
-        Ops<K> nxo;
-        Raw w;
-        bool ok2 = true;
-        if (PIPE) {
-            if (i + 2 < cnt) ok2 = mbar_test(full(rec + 2), par(rec + 2));
-            ld_lower(nxo, w, R.stage((rec + 1) % D), Q.qlow(i + 1 < cnt ? i + 1 : i));  // unused past the sweep
-        } else {
-            mbar_wait(full(rec), par(rec));
-            ld_lower(cur, w, R.stage(st), Q.qlow(i));
-            fin_lower(cur, w);
+        Ops<K> nxt;
+        Raw<K> w;
+        const bool last = i == cnt - 1;  // the next record is the twist line (an L-type record as well)
+        if constexpr (!PIPE) {
+            mbar_wait_a(full(rec), par(rec));
+            load_L(ALL, NO_N, cur, wn, sa(rec), yn, y2p, cpL);
+            mbar_arrive_if(empty(rec), lane == 0);
+            fin_L(cur, wn);
         }
         double rho[K], x[K];
 #pragma unroll
         for (int k = 0; k < K; k++) rho[k] = fma(-cur.cp[k], xprev[k], cur.pt[k]);  // line 0: xprev = 0
-        solve_line<K, false>(cur, lane, rho, x);
-        mbar_arrive(&R.empty[st]);  // every operand of stage st has been consumed
-        st_rec(xlow + Q.qlow(i) * LR, lane, x);
+        solve_line<K, false>(cur, lane, rho, x, [&](auto J) {
+            constexpr int j = decltype(J)::value;
+            if constexpr (!PIPE) {
+                if constexpr (j == 0) nbr_L(wn, adv(yn, dqB), y2p + dq * LR);
+            } else if constexpr (j < NHOOK) {
+                if (j == 0 && !okn) mbar_wait_a(full(rec + 1), par(rec + 1));
+                load_L(J, WITH_N, nxt, w, sa(rec + 1), adv(yn, dqB), y2p + dq * LR, last ? cpT : cpL);
+            } else {
+                mbar_arrive_if(empty(rec + 1), lane == 0 && !last);
+                okn = mbar_test_a(full(rec + 2), par(rec + 2));
+            }
+        });
+        st_buf(xl, x);
 #pragma unroll
         for (int k = 0; k < K; k++) xprev[k] = x[k];
-        if (PIPE) {
-            fin_lower(nxo, w);
-            if (i + 2 < cnt && !ok2) mbar_wait(full(rec + 2), par(rec + 2));
-            cur = nxo;
+        if constexpr (PIPE) {
+            fin_L(nxt, w);
+            cur = nxt;
         }
+        xl = adv(xl, dqB);
+        yn = adv(yn, dqB);
+        y2p += dq * LR;
     }
     // ---------------- exchange the lines next to the twist
-    double *mine = ex + (parity * 2 + w2) * LR;
-    const double *other = ex + (parity * 2 + (1 - w2)) * LR;
-    st_rec(mine, lane, xprev);
+    const unsigned mine = ex_a + (unsigned)((parity * 2 + w2) * LB) + l8;
+    const unsigned other = ex_a + (unsigned)((parity * 2 + (1 - w2)) * LB) + l8;
+#pragma unroll
+    for (int k = 0; k < K; k++) sts(mine + k * 256, xprev[k]);
     named_bar(bar_id, 64);
     parity ^= 1;
     double xo_[K];
-    ld_rec(other, lane, xo_);
-    // ---------------- twist line (ntd_solve.py:172-177): its record follows the lower-sweep records
+    ld_row(xo_, other);
+    // ---------------- twist line (ntd_solve.py:172-177); xl / yn are at line t2
     double xn[K];
+    Ops<K> nxt;
+    double ycur[K], xocur[K];
     {
-        Ops<K> tw;
-        Raw w;
         double u2c[K], xo[K];
-        const unsigned st = rec % D;
-        const double *sg = R.stage(st);
-        mbar_wait(full(rec), par(rec));
-        ld_lower(tw, w, sg, t2);
-        ld_rec(sg + rs4_of(K), lane, u2c);
-        if (!lower3) ld_rec(sg + rx_of(K), lane, xo);
-        fin_lower(tw, w);
+        if constexpr (!PIPE) {
+            mbar_wait_a(full(rec), par(rec));
+            load_L(ALL, NO_N, cur, wn, sa(rec), yn, y2p, cpT);
+            fin_L(cur, wn);
+        }
+        ld_row(u2c, sa(rec) + o_u2(K) * 8 + l8);
+        if (!lower3) ld_row(xo, sa(rec) + rx_of(K) * 8 + l8);
+        mbar_arrive_if(empty(rec), lane == 0);
         double rho[K];
 #pragma unroll
         for (int k = 0; k < K; k++) {
             const double xa = w2 == 0 ? xprev[k] : xo_[k], xd = w2 == 0 ? xo_[k] : xprev[k];
-            double v = tw.pt[k];
-            if (t2 > 0) v = fma(-tw.cp[k], xa, v);
+            double v = cur.pt[k];
+            if (t2 > 0) v = fma(-cur.cp[k], xa, v);
             if (t2 < ny - 1) v = fma(-u2c[k], xd, v);
             rho[k] = v;
         }
-        solve_line<K, false>(tw, lane, rho, xn);
+        solve_line<K, false>(cur, lane, rho, xn, [&](auto J) {
+            constexpr int j = decltype(J)::value;
+            if (cnt > 0) {
+                if constexpr (!PIPE) {
+                    if constexpr (j == 0) ld_buf(ycur, adv(xl, -dqB));
+                } else if constexpr (j < NHOOK) {
+                    if (j == 0 && !okn) mbar_wait_a(full(rec + 1), par(rec + 1));
+                    load_U(J, WITH_N, nxt, ycur, xocur, sa(rec + 1), adv(xl, -dqB));
+                } else {
+                    mbar_arrive_if(empty(rec + 1), lane == 0);
+                    okn = mbar_test_a(full(rec + 2), par(rec + 2));
+                }
+            }
+        });
         double nv[K];
 #pragma unroll
         for (int k = 0; k < K; k++) nv[k] = lower3 ? xn[k] : xo[k] - xn[k];  // UPPER3: final = xo - value
-        mbar_arrive(&R.empty[st]);
         rec++;
-        if (w2 == 0) st_rec(xpl + t2 * LR, lane, nv);
-        if constexpr (SMB) st_rec(xlow + t2 * LR, lane, nv);  // both warps keep the twist line
+        if (w2 == 0) {
+#pragma unroll
+            for (int k = 0; k < K; k++) stg(xpl + (i64)t2 * LR + k * 32, nv[k]);
+        }
+        if constexpr (SMB) st_buf(xl, nv);  // both warps keep the twist line
     }
     // ---------------- level-2 upper sweep (ntd_solve.py:178-185)
     //   value_q = y_q - T_q^{-1}(cp' value_prev);  LOWER3: x_q = value_q;  UPPER3: x_q = xo_q - value_q
-    auto ld_upper = [&](Ops<K> &o, double (&y)[K], double (&xo)[K], const double *sg, int q) {
-        ld_common(o, sg, lane);
-        ld_rec(xlow + q * LR, lane, y);
-        if (!lower3) ld_rec(sg + rx_of(K), lane, xo);
-    };
-    double ycur[K], xocur[K];
-    if (PIPE && cnt > 0) {
-        mbar_wait(full(rec), par(rec));
-        ld_upper(cur, ycur, xocur, R.stage(rec % D), Q.qup(0));
-        if (cnt > 1) mbar_wait(full(rec + 1), par(rec + 1));
-    }
-#pragma unroll 2
+    if constexpr (PIPE) cur = nxt;
+    BA xu = adv(xl, -dqB);
+    double *xg = xpl + (i64)(t2 - dq) * LR;
+#pragma unroll 1
     for (int i = 0; i < cnt; i++, rec++) {
-        const unsigned st = rec % D;
-        Ops<K> nxo;
+        const bool more = i + 1 < cnt;
         double ynx[K], xonx[K];
-        bool ok2 = true;
-        if (PIPE) {
-            if (i + 2 < cnt) ok2 = mbar_test(full(rec + 2), par(rec + 2));
-            ld_upper(nxo, ynx, xonx, R.stage((rec + 1) % D), Q.qup(i + 1 < cnt ? i + 1 : i));
-        } else {
-            mbar_wait(full(rec), par(rec));
-            ld_upper(cur, ycur, xocur, R.stage(st), Q.qup(i));
+        if constexpr (!PIPE) {
+            double dummy[K];
+            mbar_wait_a(full(rec), par(rec));
+            load_U(ALL, NO_N, cur, dummy, xocur, sa(rec), xu);
+            mbar_arrive_if(empty(rec), lane == 0);
         }
         double rho[K];
 #pragma unroll
         for (int k = 0; k < K; k++) rho[k] = cur.cp[k] * xn[k];
 #pragma unroll
         for (int k = 0; k < K; k++) xn[k] = ycur[k];
-        solve_line<K, true>(cur, lane, rho, xn);
+        // past the sweep's last line the loads read stale ring / buffer data that is never used
+        solve_line<K, true>(cur, lane, rho, xn, [&](auto J) {
+            constexpr int j = decltype(J)::value;
+            if constexpr (!PIPE) {
+                if constexpr (j == 0) ld_buf(ynx, adv(xu, -dqB));
+            } else if constexpr (j < NHOOK) {
+                if (j == 0 && more && !okn) mbar_wait_a(full(rec + 1), par(rec + 1));
+                load_U(J, WITH_N, nxt, ynx, xonx, sa(rec + 1), adv(xu, -dqB));
+            } else {
+                mbar_arrive_if(empty(rec + 1), lane == 0 && more);
+                okn = mbar_test_a(full(rec + 2), par(rec + 2));
+            }
+        });
         double nv[K];
 #pragma unroll
         for (int k = 0; k < K; k++) nv[k] = lower3 ? xn[k] : xocur[k] - xn[k];
-        mbar_arrive(&R.empty[st]);
-        st_rec(xpl + Q.qup(i) * LR, lane, nv);
-        if constexpr (SMB) st_rec(xlow + Q.qup(i) * LR, lane, nv);  // (xlow is the buffer)
-        if (PIPE) {
-            if (i + 2 < cnt && !ok2) mbar_wait(full(rec + 2), par(rec + 2));
-            cur = nxo;
 #pragma unroll
-            for (int k = 0; k < K; k++) {
-                ycur[k] = ynx[k];
-                xocur[k] = xonx[k];
-            }
+        for (int k = 0; k < K; k++) stg(xg + k * 32, nv[k]);
+        if constexpr (SMB) st_buf(xu, nv);
+#pragma unroll
+        for (int k = 0; k < K; k++) ycur[k] = ynx[k];
+        if constexpr (PIPE) {
+            cur = nxt;
+#pragma unroll
+            for (int k = 0; k < K; k++) xocur[k] = xonx[k];
         }
+        xu = adv(xu, -dqB);
+        xg -= dq * LR;
     }
 }
 
@@ -609,7 +868,7 @@ __global__ void __launch_bounds__(128 * NP, 1) k_apply(const double *__restrict_
     if (!producer && lane == 0) {
         for (int st = 0; st < D; st++) {
             mbar_init(&R.full[st], 1);
-            mbar_init(&R.empty[st], 32);  // every solver lane arrives: no divergent branch
+            mbar_init(&R.empty[st], 1);  // released by lane 0 of the solver warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -626,7 +885,8 @@ __global__ void __launch_bounds__(128 * NP, 1) k_apply(const double *__restrict_
     Q.w2 = w2;
     Q.cnt = w2 == 0 ? Q.t2 : (ny - 1 - Q.t2);
     unsigned rec = 0;
-    double *myex = ex[NP == 2 ? pair : 0];
+    const unsigned ex_a = smem_u32(ex[NP == 2 ? pair : 0]);
+    const unsigned ring_a = smem_u32(R.base), bars_a = smem_u32(bars[sw]), pbuf_a = smem_u32(pbuf);
     int parity = 0;
     const int t3 = (nz - 1) / 2;
     // The warp pair's plane schedule: level-3 lower sweep (ntd_solve.py:198-221),
@@ -667,28 +927,28 @@ __global__ void __launch_bounds__(128 * NP, 1) k_apply(const double *__restrict_
         return P;
     };
     const int nplanes = 2 * nlow + ntw;
-    for (int i = 0; i < nlow; i++) {
-        if (producer)
-            produce_plane<K, D>(S, desc(i), Q, R, rec);
-        else
-            solve_plane<K, D, M_LOWER3, false, SMB>(S, desc(i), Q, bar, myex, parity, R, rec, pbuf);
+    if (producer) {
+        produce_range<K, D>(S, desc, 0, nlow, Q, ring_a, bars_a, rec);
+    } else {
+        for (int i = 0; i < nlow; i++)
+            solve_plane<K, D, M_LOWER3, false, SMB>(S, desc(i), Q, bar, ex_a, parity, ring_a, bars_a, rec, pbuf_a);
     }
     phase_sync();
     if (pair == 0) {
         if (producer) {
             fence_proxy_async();
-            produce_plane<K, D>(S, desc(nlow), Q, R, rec);
+            produce_range<K, D>(S, desc, nlow, nlow + 1, Q, ring_a, bars_a, rec);
         } else {
-            solve_plane<K, D, M_LOWER3, true, SMB>(S, desc(nlow), Q, bar, myex, parity, R, rec, pbuf);
+            solve_plane<K, D, M_LOWER3, true, SMB>(S, desc(nlow), Q, bar, ex_a, parity, ring_a, bars_a, rec, pbuf_a);
         }
     }
     phase_sync();
-    if (producer) fence_proxy_async();  // x (read as xo) was written by generic stores
-    for (int i = nlow + ntw; i < nplanes; i++) {
-        if (producer)
-            produce_plane<K, D>(S, desc(i), Q, R, rec);
-        else
-            solve_plane<K, D, M_UPPER3, false, SMB>(S, desc(i), Q, bar, myex, parity, R, rec, pbuf);
+    if (producer) {
+        fence_proxy_async();  // x (read as xo) was written by generic stores
+        produce_range<K, D>(S, desc, nlow + ntw, nplanes, Q, ring_a, bars_a, rec);
+    } else {
+        for (int i = nlow + ntw; i < nplanes; i++)
+            solve_plane<K, D, M_UPPER3, false, SMB>(S, desc(i), Q, bar, ex_a, parity, ring_a, bars_a, rec, pbuf_a);
     }
 }
 
@@ -704,7 +964,8 @@ template <int K, int D, bool SMB>
 int launch_apply_ts_cluster(const double *solve, const double *bsl, double *xsl, double *xssl, const double *zpl,
                             int nx, int ny, int nz, i64 batch, const int32_t *active, cudaStream_t st, int bl)
 {
-    const size_t smem = (size_t)2 * D * ts::stage_of(K) * 8 + (SMB ? (size_t)2 * bl * ts::lr_of(K) * 8 : 0);
+    // (+ one pad line: the last upper-sweep step requests a line past its buffer)
+    const size_t smem = (size_t)2 * D * ts::stage_of(K) * 8 + (SMB ? (size_t)(2 * bl + 1) * ts::lr_of(K) * 8 : 0);
     cudaError_t e = cudaFuncSetAttribute(ts::k_apply<K, D, 1, SMB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) {

@@ -19,47 +19,52 @@
 //     x_j  = f'_j + g'_j - rho_j
 // Lane l owns K consecutive cells.  Per lane the chains are composed as prefix
 // maps (slot k: f'_k = pa_k cF + pf_k), the lane maps are scanned over the 32
-// lanes in three sliding-window levels (4, 4, 2) whose multiplicative
-// coefficients depend only on the factor (PrepTS, prepared at setup), and
-// each slot is finished with two FMAs once the carries arrive.
+// lanes (line_prep below) with multiplicative coefficients that depend only
+// on the factor (PrepTS, prepared at setup), and each slot is finished with
+// two FMAs once the carries arrive.
 #pragma once
 #include "common.cuh"
 
 struct PrepTS {
-    double p1, p2, p3;  // forward level 1 (lanes l-1, l-2, l-3)
-    double s1, s2, s3;  // forward level 2 (lanes l-4, l-8, l-12)
-    double e1;          // forward level 3, exclusive (lane l-17)
-    double q1, q2, q3;  // backward level 1 (lanes l+1, l+2, l+3)
-    double t1, t2, t3;  // backward level 2 (lanes l+4, l+8, l+12)
-    double f1;          // backward level 3, exclusive (lane l+17)
+    double m1, m2, m4, m8, e;  // forward: window multipliers of levels 1, 2, 4, 8 and the exclusive level (lane l-17)
+    double n1, n2, n4, n8, f;  // backward
 };
 
 namespace ts {
 
-__device__ __forceinline__ double up(double v, int d) { return __shfl_up_sync(FULL_MASK, v, d); }
-__device__ __forceinline__ double dn(double v, int d) { return __shfl_down_sync(FULL_MASK, v, d); }
-
-// Ordered shuffles for the solve: volatile asm statements keep their program
-// order, so the forward and backward scans stay interleaved level by level
-// (the warp issues in order; ptxas otherwise runs one scan after the other).
-__device__ __forceinline__ double vup(double v, int d)
+// 64-bit shuffles, low half first: ptxas numbers the two result registers in
+// issue order, and (low, high) in that order is an aligned register pair the
+// following DFMA reads directly (the toolkit's double overload shuffles the
+// high half first and costs two MOVs per shuffle in this kernel).
+__device__ __forceinline__ double up(double v, int d)
 {
-    int lo = __double2loint(v), hi = __double2hiint(v);
-    asm volatile("shfl.sync.up.b32 %0, %0, %2, 0, 0xffffffff;\n\tshfl.sync.up.b32 %1, %1, %2, 0, 0xffffffff;"
-                 : "+r"(lo), "+r"(hi)
-                 : "r"(d));
-    return __hiloint2double(hi, lo);
+    int lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(v));
+    lo = __shfl_up_sync(FULL_MASK, lo, d);
+    hi = __shfl_up_sync(FULL_MASK, hi, d);
+    double r;
+    asm("mov.b64 %0, {%1, %2};" : "=d"(r) : "r"(lo), "r"(hi));
+    return r;
 }
-__device__ __forceinline__ double vdn(double v, int d)
+__device__ __forceinline__ double dn(double v, int d)
 {
-    int lo = __double2loint(v), hi = __double2hiint(v);
-    asm volatile("shfl.sync.down.b32 %0, %0, %2, 0x1f, 0xffffffff;\n\tshfl.sync.down.b32 %1, %1, %2, 0x1f, 0xffffffff;"
-                 : "+r"(lo), "+r"(hi)
-                 : "r"(d));
-    return __hiloint2double(hi, lo);
+    int lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(v));
+    lo = __shfl_down_sync(FULL_MASK, lo, d);
+    hi = __shfl_down_sync(FULL_MASK, hi, d);
+    double r;
+    asm("mov.b64 %0, {%1, %2};" : "=d"(r) : "r"(lo), "r"(hi));
+    return r;
 }
 
 // Factor-only scan coefficients of one line (setup; not on the apply path).
+// The lane maps are scanned Kogge-Stone style: after the levels at distances
+// 1, 2, 4, 8 lane l holds the composition of the 16 lanes ending at l
+// (W_2d(l) = W_d(l) + M_d(l) W_d(l-d), M_d(l) the product of the lane
+// multipliers of lanes l-d+1..l), and the exclusive carry of lane l is
+// W_16(l-1) + M_16(l-1) W_16(l-17).  A shuffle costs a single warp ~6.5 issue
+// cycles per 32-bit half, so the scan is shaped for the fewest shuffles (12
+// per direction), not for the fewest levels.
 template <int K>
 __device__ __forceinline__ PrepTS line_prep(int l, const double (&eF)[K], const double (&eB)[K])
 {
@@ -71,47 +76,30 @@ __device__ __forceinline__ PrepTS line_prep(int l, const double (&eF)[K], const 
         B0 *= eB[k];
     }
     {  // forward: maps compose in increasing lane order
-        const double a1 = up(A0, 1), a2 = up(A0, 2), a3 = up(A0, 3);
-        const double A01 = A0 * a1, A012 = A01 * a2, A1 = A012 * (l >= 3 ? a3 : 1.0);
-        P.p1 = l >= 1 ? A0 : 0.0;
-        P.p2 = l >= 2 ? A01 : 0.0;
-        P.p3 = l >= 3 ? A012 : 0.0;
-        const double b4 = up(A1, 4), b8 = up(A1, 8), b12 = up(A1, 12);
-        const double A14 = A1 * b4, A148 = A14 * b8, A2 = A148 * (l >= 12 ? b12 : 1.0);
-        P.s1 = l >= 4 ? A1 : 0.0;
-        P.s2 = l >= 8 ? A14 : 0.0;
-        P.s3 = l >= 12 ? A148 : 0.0;
-        const double c1 = up(A2, 1);
-        P.e1 = l >= 17 ? c1 : 0.0;
+        const double M2 = A0 * up(A0, 1), M4 = M2 * up(M2, 2), M8 = M4 * up(M4, 4), M16 = M8 * up(M8, 8);
+        const double e = up(M16, 1);
+        P.m1 = l >= 1 ? A0 : 0.0;
+        P.m2 = l >= 2 ? M2 : 0.0;
+        P.m4 = l >= 4 ? M4 : 0.0;
+        P.m8 = l >= 8 ? M8 : 0.0;
+        P.e = l >= 17 ? e : 0.0;
     }
     {  // backward: maps compose in decreasing lane order
-        const double a1 = dn(B0, 1), a2 = dn(B0, 2), a3 = dn(B0, 3);
-        const double B01 = B0 * a1, B012 = B01 * a2, B1 = B012 * (l <= 28 ? a3 : 1.0);
-        P.q1 = l <= 30 ? B0 : 0.0;
-        P.q2 = l <= 29 ? B01 : 0.0;
-        P.q3 = l <= 28 ? B012 : 0.0;
-        const double b4 = dn(B1, 4), b8 = dn(B1, 8), b12 = dn(B1, 12);
-        const double B14 = B1 * b4, B148 = B14 * b8, B2 = B148 * (l <= 19 ? b12 : 1.0);
-        P.t1 = l <= 27 ? B1 : 0.0;
-        P.t2 = l <= 23 ? B14 : 0.0;
-        P.t3 = l <= 19 ? B148 : 0.0;
-        const double c1 = dn(B2, 1);
-        P.f1 = l <= 14 ? c1 : 0.0;
+        const double M2 = B0 * dn(B0, 1), M4 = M2 * dn(M2, 2), M8 = M4 * dn(M4, 4), M16 = M8 * dn(M8, 8);
+        const double f = dn(M16, 1);
+        P.n1 = l <= 30 ? B0 : 0.0;
+        P.n2 = l <= 29 ? M2 : 0.0;
+        P.n4 = l <= 27 ? M4 : 0.0;
+        P.n8 = l <= 23 ? M8 : 0.0;
+        P.f = l <= 14 ? f : 0.0;
     }
     return P;
 }
 
-// Local (carry-free) part of a line solve: prefix maps of both chains and the
-// carry-independent remainder R_k = pf_k + eB_k pb_{k+1} (= pf_k + pb_k - rho_k).
+// One line (reference form, used by the micro-benchmarks): rho[k] = mu r of
+// this lane's K cells, x[k] out.  The production kernel inlines the same
+// sequence with its operand loads placed between the levels (ntd_apply_ts.cuh).
 template <int K>
-struct LocalTS {
-    double pa[K], qa[K], R[K];
-    double C0, D0;
-};
-
-// One line.  rho[k] = mu r (this lane's K cells), x[k] out.  `l` = lane.
-// SUB: x = y - T^{-1} r instead (the level-2/3 upper sweeps), y passed in x.
-template <int K, bool SUB = false, bool ORD = true>
 __device__ __forceinline__ void line_solve(const PrepTS &P, int l, const double (&eF)[K], const double (&eB)[K],
                                            const double (&rho)[K], double (&x)[K])
 {
@@ -127,30 +115,22 @@ __device__ __forceinline__ void line_solve(const PrepTS &P, int l, const double 
         pb[K - 1 - k] = fma(eB[K - 1 - k], pb[K - k], rho[K - 1 - k]);
         qa[K - 1 - k] = eB[K - 1 - k] * qa[K - k];
     }
-    const double C0 = pf[K - 1], D0 = pb[0];
-    // level 1
-    auto U = [](double v, int d) { return ORD ? vup(v, d) : up(v, d); };
-    auto Dn = [](double v, int d) { return ORD ? vdn(v, d) : dn(v, d); };
-    const double c3 = U(C0, 3), d3 = Dn(D0, 3), c2 = U(C0, 2), d2 = Dn(D0, 2), c1 = U(C0, 1), d1 = Dn(D0, 1);
-    const double C1 = fma(P.p1, c1, C0) + fma(P.p2, c2, P.p3 * c3);
-    const double D1 = fma(P.q1, d1, D0) + fma(P.q2, d2, P.q3 * d3);
-    // level 2
-    const double c12 = U(C1, 12), c8 = U(C1, 8), c4 = U(C1, 4);
-    const double d12 = Dn(D1, 12), d8 = Dn(D1, 8), d4 = Dn(D1, 4);
-    const double C2 = fma(P.s1, c4, C1) + fma(P.s2, c8, P.s3 * c12);
-    const double D2 = fma(P.t1, d4, D1) + fma(P.t2, d8, P.t3 * d12);
-    // level 3: exclusive carries
-    const double u17 = U(C2, 17), u1 = U(C2, 1);
-    const double v17 = Dn(D2, 17), v1 = Dn(D2, 1);
-    const double cF = fma(P.e1, u17, l >= 1 ? u1 : 0.0);
-    const double cB = fma(P.f1, v17, l <= 30 ? v1 : 0.0);
+    double C = pf[K - 1], D = pb[0];
+    C = fma(P.m1, up(C, 1), C);
+    D = fma(P.n1, dn(D, 1), D);
+    C = fma(P.m2, up(C, 2), C);
+    D = fma(P.n2, dn(D, 2), D);
+    C = fma(P.m4, up(C, 4), C);
+    D = fma(P.n4, dn(D, 4), D);
+    C = fma(P.m8, up(C, 8), C);
+    D = fma(P.n8, dn(D, 8), D);
+    const double u17 = up(C, 17), v17 = dn(D, 17), u1 = up(C, 1), v1 = dn(D, 1);
+    const double cF = fma(P.e, u17, l >= 1 ? u1 : 0.0);
+    const double cB = fma(P.f, v17, l <= 30 ? v1 : 0.0);
 #pragma unroll
     for (int k = 0; k < K; k++) {
         const double R = k < K - 1 ? fma(eB[k], pb[k + 1 < K ? k + 1 : k], pf[k]) : pf[k];
-        if (SUB)
-            x[k] = fma(-pa[k], cF, fma(-qa[k], cB, x[k] - R));
-        else
-            x[k] = fma(pa[k], cF, fma(qa[k], cB, R));
+        x[k] = fma(pa[k], cF, fma(qa[k], cB, R));
     }
 }
 

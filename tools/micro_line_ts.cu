@@ -1,15 +1,13 @@
 // Latency + numerics of the two-sided line solve (ntd_line_ts.cuh) against a
-// host Thomas solve, with the twisted radix-4 solve (ntd_line4.cuh) timed
-// beside it on the same dependent line-to-line chain.
+// host Thomas solve (long double), on a dependent line-to-line chain.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_1909_09771_b200/csrc -o /tmp/micro_line_ts tools/micro_line_ts.cu
 #include <cmath>
 #include <cstdio>
 #include <vector>
-#include "ntd_line4.cuh"
 #include "ntd_line_ts.cuh"
 
-template <int K, bool ORD>
-__global__ void k_ts(const double *eFg, const double *eBg, const double *rhog, double *xg, long long *cyc, int iters)
+template <int K>
+__global__ void __launch_bounds__(32, 1) k_ts(const double *eFg, const double *eBg, const double *rhog, double *xg, long long *cyc, int iters)
 {
     const int lane = threadIdx.x & 31;
     double eF[K], eB[K], rho[K], x[K];
@@ -19,48 +17,19 @@ __global__ void k_ts(const double *eFg, const double *eBg, const double *rhog, d
         rho[k] = rhog[lane * K + k];
     }
     const PrepTS P = ts::line_prep<K>(lane, eF, eB);
-    ts::line_solve<K, false, ORD>(P, lane, eF, eB, rho, x);
+    ts::line_solve<K>(P, lane, eF, eB, rho, x);
     for (int k = 0; k < K; k++) xg[lane * K + k] = x[k];
     double c[K];
     for (int k = 0; k < K; k++) c[k] = rho[k];
     long long t0 = clock64();
     for (int it = 0; it < iters; it++) {
-        ts::line_solve<K, false, ORD>(P, lane, eF, eB, c, x);
+        ts::line_solve<K>(P, lane, eF, eB, c, x);
 #pragma unroll
         for (int k = 0; k < K; k++) c[k] = fma(-0.1 * eF[k], x[k], rho[k]);
     }
     long long t1 = clock64();
     if (threadIdx.x == 0) cyc[0] = t1 - t0;
     xg[32 * K + lane] = x[0];
-}
-
-template <int K>
-__global__ void k_l4(double *out, long long *cyc, int iters, int n)
-{
-    const int lane = threadIdx.x & 31, s = lane & 15;
-    const int t = (n - 1) / 2;
-    const int L = lane < 16 ? t : n - 1 - t, P0 = 16 * K - L;
-    double aL[K], aU[K], cr[K], x2[K], c0[K];
-    for (int k = 0; k < K; k++) {
-        const int j = s * K + k - P0;
-        const bool v = j >= 0;
-        aL[k] = v ? -0.2 - 0.003 * ((lane + 3 * k) % 7) : 0.0;
-        aU[k] = v ? -0.21 + 0.002 * ((lane + k) % 3) : 0.0;
-        c0[k] = cr[k] = v ? 1.0 + 0.1 * lane - 0.05 * k : 0.0;
-    }
-    double xt2;
-    LinePrep P = line_prep<K>(s, aL, aU);
-    long long t0 = clock64();
-    double bt = 0.7;
-    for (int it = 0; it < iters; it++) {
-        line_solve4<K>(P, n, t, aL, cr, aU, bt, -0.05, -0.06, x2, xt2);
-#pragma unroll
-        for (int k = 0; k < K; k++) cr[k] = fma(-0.1 * aL[k], x2[k], c0[k]);
-        bt = 0.7 - 0.01 * xt2;
-    }
-    long long t1 = clock64();
-    if (threadIdx.x == 0) cyc[0] = t1 - t0;
-    out[lane] = x2[0];
 }
 
 template <int K>
@@ -106,30 +75,25 @@ void run(int n, double dom)
         }
     }
     double *g[4];
-    long long *cyc, c1, c2;
+    long long *cyc, c1;
     for (auto &p : g) cudaMalloc(&p, (NS + 32) * 8);
     cudaMalloc(&cyc, 8);
     cudaMemcpy(g[0], eF.data(), NS * 8, cudaMemcpyHostToDevice);
     cudaMemcpy(g[1], eB.data(), NS * 8, cudaMemcpyHostToDevice);
     cudaMemcpy(g[2], rho.data(), NS * 8, cudaMemcpyHostToDevice);
     const int IT = 20000;
-    long long c0;
-    for (int rep = 0; rep < 2; rep++) k_ts<K, false><<<1, 32>>>(g[0], g[1], g[2], g[3], cyc, IT);
-    cudaMemcpy(&c0, cyc, 8, cudaMemcpyDeviceToHost);
-    for (int rep = 0; rep < 2; rep++) k_ts<K, true><<<1, 32>>>(g[0], g[1], g[2], g[3], cyc, IT);
+    for (int rep = 0; rep < 2; rep++) k_ts<K><<<1, 32>>>(g[0], g[1], g[2], g[3], cyc, IT);
     std::vector<double> x(NS);
     cudaMemcpy(x.data(), g[3], NS * 8, cudaMemcpyDeviceToHost);
     cudaMemcpy(&c1, cyc, 8, cudaMemcpyDeviceToHost);
-    for (int rep = 0; rep < 2; rep++) k_l4<K><<<1, 32>>>(g[3], cyc, IT, n);
-    cudaMemcpy(&c2, cyc, 8, cudaMemcpyDeviceToHost);
     double err = 0, nrm = 0;
     for (int j = 0; j < n; j++) {
         err = std::fmax(err, std::fabs(x[j] - xr[j]));
         nrm = std::fmax(nrm, std::fabs(xr[j]));
     }
     for (int j = n; j < NS; j++) err = std::fmax(err, std::fabs(x[j]));
-    printf("K=%2d n=%3d dom=%.0e  max err/max|x| = %.2e   two-sided %.1f (free order %.1f) cycles/line   twisted radix-4 %.1f   (%s)\n", K, n,
-           dom, err / nrm, (double)c1 / IT, (double)c0 / IT, (double)c2 / IT, cudaGetErrorString(cudaGetLastError()));
+    printf("K=%2d n=%3d dom=%.0e  max err/max|x| = %.2e   two-sided %.1f cycles/line   (%s)\n", K, n,
+           dom, err / nrm, (double)c1 / IT, cudaGetErrorString(cudaGetLastError()));
     for (auto &p : g) cudaFree(p);
     cudaFree(cyc);
 }
