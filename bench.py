@@ -45,24 +45,34 @@ CFG4_REF_ITERS = [21, 21, 24, 21, 22, 22, 20, 20, 20, 24, 22, 23, 20, 21, 19, 21
                   22, 22, 22, 23, 21, 23, 21, 20, 21, 25, 21, 24, 21, 22, 21, 21, 19, 20, 23, 20, 25, 21, 25, 21,
                   20, 22, 23, 21, 20, 21, 21, 21, 20, 21, 21, 21, 23, 20, 23, 22]
 
-# Dependent-instruction latencies measured on this pool's B200s (tools/micro_lat.cu,
-# profiles/r02e_micro_lat.txt): a dependent DFMA/DMUL/DADD ~25 cycles, a 64-bit
-# warp shuffle ~23.  The NTD line solve (ntd_line4.cuh) has 2K + 14 dependent
-# fp64 operations and 4 dependent shuffle rounds per line step, and one apply
-# is (nz + 1)(ny + 1) dependent line steps: its latency roofline.
-FP64_DEP_CYCLES = 25.1
-SHFL64_CYCLES = 23.0
+# Single-warp issue costs measured on this pool's B200s (tools/micro_lat2.cu,
+# tools/micro_tput.cu, tools/micro_line_ts.cu; profiles/r02g_micro_*.txt): a
+# dependent DFMA/DADD/DMUL 8.2 cycles, a dependent 64-bit shuffle 24.3, and --
+# what bounds the sweep -- one warp gets a shuffle or a shared-memory access
+# through its in-order memory queue only every ~6 cycles (SHFL.32 5.6-7.0,
+# LDS.64 ~5.7, STS.64 6.4).  A line step of the NTD apply (ntd_apply_ts.cuh)
+# is one warp: 24 shuffles, (5.5 K + 8) 8-byte shared loads per lane on
+# average over the lower- and upper-sweep steps, 1.5 K stores; the two-sided
+# line solve alone (its dependent chain) measures 214 + 16 K cycles.  An apply
+# is (nz + 1)(ny + 1) dependent line steps.
+SHFL32_ISSUE = 6.5
+LDS64_ISSUE = 5.7
+ST64_ISSUE = 6.4
 
 
 def ntd_latency_roofline(nx, ny, nz, apply_s, sm_mhz):
     K = next(k for k in (1, 2, 3, 4, 5, 6, 8, 11, 12, 16) if 32 * k >= nx)
-    chain = (2 * K + 14) * FP64_DEP_CYCLES + 4 * SHFL64_CYCLES
+    mio = 24 * SHFL32_ISSUE + (5.5 * K + 8) * LDS64_ISSUE + 1.5 * K * ST64_ISSUE
+    chain = 214.0 + 16.0 * K
+    bound = max(mio, chain)
     steps = (nz + 1) * (ny + 1)
     measured = apply_s * sm_mhz * 1e6 / steps
-    return {"bound": "latency (dependent fp64 chain of the line solves)", "line_steps_per_apply": steps,
+    return {"bound": "single-warp issue: shuffles + shared-memory accesses of a line step (in-order memory queue), "
+                     "or the line solve's dependent chain if longer",
+            "line_steps_per_apply": steps, "mio_cycles_per_step": round(mio, 1),
             "chain_cycles_per_step": round(chain, 1), "measured_cycles_per_step": round(measured, 1),
-            "sm_mhz": sm_mhz, "frac": round(chain / measured, 3),
-            "source": "tools/micro_lat.cu latencies, profiles/r02e_micro_lat.txt"}
+            "sm_mhz": sm_mhz, "frac": round(bound / measured, 3),
+            "source": "tools/micro_tput.cu, micro_lat2.cu, micro_line_ts.cu; profiles/r02g_micro_*.txt"}
 
 
 METRIC = "pcg_munknowns_per_s"
@@ -392,7 +402,7 @@ def run_ntd(args):
                        "l2": "inputs larger than L2 (each batch vector %.0f MB)" % (8 * n * B / 1e6)},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n * B * world,
                     "d2h_bytes_per_step": 8 * n * B * world},
-            "roofline": {"kernel": "NTD apply sweep sl::k_apply (ntd_apply_slot), timed-region launches, rank 0",
+            "roofline": {"kernel": "NTD apply sweep ts::k_apply (ntd_apply_slot), timed-region launches, rank 0",
                          "bound": "hbm",
                          "achieved": achieved, "peak": peak[0], "unit": "GB/s", "frac": achieved / peak[0],
                          "peak_source": peak[1], "traffic": _traffic(cfg, Bg),

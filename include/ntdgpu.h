@@ -171,10 +171,13 @@ int64_t ntd_factor_work_doubles(int64_t nx, int64_t ny, int64_t nz,
 int ntd_factor(const double *a, double *pre, double *work, int64_t *status,
                int64_t nx, int64_t ny, int64_t nz, int64_t batch, void *stream);
 
-/* Solve arrays of a factor, derived data for the apply: the factor bands
- * m_recip, -(l1*m_recip), -(u1*m_recip), l2, u2, l3, u3 re-laid per grid line
- * in the apply's slot layout (chain coefficients precomputed; the reference
- * forms them inside _chain_scaled/_chain_unit, ntd_solve.py:20-104).
+/* Solve records of a factor, derived data for the apply: per grid line, in
+ * the apply's lane layout, the elimination multipliers of the two-sided line
+ * solve (forward and backward pivots of every cell rebuilt from l1, u1,
+ * m_recip by the reference's pivot recurrences, ntd_factor.py:86-110), the
+ * factor-only scan coefficients (the reference composes its chain lanes
+ * inside _chain_scaled/_chain_unit, ntd_solve.py:20-104) and l2, u2, l3, u3
+ * scaled by the per-cell pivot reciprocal mu; mu of every cell follows.
  * solve: >= ntd_solve_doubles (0 = grid served by the direct path; then pass
  * solve = NULL to ntd_apply). */
 int64_t ntd_solve_doubles(int64_t nx, int64_t ny, int64_t nz, int64_t batch);
