@@ -358,7 +358,7 @@ __device__ __forceinline__ bool mbar_test_a(unsigned bar, unsigned parity)
                  : "=r"(ok)
                  : "r"(bar), "r"(parity)
                  : "memory");
-    return ok != 0;
+    return __all_sync(FULL_MASK, ok != 0);  // (warp-uniform by construction; the vote lets the compiler know)
 }
 // one lane releases a stage (barrier count 1): the warp's loads of the stage
 // precede it in program order, and a 32-lane arrive would serialise 32 atomics
@@ -692,6 +692,9 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
             mbar_arrive_if(empty(rec), lane == 0);
             fin_L(cur, wn);
         }
+        // (checked here, at a block boundary: a branch inside the line solve splits its straight-line
+        // code and costs ~65 cycles per step)
+        if (PIPE && !okn) mbar_wait_a(full(rec + 1), par(rec + 1));
         double rho[K], x[K];
 #pragma unroll
         for (int k = 0; k < K; k++) rho[k] = fma(-cur.cp[k], xprev[k], cur.pt[k]);  // line 0: xprev = 0
@@ -700,7 +703,6 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
             if constexpr (!PIPE) {
                 if constexpr (j == 0) nbr_L(wn, adv(yn, dqB), y2p + dq * LR);
             } else if constexpr (j < NHOOK) {
-                if (j == 0 && !okn) mbar_wait_a(full(rec + 1), par(rec + 1));
                 load_L(J, WITH_N, nxt, w, sa(rec + 1), adv(yn, dqB), y2p + dq * LR, last ? cpT : cpL);
             } else {
                 mbar_arrive_if(empty(rec + 1), lane == 0 && !last);
@@ -741,6 +743,7 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
         ld_row(u2c, sa(rec) + o_u2(K) * 8 + l8);
         if (!lower3) ld_row(xo, sa(rec) + rx_of(K) * 8 + l8);
         mbar_arrive_if(empty(rec), lane == 0);
+        if (PIPE && cnt > 0 && !okn) mbar_wait_a(full(rec + 1), par(rec + 1));
         double rho[K];
 #pragma unroll
         for (int k = 0; k < K; k++) {
@@ -756,7 +759,6 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
                 if constexpr (!PIPE) {
                     if constexpr (j == 0) ld_buf(ycur, adv(xl, -dqB));
                 } else if constexpr (j < NHOOK) {
-                    if (j == 0 && !okn) mbar_wait_a(full(rec + 1), par(rec + 1));
                     load_U(J, WITH_N, nxt, ycur, xocur, sa(rec + 1), adv(xl, -dqB));
                 } else {
                     mbar_arrive_if(empty(rec + 1), lane == 0);
@@ -789,6 +791,7 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
             load_U(ALL, NO_N, cur, dummy, xocur, sa(rec), xu);
             mbar_arrive_if(empty(rec), lane == 0);
         }
+        if (PIPE && more && !okn) mbar_wait_a(full(rec + 1), par(rec + 1));
         double rho[K];
 #pragma unroll
         for (int k = 0; k < K; k++) rho[k] = cur.cp[k] * xn[k];
@@ -800,7 +803,6 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
             if constexpr (!PIPE) {
                 if constexpr (j == 0) ld_buf(ynx, adv(xu, -dqB));
             } else if constexpr (j < NHOOK) {
-                if (j == 0 && more && !okn) mbar_wait_a(full(rec + 1), par(rec + 1));
                 load_U(J, WITH_N, nxt, ynx, xonx, sa(rec + 1), adv(xu, -dqB));
             } else {
                 mbar_arrive_if(empty(rec + 1), lane == 0 && more);
@@ -854,7 +856,9 @@ __global__ void __launch_bounds__(128 * NP, 1) k_apply(const double *__restrict_
     S.x = xsl + sys * nsl;
     S.xs = xssl + sys * nsl;
     S.zero = zpl;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // (warp index through a shuffle: provably warp-uniform, so every branch on the warp's role,
+    // half and trip counts is a uniform branch and the shuffles need no divergence checks)
+    const int lane = threadIdx.x & 31, warp = __shfl_sync(FULL_MASK, (int)(threadIdx.x >> 5), 0);
     const bool producer = warp >= 2 * NP;
     const int sw = warp & (2 * NP - 1);  // solver warp this warp is (or feeds)
     const int pair = NP == 2 ? sw >> 1 : (int)(blockIdx.x & 1), w2 = sw & 1, bar = NP == 2 ? 1 + pair : 1;
