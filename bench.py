@@ -45,18 +45,18 @@ CFG4_REF_ITERS = [21, 21, 24, 21, 22, 22, 20, 20, 20, 24, 22, 23, 20, 21, 19, 21
                   22, 22, 22, 23, 21, 23, 21, 20, 21, 25, 21, 24, 21, 22, 21, 21, 19, 20, 23, 20, 25, 21, 25, 21,
                   20, 22, 23, 21, 20, 21, 21, 21, 20, 21, 21, 21, 23, 20, 23, 22]
 
-# Single-warp issue costs measured on this pool's B200s (tools/micro_lat2.cu,
-# tools/micro_tput.cu, tools/micro_line_ts.cu; profiles/r02g_micro_*.txt): a
-# dependent DFMA/DADD/DMUL 8.2 cycles, a dependent 64-bit shuffle 24.3, and --
-# what bounds the sweep -- one warp gets a shuffle or a shared-memory access
-# through its in-order memory queue only every ~6 cycles (SHFL.32 5.6-7.0,
-# LDS.64 ~5.7, STS.64 6.4).  A line step of the NTD apply (ntd_apply_ts.cuh)
-# is one warp: 24 shuffles, (5.5 K + 8) 8-byte shared loads per lane on
-# average over the lower- and upper-sweep steps, 1.5 K stores; the two-sided
-# line solve alone (its dependent chain) measures 214 + 16 K cycles.  An apply
-# is (nz + 1)(ny + 1) dependent line steps.
-SHFL32_ISSUE = 6.5
-LDS64_ISSUE = 5.7
+# Costs measured on this pool's B200s (tools/micro_lat2.cu, micro_tput2.cu,
+# micro_line_ts.cu; profiles/r02g_micro_*.txt): a dependent DFMA/DADD/DMUL 8.2
+# cycles, a dependent 64-bit shuffle 24.3 (two SHFL.32); one warp issues a
+# SHFL.32 every 4.5 cycles, an LDS.64 every 2.25 and an STS.64 every ~6.4.  A
+# line step of the NTD apply (ntd_apply_ts.cuh) is one warp: 24 shuffles,
+# (5.5 K + 8) 8-byte shared loads per lane on average over the lower- and
+# upper-sweep steps, 1.5 K stores; the two-sided line solve alone (its
+# dependent chain: 5 shuffle rounds + 2 K + 8 fp64 operations) measures
+# 214 + 16 K cycles.  An apply is (nz + 1)(ny + 1) dependent line steps, so
+# its roofline is the longer of the two per step.
+SHFL32_ISSUE = 4.5
+LDS64_ISSUE = 2.25
 ST64_ISSUE = 6.4
 
 
@@ -67,12 +67,12 @@ def ntd_latency_roofline(nx, ny, nz, apply_s, sm_mhz):
     bound = max(mio, chain)
     steps = (nz + 1) * (ny + 1)
     measured = apply_s * sm_mhz * 1e6 / steps
-    return {"bound": "single-warp issue: shuffles + shared-memory accesses of a line step (in-order memory queue), "
-                     "or the line solve's dependent chain if longer",
+    return {"bound": "latency: the dependent chain of a line step (5 shuffle rounds + fp64 chain of the two-sided "
+                     "line solve), or one warp's shuffle / shared-memory issue per step if longer",
             "line_steps_per_apply": steps, "mio_cycles_per_step": round(mio, 1),
             "chain_cycles_per_step": round(chain, 1), "measured_cycles_per_step": round(measured, 1),
             "sm_mhz": sm_mhz, "frac": round(bound / measured, 3),
-            "source": "tools/micro_tput.cu, micro_lat2.cu, micro_line_ts.cu; profiles/r02g_micro_*.txt"}
+            "source": "tools/micro_tput2.cu, micro_lat2.cu, micro_line_ts.cu; profiles/r02g_micro_*.txt"}
 
 
 METRIC = "pcg_munknowns_per_s"

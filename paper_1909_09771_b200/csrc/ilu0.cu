@@ -78,7 +78,7 @@ template <bool FWD>
 __device__ void ilu_sweep(const SweepGeom &g, const double *__restrict__ f, const double *__restrict__ rin,
                           double *z, double *acc_out, volatile unsigned long long *prog, unsigned long long base_word)
 {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, warp = __shfl_sync(FULL_MASK, (int)(threadIdx.x >> 5), 0), W = blockDim.x >> 5;
     const i64 n = g.n, nxy = g.nxy;
     const int nx = g.nx, ny = g.ny, S = g.S, G = g.G;
     const double *fa = FWD ? f + 2 * n : f + 4 * n;  // x coupling (f2 | f4)
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(ILU_WARPS * 32) k_ilu0_factor(const double *__
     const i64 nxy = g.nxy;
     if (threadIdx.x < ILU_WARPS) prog[threadIdx.x] = 0ull;
     __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, warp = __shfl_sync(FULL_MASK, (int)(threadIdx.x >> 5), 0), W = blockDim.x >> 5;
     const int S = g.S, G = g.G;
     unsigned long long cw1 = 0, cw2 = 0;
     int cu1 = -1, cu2 = -1;

@@ -113,7 +113,7 @@ __device__ __forceinline__ void sweep(const Sweep &w, const double *__restrict__
                                       double *zf, double *zout, double *accio, double *buf, int nc, int crank,
                                       const Link &lk)
 {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, warp = __shfl_sync(FULL_MASK, (int)(threadIdx.x >> 5), 0), W = blockDim.x >> 5;  // (provably warp-uniform)
     constexpr int NCF = FWD ? 3 : 4;
     constexpr int NOP = FWD ? 4 : ((OUT & 2) ? 6 : 5);  // operands per unit and step
     constexpr int NO = NOP + (GL ? 1 : 0);             // (+ the speculative halo value)

@@ -262,7 +262,7 @@ template <bool FWD>
 __device__ void sweep(const Geom &g, int u_lo, int u_hi, const double *__restrict__ coef, const double *in,
                       double *z, const Prog &prog, double *ring, double *zout, double *acc_out)
 {
-    const int lane = threadIdx.x & 31, lwarp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, lwarp = __shfl_sync(FULL_MASK, (int)(threadIdx.x >> 5), 0);  // provably warp-uniform
     const int WT = prog.nw * prog.nc, warp = prog.crank * prog.nw + lwarp;  // cluster-wide warp
     const int T = g.T, G = g.G, nx = g.nx;
     constexpr int NC = FWD ? 3 : 4;
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_apply(const double *__restrict__
     const double *rn = r + sys * g.n;
     double *zn = z ? z + sys * g.n : nullptr, *an = acc ? acc + sys * g.n : nullptr;
     double *zfs = zf + sys * per, *zbs = zb + sys * per;
-    double *ring = skew_ring + (size_t)(threadIdx.x >> 5) * PS * ROWS * 32;
+    double *ring = skew_ring + (size_t)__shfl_sync(FULL_MASK, (int)(threadIdx.x >> 5), 0) * PS * ROWS * 32;
     const int nw = blockDim.x >> 5;
     const Prog P{prog_s, nc, (int)(blockIdx.x % nc), nw};
     if (threadIdx.x < nw) prog_s[threadIdx.x] = 0u;

@@ -461,9 +461,11 @@ __device__ __forceinline__ void solve_line(const Ops<K> &o, int l, const double 
     }
 #pragma unroll
     for (int k = 0; k < K; k++) Rr[k] = k < K - 1 ? fma(o.eB[k], pb[k + 1 < K ? k + 1 : k], pf[k]) : pf[k];
-    const double m1 = l >= 1 ? pa[K - 1] : 0.0, n1 = l <= 30 ? qa[0] : 0.0;
-    C = fma(m1, c1, C);
-    D = fma(n1, d1, D);
+    // (no lane masks on the level-1 multipliers and on the carries: the multiplier of a line's first
+    // cell and of its last cell -- and of every padding cell -- is an exact zero, so lane 0's pa[] and
+    // lane 31's qa[] are zeros and whatever finite value the edge shuffles return drops out)
+    C = fma(pa[K - 1], c1, C);
+    D = fma(qa[0], d1, D);
     const double c2 = up(C, 2), d2 = dn(D, 2);
     hook(std::integral_constant<int, 1>{});
     C = fma(o.pr[0], c2, C);
@@ -479,8 +481,8 @@ __device__ __forceinline__ void solve_line(const Ops<K> &o, int l, const double 
     // exclusive carries
     const double u17 = up(C, 17), v17 = dn(D, 17), u1 = up(C, 1), v1 = dn(D, 1);
     hook(std::integral_constant<int, 4>{});
-    const double cF = fma(o.pr[3], u17, l >= 1 ? u1 : 0.0);
-    const double cB = fma(o.pr[7], v17, l <= 30 ? v1 : 0.0);
+    const double cF = fma(o.pr[3], u17, u1);
+    const double cB = fma(o.pr[7], v17, v1);
     hook(std::integral_constant<int, 5>{});
 #pragma unroll
     for (int k = 0; k < K; k++) {

@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(128) k_ntd_apply(const double *__restrict__ pr
     if (active && !active[sys]) return;
     const i64 nxy = (i64)nx * ny, n = nxy * nz;
     const FactorPtrs F = factor_ptrs(pre + sys * 7 * n, n);
-    const int warp = threadIdx.x >> 5, pair = warp >> 1, w2 = warp & 1, bar = 1 + pair;
+    const int warp = __shfl_sync(FULL_MASK, (int)(threadIdx.x >> 5), 0), pair = warp >> 1, w2 = warp & 1, bar = 1 + pair;
     double *myex = ex[pair];
     int parity = 0;
     PlaneIO io;
@@ -1020,7 +1020,7 @@ __global__ void __launch_bounds__(128) k_ntd_factor(const double *__restrict__ a
     c.nx = nx;
     c.ny = ny;
     c.nz = nz;
-    const int warp = threadIdx.x >> 5, pair = warp >> 1, w2 = warp & 1, bar = 1 + pair;
+    const int warp = __shfl_sync(FULL_MASK, (int)(threadIdx.x >> 5), 0), pair = warp >> 1, w2 = warp & 1, bar = 1 + pair;
     double *lsm = lsm_all + warp * 3 * nx;
     double *car = car_s[warp];
     if (threadIdx.x < 2) {
