@@ -668,6 +668,7 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
     Ops<K> cur;
     Raw<K> wn;  // wide lines: neighbour values of the next lower-type record
     bool okn = true;
+    bool okw = false;  // wide lines: this step's record was seen complete by the previous step's test
     // ---------------- prologue: the plane's first record (a lower line, or the twist line when cnt == 0)
     if constexpr (PIPE) {
         Raw<K> w;
@@ -689,7 +690,7 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
         Raw<K> w;
         const bool last = i == cnt - 1;  // the next record is the twist line (an L-type record as well)
         if constexpr (!PIPE) {
-            mbar_wait_a(full(rec), par(rec));
+            if (!okw) mbar_wait_a(full(rec), par(rec));  // (tested during the previous step)
             load_L(ALL, NO_N, cur, wn, sa(rec), yn, y2p, cpL);
             mbar_arrive_if(empty(rec), lane == 0);
             fin_L(cur, wn);
@@ -704,6 +705,7 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
             constexpr int j = decltype(J)::value;
             if constexpr (!PIPE) {
                 if constexpr (j == 0) nbr_L(wn, adv(yn, dqB), y2p + dq * LR);
+                if constexpr (j == NHOOK) okw = mbar_test_a(full(rec + 1), par(rec + 1));
             } else if constexpr (j < NHOOK) {
                 load_L(J, WITH_N, nxt, w, sa(rec + 1), adv(yn, dqB), y2p + dq * LR, last ? cpT : cpL);
             } else {
@@ -738,7 +740,7 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
     {
         double u2c[K], xo[K];
         if constexpr (!PIPE) {
-            mbar_wait_a(full(rec), par(rec));
+            if (!okw) mbar_wait_a(full(rec), par(rec));
             load_L(ALL, NO_N, cur, wn, sa(rec), yn, y2p, cpT);
             fin_L(cur, wn);
         }
@@ -760,6 +762,7 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
             if (cnt > 0) {
                 if constexpr (!PIPE) {
                     if constexpr (j == 0) ld_buf(ycur, adv(xl, -dqB));
+                    if constexpr (j == NHOOK) okw = mbar_test_a(full(rec + 1), par(rec + 1));
                 } else if constexpr (j < NHOOK) {
                     load_U(J, WITH_N, nxt, ycur, xocur, sa(rec + 1), adv(xl, -dqB));
                 } else {
@@ -789,7 +792,7 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
         double ynx[K], xonx[K];
         if constexpr (!PIPE) {
             double dummy[K];
-            mbar_wait_a(full(rec), par(rec));
+            if (!okw) mbar_wait_a(full(rec), par(rec));
             load_U(ALL, NO_N, cur, dummy, xocur, sa(rec), xu);
             mbar_arrive_if(empty(rec), lane == 0);
         }
@@ -804,6 +807,7 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
             constexpr int j = decltype(J)::value;
             if constexpr (!PIPE) {
                 if constexpr (j == 0) ld_buf(ynx, adv(xu, -dqB));
+                if constexpr (j == NHOOK) okw = more && mbar_test_a(full(rec + 1), par(rec + 1));
             } else if constexpr (j < NHOOK) {
                 load_U(J, WITH_N, nxt, ynx, xonx, sa(rec + 1), adv(xu, -dqB));
             } else {
