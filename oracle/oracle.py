@@ -5,7 +5,7 @@ ctypes wrapper over ``ntd_oracle.c``, a plain-C restatement of the reference
 function in the C source).  Only ``tests/``, ``__graft_entry__.smoke()`` and
 ``bench.py``'s CPU-baseline / ``--impl reference`` leg may import this module,
 and only as the checker or the timed CPU baseline.  The product package
-``paper_1909_09771_b200`` never imports it (tests/test_no_oracle_in_product.py
+``paper_1909_09771_b200`` never imports it (tests/test_product_boundary.py
 checks that).
 
 Parity pin: tests/test_oracle_golden.py checks every function here against
