@@ -1,6 +1,6 @@
 """Config-4 batch (64 x 96^3) solve rate under different ILU0 / NTD mapping
 policies (experiments; the product picks them in device.ilu0_hp_config /
-ilu0_ctas / ntd_ctas).  python tools/batch_variants.py policy [systems]
+ilu0_ctas / ntd_ctas).  python tools/batch_variants.py policy [systems] [groups]
 policies: auto, skew, hp:nc:w (fixed), hpmin (hp whenever it fits)."""
 import os
 import sys
@@ -16,6 +16,7 @@ from paper_1909_09771_b200.batch import BatchSolver  # noqa: E402
 
 policy = sys.argv[1] if len(sys.argv) > 1 else "auto"
 S = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+GROUPS = int(sys.argv[3]) if len(sys.argv) > 3 else None
 orig = D.ilu0_hp_config
 if policy == "skew":
     D.ilu0_hp_config = lambda *a, **k: None
@@ -35,7 +36,7 @@ a = D.assemble(torch.from_numpy(np.stack(kaps)).cuda(), nx, ny, nz, bc)
 xt = torch.from_numpy(np.stack(xts)).cuda()
 b = torch.empty_like(xt)
 _lib.call("ntd_spmv", _lib.ptr(a), _lib.ptr(xt), _lib.ptr(b), nx, ny, nz, S, None, _lib.stream())
-solver = BatchSolver(a, nx, ny, nz).setup()
+solver = BatchSolver(a, nx, ny, nz, groups=GROUPS).setup()
 solver.reserve(4)
 solver.solve_many([b] * 2, 1e-8, x_outs=[solver.x] * 2)
 torch.cuda.synchronize()
@@ -45,5 +46,5 @@ res = solver.solve_many([b] * 3, 1e-8, x_outs=[solver.x] * 3)
 e[1].record()
 torch.cuda.synchronize()
 work = sum(n * sum(r.iterations) for r in res)
-print(f"policy {policy} systems {S}: {work / (e[0].elapsed_time(e[1]) / 1e3) / 1e6:.0f} Munk-iter/s, "
+print(f"policy {policy} systems {S} groups {len(solver.groups)}: {work / (e[0].elapsed_time(e[1]) / 1e3) / 1e6:.0f} Munk-iter/s, "
       f"iters {min(res[0].iterations)}-{max(res[0].iterations)}", flush=True)
