@@ -508,8 +508,10 @@ constexpr int REF_LANES = 4;
 //   UNIT:   x_e = x_e - dr_e off_e x_{e-1}     (_chain_unit, in place)
 // aw/cw: smem prefix maps (m each); car: smem carries (REF_LANES + 1).
 template <bool SCALED>
-__device__ __forceinline__ void chain_ref_compose(double *x, const double *dr, const double *off, const double *rhs,
-                                                  int lo, int step, int m, double *aw, double *cw, int sl)
+__device__ __forceinline__ void chain_ref_compose(const double *__restrict__ x, const double *__restrict__ dr,
+                                                  const double *__restrict__ off, const double *__restrict__ rhs,
+                                                  int lo, int step, int m, double *__restrict__ aw,
+                                                  double *__restrict__ cw, int sl)
 {
     // sl: lane within the half-warp; lanes 0..REF_LANES-1 compose one chunk each
     if (m < 2 * REF_LANES || sl >= REF_LANES) return;
@@ -519,6 +521,9 @@ __device__ __forceinline__ void chain_ref_compose(double *x, const double *dr, c
     double aa = a, cc = SCALED ? mul_rn(rhs[p], dr[p]) : x[p];
     aw[base] = aa;
     cw[base] = cc;
+    // (the prefix maps are separate shared-memory arrays: with the no-alias promise the operand loads
+    // of the next cells are issued ahead of this cell's dependent multiply-adds)
+#pragma unroll 4
     for (int t = 1; t < chunk; t++) {
         p += step;
         a = SCALED ? mul_rn(-off[p], dr[p]) : mul_rn(-dr[p], off[p]);
