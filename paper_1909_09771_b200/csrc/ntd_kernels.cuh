@@ -732,26 +732,19 @@ static __device__ int line_factor_warp(const double *__restrict__ td, const doub
     }
     __syncwarp();
     int bad = -1;
-    if (lane == 0) {
+    if (lane == 0 || lane == 16) {
+        // Lane 0 walks the ascending pivots, lane 16 the descending ones -- in ONE loop, so the two
+        // recurrences run concurrently (as two branches of a warp they ran one after the other).
+        // The first cell needs no special case (its product sc is an exact 0 and m starts at 0), and a
+        // bad pivot is recorded without leaving the loop: what follows it is never used, the line fails.
+        const bool asc = lane == 0;
+        const int cnt = asc ? t : nx - 1 - t, stp = asc ? 1 : -1;
+        int i = asc ? 0 : nx - 1;
         double m = 0.0;
-        for (int i = 0; i < t; i++) {
-            double piv = (i == 0) ? sd[0] : sub_rn(sd[i], mul_rn(sc[i], m));
-            if (piv == 0.0 || !isfinite(piv)) {
-                bad = i;
-                break;
-            }
-            m = 1.0 / piv;
-            sm[i] = m;
-        }
-    } else if (lane == 16) {
-        double m = 0.0;
-        for (int i = nx - 1; i > t; i--) {
-            double piv = (i == nx - 1) ? sd[i] : sub_rn(sd[i], mul_rn(sc[i], m));
-            if (piv == 0.0 || !isfinite(piv)) {
-                bad = i;
-                break;
-            }
-            m = 1.0 / piv;
+        for (int it = 0; it < cnt; it++, i += stp) {
+            const double piv = sub_rn(sd[i], mul_rn(sc[i], m));
+            if (bad < 0 && (piv == 0.0 || !isfinite(piv))) bad = i;
+            m = __drcp_rn(piv);  // == 1.0 / piv (both correctly rounded)
             sm[i] = m;
         }
     }
