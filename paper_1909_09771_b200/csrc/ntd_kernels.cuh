@@ -926,20 +926,31 @@ __device__ void correct_from_pair(const FactorCtx &c, int p, int m, double *P[5]
     plane_solve_ref(F, (i64)m * nxy, useg, W, S.at(S_YL), BETA, QD, c.nx, c.ny, w2, bar_id, lsm, car);
     // beta (_beta_from :242-249), qw (_plane_band_action :266-274), qd shift (:393-399)
     int fb = 0, fq = 0;
-    for (i64 k = tid; k < nxy; k += 64) {
-        double u = useg[k], w = W[k];
-        double bet = u != 0.0 ? w / u : 0.0;
-        if (!isfinite(bet)) fb = 1;
-        BETA[k] = bet;
-        double qw = mul_rn(Q[0][k], w);
-        if (k >= 1) qw = add_rn(qw, mul_rn(Q[1][k], W[k - 1]));
-        if (k + 1 < nxy) qw = add_rn(qw, mul_rn(Q[2][k], W[k + 1]));
-        if (k >= nx) qw = add_rn(qw, mul_rn(Q[3][k], W[k - nx]));
-        if (k + nx < nxy) qw = add_rn(qw, mul_rn(Q[4][k], W[k + nx]));
-        double qd = Q[0][k];
-        if (w != 0.0) qd = add_rn(qd, sub_rn(u, qw) / w);
-        if (!isfinite(qd)) fq = 1;
-        QD[k] = qd;
+    // The plane loops below are elementwise over distinct scratch planes, walked by the pair's 64
+    // threads: with the pointers held in no-alias locals (not re-read from the pointer arrays, which
+    // live in local memory) every load of an iteration is issued before its first store, one memory
+    // round trip per iteration instead of one per band.
+    {
+        const double *__restrict__ q0 = Q[0], *__restrict__ q1 = Q[1], *__restrict__ q2 = Q[2],
+                     *__restrict__ q3 = Q[3], *__restrict__ q4 = Q[4];
+        const double *__restrict__ us = useg, *__restrict__ Wr = W;
+        double *__restrict__ Bo = BETA, *__restrict__ Qo = QD;
+#pragma unroll 2
+        for (i64 k = tid; k < nxy; k += 64) {
+            double u = us[k], w = Wr[k];
+            double bet = u != 0.0 ? w / u : 0.0;
+            if (!isfinite(bet)) fb = 1;
+            Bo[k] = bet;
+            double qw = mul_rn(q0[k], w);
+            if (k >= 1) qw = add_rn(qw, mul_rn(q1[k], Wr[k - 1]));
+            if (k + 1 < nxy) qw = add_rn(qw, mul_rn(q2[k], Wr[k + 1]));
+            if (k >= nx) qw = add_rn(qw, mul_rn(q3[k], Wr[k - nx]));
+            if (k + nx < nxy) qw = add_rn(qw, mul_rn(q4[k], Wr[k + nx]));
+            double qd = q0[k];
+            if (w != 0.0) qd = add_rn(qd, sub_rn(u, qw) / w);
+            if (!isfinite(qd)) fq = 1;
+            Qo[k] = qd;
+        }
     }
     if (fb) flag[0] = 1;
     if (fq) flag[1] = 1;
@@ -950,16 +961,24 @@ __device__ void correct_from_pair(const FactorCtx &c, int p, int m, double *P[5]
         return;
     }
     // _plane_correction (ntd_factor.py:222-239)
-    for (i64 k = tid; k < nxy; k += 64) {
-        double rs = rowscale[k], bet = BETA[k];
-        double inner = sub_rn(mul_rn(2.0, bet), mul_rn(mul_rn(bet, QD[k]), bet));
-        P[0][k] = sub_rn(P[0][k], mul_rn(mul_rn(rs, inner), useg[k]));
-        double rb = mul_rn(rs, bet);
-        if (k >= 1) P[1][k] = add_rn(P[1][k], mul_rn(mul_rn(mul_rn(rb, Q[1][k]), BETA[k - 1]), useg[k - 1]));
-        if (k + 1 < nxy) P[2][k] = add_rn(P[2][k], mul_rn(mul_rn(mul_rn(rb, Q[2][k]), BETA[k + 1]), useg[k + 1]));
-        if (k >= nx) P[3][k] = add_rn(P[3][k], mul_rn(mul_rn(mul_rn(rb, Q[3][k]), BETA[k - nx]), useg[k - nx]));
-        if (k + nx < nxy)
-            P[4][k] = add_rn(P[4][k], mul_rn(mul_rn(mul_rn(rb, Q[4][k]), BETA[k + nx]), useg[k + nx]));
+    {
+        double *__restrict__ p0 = P[0], *__restrict__ p1 = P[1], *__restrict__ p2 = P[2], *__restrict__ p3 = P[3],
+                            *__restrict__ p4 = P[4];
+        const double *__restrict__ q1 = Q[1], *__restrict__ q2 = Q[2], *__restrict__ q3 = Q[3],
+                     *__restrict__ q4 = Q[4];
+        const double *__restrict__ us = useg, *__restrict__ rsc = rowscale, *__restrict__ Br = BETA,
+                     *__restrict__ Qr = QD;
+#pragma unroll 2
+        for (i64 k = tid; k < nxy; k += 64) {
+            double rs = rsc[k], bet = Br[k];
+            double inner = sub_rn(mul_rn(2.0, bet), mul_rn(mul_rn(bet, Qr[k]), bet));
+            p0[k] = sub_rn(p0[k], mul_rn(mul_rn(rs, inner), us[k]));
+            double rb = mul_rn(rs, bet);
+            if (k >= 1) p1[k] = add_rn(p1[k], mul_rn(mul_rn(mul_rn(rb, q1[k]), Br[k - 1]), us[k - 1]));
+            if (k + 1 < nxy) p2[k] = add_rn(p2[k], mul_rn(mul_rn(mul_rn(rb, q2[k]), Br[k + 1]), us[k + 1]));
+            if (k >= nx) p3[k] = add_rn(p3[k], mul_rn(mul_rn(mul_rn(rb, q3[k]), Br[k - nx]), us[k - nx]));
+            if (k + nx < nxy) p4[k] = add_rn(p4[k], mul_rn(mul_rn(mul_rn(rb, q4[k]), Br[k + nx]), us[k + nx]));
+        }
     }
     named_bar(bar_id, 64);
 }
@@ -969,12 +988,16 @@ static __device__ void load_plane_bands(const FactorCtx &c, int p, double *P[5],
 {
     const int tid = threadIdx.x & 63;
     const i64 pb = (i64)p * c.nxy, n = c.n;
+    double *__restrict__ p0 = P[0], *__restrict__ p1 = P[1], *__restrict__ p2 = P[2], *__restrict__ p3 = P[3],
+                        *__restrict__ p4 = P[4];
+    const double *__restrict__ a = c.a + pb;
+#pragma unroll 4
     for (i64 k = tid; k < c.nxy; k += 64) {
-        P[0][k] = c.a[3 * n + pb + k];
-        P[1][k] = c.a[2 * n + pb + k];
-        P[2][k] = c.a[4 * n + pb + k];
-        P[3][k] = c.a[1 * n + pb + k];
-        P[4][k] = c.a[5 * n + pb + k];
+        p0[k] = a[3 * n + k];
+        p1[k] = a[2 * n + k];
+        p2[k] = a[4 * n + k];
+        p3[k] = a[1 * n + k];
+        p4[k] = a[5 * n + k];
     }
     named_bar(bar_id, 64);
 }
@@ -987,9 +1010,14 @@ __device__ void factor_one_pair(const FactorCtx &c, int p, double *P[5], const P
 {
     const int tid = threadIdx.x & 63;
     const i64 pb = (i64)p * c.nxy, n = c.n;
-    for (i64 k = tid; k < c.nxy; k += 64) {
-        c.pre[2 * n + pb + k] = P[3][k];
-        c.pre[3 * n + pb + k] = P[4][k];
+    {
+        const double *__restrict__ p3 = P[3], *__restrict__ p4 = P[4];
+        double *__restrict__ o2 = c.pre + 2 * n + pb, *__restrict__ o3 = c.pre + 3 * n + pb;
+#pragma unroll 4
+        for (i64 k = tid; k < c.nxy; k += 64) {
+            o2[k] = p3[k];
+            o3[k] = p4[k];
+        }
     }
     named_bar(bar_id, 64);
     const double *Pc[5] = {P[0], P[1], P[2], P[3], P[4]};
