@@ -53,8 +53,11 @@ def lognormal_grid(nx, ny, nz, seed):
 
 
 # nx -> the instantiated K = ceil(nx/32) it selects; 400 / 500 take the direct path
+# (odd widths next to a lane boundary, single-line / single-plane grids, and planes too tall for the
+# shared-memory plane buffer: 20x40, 40x70 take the ring kernel with global neighbour lines)
 K_GRIDS = [(20, 9, 7), (40, 11, 6), (96, 10, 5), (120, 7, 6), (150, 9, 5), (180, 6, 5), (250, 7, 4),
-           (350, 5, 4), (400, 5, 3), (500, 4, 3)]
+           (350, 5, 4), (400, 5, 3), (500, 4, 3), (95, 4, 3), (97, 3, 3), (33, 2, 2), (161, 3, 2), (65, 1, 4),
+           (31, 5, 1), (20, 40, 3), (40, 70, 2), (200, 200, 2)]
 
 
 @pytest.mark.parametrize("grid", K_GRIDS, ids=[f"nx{g[0]}" for g in K_GRIDS])
