@@ -365,16 +365,6 @@ __device__ void plane_solve(const FactorPtrs &F, const PlaneIO &io, i64 pb, int 
     }
 }
 
-#ifdef NTD_TIMING
-__device__ unsigned long long g_ntd_timing[8][8];
-#define TSTAMP(v) long long v = clock64()
-#define TACC(slot, a, b) \
-    if ((threadIdx.x & 31) == 0 && blockIdx.x == 0) atomicAdd(&g_ntd_timing[threadIdx.x >> 5][slot], (unsigned long long)((b) - (a)))
-#else
-#define TSTAMP(v)
-#define TACC(slot, a, b)
-#endif
-
 // ---- TMA / mbarrier helpers (1-D bulk copies)
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 

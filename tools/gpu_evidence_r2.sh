@@ -1,5 +1,5 @@
 # Round-2 evidence: latencies, bench, launch list, ncu of the NTD and ILU0 sweeps as the bench launches them.
-./tools/micro_lat2.bin > gpurun_out/micro_lat2.txt 2>&1; ./tools/micro_tput.bin > gpurun_out/micro_tput.txt 2>&1; ./tools/micro_line_ts.bin > gpurun_out/micro_line_ts.txt 2>&1; cat gpurun_out/micro_lat2.txt
+./tools/micro_lat2.bin > gpurun_out/micro_lat2.txt 2>&1; ./tools/micro_tput2.bin > gpurun_out/micro_tput2.txt 2>&1; ./tools/micro_line_ts.bin > gpurun_out/micro_line_ts.txt 2>&1; cat gpurun_out/micro_lat2.txt
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 timeout 900 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-configs > gpurun_out/plain.log 2>&1 && \
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -s 6000 -c 3000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-configs > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
