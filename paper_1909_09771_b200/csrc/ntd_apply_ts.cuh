@@ -14,7 +14,7 @@
 //
 // Solve record of one line (record-major, [system][line][RECD]), derived once
 // at setup from the factor (ntd_solve_bands):
-//   [ L2' | L3' | EFB (eF, eB pairs, 2 LR) | PREP (NPREP x 32, pairs) | U3' | U2' ]
+//   [ L3' | L2' | EFB (eF, eB pairs, 2 LR) | PREP (NPREP x 32, pairs) | U2' | U3' ]
 // eF / eB are the scaled elimination multipliers of the two-sided solve,
 // PREP the factor-only scan coefficients, and the couplings are pre-multiplied
 // by mu (the twisted pivot reciprocal at the cell): c' = c mu, as is the
@@ -29,13 +29,14 @@ namespace ts {
 
 constexpr int NPREP = 8;  // stored PrepTS coefficients per lane (m2 m4 m8 e, n2 n4 n8 f); m1 and n1 are rebuilt
 __host__ __device__ constexpr int lr_of(int K) { return 32 * K; }
-// record: [ L2' | L3' | EFB | PREP | U3' | U2' ] -- whatever a line step reads is one contiguous range
-__host__ __device__ constexpr int o_l2(int K) { return 0; }
-__host__ __device__ constexpr int o_l3(int K) { return lr_of(K); }
+// record: [ L3' | L2' | EFB | PREP | U2' | U3' ] -- whatever a line step reads is one contiguous range
+// (the in-plane couplings sit next to the block: an upper-sweep step copies nothing it does not read)
+__host__ __device__ constexpr int o_l3(int K) { return 0; }
+__host__ __device__ constexpr int o_l2(int K) { return lr_of(K); }
 __host__ __device__ constexpr int o_efb(int K) { return 2 * lr_of(K); }
 __host__ __device__ constexpr int o_prep(int K) { return 4 * lr_of(K); }
-__host__ __device__ constexpr int o_u3(int K) { return 4 * lr_of(K) + NPREP * 32; }
-__host__ __device__ constexpr int o_u2(int K) { return 5 * lr_of(K) + NPREP * 32; }
+__host__ __device__ constexpr int o_u2(int K) { return 4 * lr_of(K) + NPREP * 32; }
+__host__ __device__ constexpr int o_u3(int K) { return 5 * lr_of(K) + NPREP * 32; }
 __host__ __device__ constexpr int recd_of(int K) { return 6 * lr_of(K) + NPREP * 32; }
 // ring stage: [ record | X: b' or xo ]
 __host__ __device__ constexpr int rx_of(int K) { return recd_of(K); }
@@ -265,8 +266,8 @@ __device__ __forceinline__ void rec_copy(const TsArrays &S, const PlaneDesc &P, 
     // one range [lo, hi) (at most one unused coupling inside it)
     const bool l2 = ph == 1 || ((ph == 0) == (Q.w2 == 0)), u2 = ph == 1 || !l2;
     const bool l3 = ph < 2 && (P.two || P.c1 == o_l3(K)), u3 = ph < 2 && (P.two || P.c1 == o_u3(K));
-    const int lo = l2 ? o_l2(K) : l3 ? o_l3(K) : o_efb(K);
-    const int hi = u2 ? recd_of(K) : u3 ? o_u2(K) : o_u3(K);
+    const int lo = l3 ? o_l3(K) : l2 ? o_l2(K) : o_efb(K);
+    const int hi = u3 ? recd_of(K) : u2 ? o_u3(K) : o_u2(K);
     const bool extra = ph == 0 ? lower3 : ph == 1 ? true : !lower3;
     const double *xsrc = (lower3 ? S.b : S.x) + line * (i64)LR;
     mbar_expect_tx_a(bar, (unsigned)(hi - lo) * 8u + (extra ? lb : 0u));
@@ -925,7 +926,7 @@ __global__ void __launch_bounds__(128 * NP, 1) k_apply(const double *__restrict_
             P.two = true;
             P.hasM = t3 > 0;
             P.hasP = t3 < nz - 1;
-            P.c1 = o_l3(K);  // L3 then U3 (contiguous)
+            P.c1 = o_l3(K);  // (and U3 as the second coupling)
         } else {
             const int u = idx - nlow - ntw;
             const int p = pair == 0 ? t3 - 1 - u : t3 + 1 + u;
