@@ -116,7 +116,7 @@ __device__ __forceinline__ void sweep(const Sweep &w, const double *__restrict__
     const int lane = threadIdx.x & 31, warp = __shfl_sync(FULL_MASK, (int)(threadIdx.x >> 5), 0), W = blockDim.x >> 5;  // (provably warp-uniform)
     constexpr int NCF = FWD ? 3 : 4;
     constexpr int NOP = FWD ? 4 : ((OUT & 2) ? 6 : 5);  // operands per unit and step
-    constexpr int NO = NOP + (GL ? 1 : 0);             // (+ the speculative halo value)
+    constexpr int NO = NOP;
     const int G = w.G, Tu = w.T, U = w.U;
     const int rows = w.rows, zrow = w.rows - 1;
     // sweep-order index of this CTA's first plane; the CTA that receives our
@@ -164,28 +164,18 @@ __device__ __forceinline__ void sweep(const Sweep &w, const double *__restrict__
             d[4] = __ldcg(zf + (uu[j] * Tu + t) * 32 + lane);         // forward result
             if constexpr (has_ao) d[5] = ok ? accio[rb[j] + t] : 0.0;
         }
-        if constexpr (GL) {
-            // the halo this step will read (produced at its global step - 1)
-            if (lk.halo_in && mm[j] < G)
-                d[NOP] = ld_relaxed(lk.halo_in + ((tau + sm[j] - 1) % RING) * G * 32 + mm[j] * 32 + lane);
-        }
     };
+    // global-link mode: the halo value of a unit's NEXT step, requested one step ahead (not PF steps
+    // like the other operands: every step of look-ahead on the halo is a step of lag between
+    // consecutive CTAs of the wavefront, 47 times per sweep at 96^3)
+    double hnext[UPW];
+#pragma unroll
+    for (int j = 0; j < UPW; j++) hnext[j] = __longlong_as_double(-1ll);
     unsigned seen_succ = 0;  // (thread 0) last observed successor progress
     for (int T = -PF; T < w.S; T++) {
         const int cur = T & 1, prv = cur ^ 1;
         double *bc = buf + (size_t)cur * rows * 32, *bp = buf + (size_t)prv * rows * 32;
         // step tau of unit j with operand set op, then the loads of step tau + PF into op
-        if (GL && T >= 0 && lk.halo_out) {
-            // before slot T % RING is reused: the successor has completed the
-            // last step that read it (T - RING + 1)
-            const int need = T - RING + 2;
-            if (threadIdx.x == 0 && need > 0 && seen_succ < (unsigned)need) {
-                long long spins = 0;  // (a protocol error must not hang the GPU: fail the launch)
-                while ((seen_succ = ld_acquire(lk.flag_succ)) < (unsigned)need)
-                    if (++spins > (1ll << 28)) __trap();
-            }
-            __syncthreads();
-        }
         auto unit_step = [&](int j, int tau, double *op) {
             if (tau >= 0) {
                 const int m = mm[j], h = m % G;
@@ -203,13 +193,16 @@ __device__ __forceinline__ void sweep(const Sweep &w, const double *__restrict__
                     if constexpr (GL) {
                         if (lk.halo_in) {
                             double *slot = lk.halo_in + ((T - 1) % RING) * G * 32 + h * 32 + lane;
-                            zz = op[NOP];
+                            zz = hnext[j];
                             long long spins = 0;
                             while (is_empty_slot(zz)) {
                                 zz = ld_relaxed(slot);
                                 if (++spins > (1ll << 28)) __trap();
                             }
                             st_relaxed(slot, __longlong_as_double(-1ll));  // empty again
+                            // the next step's halo (slot T % RING), speculatively
+                            hnext[j] = tau + 1 < Tu ? ld_relaxed(lk.halo_in + (T % RING) * G * 32 + h * 32 + lane)
+                                                    : __longlong_as_double(-1ll);
                         }
                     }
                 } else {
@@ -267,6 +260,17 @@ __device__ __forceinline__ void sweep(const Sweep &w, const double *__restrict__
         HPT_NOW(t_w1);
         HPT_ADD(0, t_w1 - t_w0);
         if (GL || nc == 1) {
+            if (GL && lk.halo_out && T + 1 >= 0) {
+                // before slot (T + 1) % RING is reused by the next step: the successor has completed
+                // the last step that read it (T + 1 - RING + 1).  Checked by thread 0 ahead of this
+                // step's barrier, which then also holds the other warps back: one barrier per step.
+                const int need = T + 1 - RING + 2;
+                if (threadIdx.x == 0 && need > 0 && seen_succ < (unsigned)need) {
+                    long long spins = 0;  // (a protocol error must not hang the GPU: fail the launch)
+                    while ((seen_succ = ld_acquire(lk.flag_succ)) < (unsigned)need)
+                        if (++spins > (1ll << 28)) __trap();
+                }
+            }
             __syncthreads();
 #ifdef HP_TIMING
             { HPT_NOW(t_w2); HPT_ADD(2, t_w2 - t_w1); HPT_ADD(3, 1); }
