@@ -298,6 +298,16 @@ int ntd_ilu0_hp_apply(const double *coef, int64_t split, const double *r,
                       int64_t ny, int64_t nz, int64_t batch,
                       const int32_t *active, int64_t ctas_per_half,
                       int64_t warps_per_cta, void *stream);
+/* ntd_ilu0_hp_apply with the link mode chosen by the caller: links = 1 a
+ * thread-block cluster (<= 16 CTAs per half: boundary rows by DSMEM stores,
+ * a cluster barrier per step), 2 global-memory rings with sentinel values
+ * (cooperative launch, 2 * batch * ctas_per_half <= 148; what a lone system
+ * uses), 0 = 2 above 16 CTAs per half, else 1.  Bitwise the same result. */
+int ntd_ilu0_hp_apply_ex(const double *coef, int64_t split, const double *r,
+                         double *z, double *acc, double *work, int64_t nx,
+                         int64_t ny, int64_t nz, int64_t batch,
+                         const int32_t *active, int64_t ctas_per_half,
+                         int64_t warps_per_cta, int64_t links, void *stream);
 
 #ifdef __cplusplus
 }

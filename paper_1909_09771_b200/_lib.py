@@ -65,6 +65,7 @@ _SIGS = {
     "ntd_ilu0_skew_apply_ex": (_INT, [_P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _P]),
     "ntd_ilu0_hp_units": (_I, [_I, _I, _I, _I]),
     "ntd_ilu0_hp_apply": (_INT, [_P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _P]),
+    "ntd_ilu0_hp_apply_ex": (_INT, [_P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _I, _P]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -77,7 +78,7 @@ KERNELS_PER_CALL = {
     "ntd_apply": 3, "ntd_apply_ex": 3, "ntd_apply_direct": 1, "ntd_solve_bands": 1, "ntd_ilu0_factor": 2, "ntd_ilu0_apply": 1, "ntd_ilu0_skew_build": 1,
     "ntd_ilu0_skew_apply": 1, "ntd_ilu0_skew_apply_ex": 1, "ntd_sym_pack": 1, "ntd_residual_sym": 1, "ntd_pcg_spmv_alpha_sym": 2,
     "ntd_pcg_update_residual_sym": 3, "ntd_residual_to_slot": 1, "ntd_apply_slot": 1, "ntd_apply_slot_ex": 1,
-    "ntd_residual_from_slot": 1, "ntd_ilu0_hp_apply": 2,
+    "ntd_residual_from_slot": 1, "ntd_ilu0_hp_apply": 2, "ntd_ilu0_hp_apply_ex": 2,
 }
 _launches = [0]
 

@@ -363,16 +363,32 @@ extern "C" int64_t ntd_ilu0_hp_units(int64_t nx, int64_t ny, int64_t nz, int64_t
     return nk * G;  // units of the larger half
 }
 
+extern "C" int ntd_ilu0_hp_apply_ex(const double *coef, int64_t split, const double *r, double *z, double *acc,
+                                    double *work, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+                                    const int32_t *active, int64_t ctas_per_half, int64_t warps_per_cta,
+                                    int64_t links, void *stream);
+
 extern "C" int ntd_ilu0_hp_apply(const double *coef, int64_t split, const double *r, double *z, double *acc,
                                  double *work, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
                                  const int32_t *active, int64_t ctas_per_half, int64_t warps_per_cta, void *stream)
 {
+    return ntd_ilu0_hp_apply_ex(coef, split, r, z, acc, work, nx, ny, nz, batch, active, ctas_per_half,
+                                warps_per_cta, 0, stream);
+}
+
+// links: how the CTAs of a half exchange their boundary planes.  1: a thread-block cluster (<= 16 CTAs,
+// DSMEM stores, cluster barrier per step); 2: global-memory rings (cooperative launch, every CTA
+// resident: 2 * batch * CTAs <= 148); 0: 2 above 16 CTAs per half, else 1.
+extern "C" int ntd_ilu0_hp_apply_ex(const double *coef, int64_t split, const double *r, double *z, double *acc,
+                                    double *work, int64_t nx, int64_t ny, int64_t nz, int64_t batch,
+                                    const int32_t *active, int64_t ctas_per_half, int64_t warps_per_cta,
+                                    int64_t links, void *stream)
+{
     if (!coef || !r || !work || (!z && !acc) || nx < 1 || ny < 1 || nz < 1 || batch < 1) return NTD_EINVAL;
     const int nc = (int)ctas_per_half, W = (int)warps_per_cta;
-    if (nc < 1 || nc > 74 || W < 1 || W > 24) return NTD_EINVAL;
-    // more than 16 CTAs per half: global-memory links, every CTA on its own
-    // SM (cooperative launch)
-    const bool gl = nc > 16;
+    if (nc < 1 || nc > 74 || W < 1 || W > 24 || links < 0 || links > 2) return NTD_EINVAL;
+    if (links == 1 && nc > 16) return NTD_EINVAL;
+    const bool gl = nc > 1 && (links == 2 || (links == 0 && nc > 16));
     if (gl && 2 * batch * nc > 148) return NTD_EINVAL;
     const i64 nxy = nx * ny, G = (ny + 31) / 32, T = nx + 31;
     if (split % nxy != 0) return NTD_ENOTSUP;

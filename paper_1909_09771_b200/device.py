@@ -157,8 +157,8 @@ def _hp_warps(umax):
 
 
 def ilu0_hp_config(nx, ny, nz, split, systems_on_gpu):
-    """(CTAs per half, warps per CTA) of the hyperplane ILU0 kernel
-    (ntd_ilu0_hp_apply) for this grid, or None when the batch leaves it no
+    """(CTAs per half, warps per CTA[, link mode]) of the hyperplane ILU0 kernel
+    (ntd_ilu0_hp_apply_ex) for this grid, or None when the batch leaves it no
     room (then the skewed progress-word kernel, which needs one SM per half,
     is used: at 64 systems per GPU it is 1.8x faster alone and the whole
     batched solve runs 3-25% faster with it; at 8 systems the hyperplane
@@ -177,16 +177,19 @@ def ilu0_hp_config(nx, ny, nz, split, systems_on_gpu):
     if units <= 24:
         return 1, max(1, units)
     nc = min(16, budget, nk)
-    if systems_on_gpu == 1 and nk > 32:
-        # a lone large system: up to 74 CTAs per half (one per SM) linked
-        # through global memory (cooperative launch) beat a 16-CTA cluster
-        # (measured per apply: 96^3 0.50 vs 0.53 ms, 128^3 0.76 vs 0.85 ms,
-        # 350^3 2.95 ms on 74 CTAs vs 15.7 ms on 16 at 8 units per warp);
-        # 48 CTAs when that keeps one unit per warp
-        for ncg in (min(48, nk), min(74, nk)):
-            wu = _hp_warps(-(-nk // ncg) * g)
-            if wu is not None and (wu[1] == 1 or ncg == min(74, nk)):
-                return ncg, wu[0]
+    if systems_on_gpu == 1:
+        # a lone system: CTAs on separate SMs linked through global-memory
+        # rings (cooperative launch; third element 2 = that link mode) beat a
+        # cluster with its barrier per step, and with the halo requested one
+        # step ahead fewer, fuller CTAs beat many thin ones (every CTA of the
+        # chain adds a step of lag): about 12 units = warps per CTA, at most 74
+        # CTAs per half.  Measured per apply: 64^3 0.22 ms (cluster 0.27),
+        # 96^3 0.42 ms on 16-24 CTAs (0.45 on 48, cluster 0.53), 128^3 0.62 ms
+        # (0.65 on 48), 350^3 2.5 ms on 74 CTAs x 16 warps.
+        ncg = min(74, nk, -(-nk // max(1, 12 // g)))
+        wu = _hp_warps(-(-nk // ncg) * g)
+        if ncg > 1 and wu is not None:
+            return ncg, wu[0], 2
     while nc >= 2:
         wu = _hp_warps(-(-nk // nc) * g)
         if wu is not None:
@@ -220,8 +223,9 @@ def ilu0_apply(f_dev, split, r_dev, nx, ny, nz, batch, z=None, acc=None, active=
         if isinstance(hp, str):
             hp = ilu0_hp_config(nx, ny, nz, split, batch)
         if hp is not None:
-            _lib.call("ntd_ilu0_hp_apply", _lib.ptr(skew), split, _lib.ptr(r_dev), _lib.ptr(z), _lib.ptr(acc),
-                      _lib.ptr(work), nx, ny, nz, batch, _lib.ptr(active), hp[0], hp[1], _lib.stream())
+            _lib.call("ntd_ilu0_hp_apply_ex", _lib.ptr(skew), split, _lib.ptr(r_dev), _lib.ptr(z), _lib.ptr(acc),
+                      _lib.ptr(work), nx, ny, nz, batch, _lib.ptr(active), hp[0], hp[1],
+                      hp[2] if len(hp) > 2 else 0, _lib.stream())
             return z
         nc, nw = ilu0_ctas(batch) if ctas is None else ctas
         _lib.call("ntd_ilu0_skew_apply_ex", _lib.ptr(skew), split, _lib.ptr(r_dev), _lib.ptr(z), _lib.ptr(acc),

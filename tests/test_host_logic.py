@@ -1,6 +1,6 @@
 """Host-side launch-mapping logic (no GPU needed): every mapping the
 package picks for the hyperplane ILU0 kernel is one the kernel accepts
-(include/ntdgpu.h ntd_ilu0_hp_apply limits), across grids and batch sizes."""
+(include/ntdgpu.h ntd_ilu0_hp_apply_ex limits), across grids and batch sizes."""
 
 import pytest
 
@@ -20,7 +20,8 @@ def test_hp_mappings_within_kernel_limits(grid):
             cfg = D.ilu0_hp_config(nx, ny, nz, split, systems)
             if cfg is None:
                 continue
-            nc, w = cfg
+            nc, w = cfg[:2]
+            links = cfg[2] if len(cfg) > 2 else 0
             g = (ny + 31) // 32
             nxy = nx * ny
             assert split % nxy == 0
@@ -29,7 +30,9 @@ def test_hp_mappings_within_kernel_limits(grid):
             upw = -(-umax // w)
             assert 1 <= nc <= nk and umax <= 380 and 1 <= upw <= 8
             assert w <= (24 if upw == 1 else 16)
-            if nc > 16:  # global-memory links: a lone system, one CTA per SM
+            if nc > 16 or links == 2:  # global-memory links: a lone system, one CTA per SM
                 assert systems == 1 and 2 * systems * nc <= 148
+            else:
+                assert links in (0, 1)
     assert D.ilu0_hp_config(96, 96, 96, 96 ** 3 // 2, 64) is None  # the batch keeps the skewed kernel
     assert D.ilu0_hp_config(350, 350, 350, 350 ** 3 // 2, 1)[0] > 16

@@ -14,6 +14,8 @@ from paper_1909_09771_b200 import _lib, problems  # noqa: E402
 from paper_1909_09771_b200 import device as D  # noqa: E402
 from paper_1909_09771_b200.batch import BatchSolver  # noqa: E402
 
+if os.environ.get("VARIANT_LIB"):  # experiments: a variant build (tools/variant_lib.sh)
+    _lib.LIB_PATH = os.environ["VARIANT_LIB"]
 policy = sys.argv[1] if len(sys.argv) > 1 else "auto"
 S = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 GROUPS = int(sys.argv[3]) if len(sys.argv) > 3 else None

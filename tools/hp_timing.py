@@ -23,7 +23,7 @@ skew = D.ilu0_skew_build(f, split, nx, ny, nz, 1)
 work = torch.empty(_lib.load().ntd_ilu0_skew_work_doubles(nx, ny, nz, 1), dtype=torch.float64, device="cuda")
 v = torch.rand((1, n), dtype=torch.float64, device="cuda")
 z = torch.empty_like(v)
-hp = (int(sys.argv[2]), int(sys.argv[3])) if len(sys.argv) > 3 else D.ilu0_hp_config(nx, ny, nz, split, 1)
+hp = (int(sys.argv[2]), int(sys.argv[3])) + ((int(sys.argv[4]),) if len(sys.argv) > 4 else ()) if len(sys.argv) > 3 else D.ilu0_hp_config(nx, ny, nz, split, 1)
 lib = _lib.load()
 lib.ntd_hp_timing.argtypes = [ctypes.c_void_p, ctypes.c_int]
 buf = (ctypes.c_ulonglong * 128)()

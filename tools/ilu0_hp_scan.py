@@ -15,6 +15,7 @@ from paper_1909_09771_b200 import device as D  # noqa: E402
 if os.environ.get("VARIANT_LIB"):  # experiments: a variant build (tools/variant_lib.sh)
     _lib.LIB_PATH = os.environ["VARIANT_LIB"]
 QUICK = os.environ.get("QUICK") == "1"  # only the auto hp mapping
+LINKS = int(os.environ.get("LINKS", "0"))  # 1 cluster, 2 global-memory links, 0 the kernel's default
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 S = int(sys.argv[2]) if len(sys.argv) > 2 else 1
@@ -71,8 +72,9 @@ for nc in (1, 2, 4, 8, 16, 24, 37, 48, 74):
             continue
         z = torch.empty_like(v)
         try:
-            t = timed(lambda: D.ilu0_apply(f, split, v, nx, ny, nz, S, z=z, skew=skew, work=work, hp=(nc, w)))
+            hp = (nc, w, LINKS) if LINKS else (nc, w)
+            t = timed(lambda: D.ilu0_apply(f, split, v, nx, ny, nz, S, z=z, skew=skew, work=work, hp=hp))
         except Exception as exc:  # noqa: BLE001
-            print(f"  hp ({nc},{w}) upw {upw}: FAILED {exc}", flush=True)
+            print(f"  hp {hp} upw {upw}: FAILED {exc}", flush=True)
             continue
-        print(f"  hp ({nc},{w}) upw {upw}: {t:.3f} ms  bitwise={torch.equal(z, z_ref)}", flush=True)
+        print(f"  hp {hp} upw {upw}: {t:.3f} ms  bitwise={torch.equal(z, z_ref)}", flush=True)
