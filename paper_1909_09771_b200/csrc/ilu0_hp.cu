@@ -31,11 +31,14 @@
 namespace hp {
 
 #ifdef HP_TIMING
-// per-warp cycle accounting of CTA 0 (experiments): [warp][0 work, 1 loads, 2 barrier, 3 steps]
+#ifndef HP_TIMING_BLOCK
+#define HP_TIMING_BLOCK 0
+#endif
+// per-warp cycle accounting of one CTA (experiments): [warp][0 work, 1 loads, 2 barrier, 3 steps]
 __device__ unsigned long long g_hp_timing[32][4];
 #define HPT_NOW(v) const long long v = clock64()
 #define HPT_ADD(k, val) \
-    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) g_hp_timing[threadIdx.x >> 5][k] += (unsigned long long)(val)
+    if (blockIdx.x == HP_TIMING_BLOCK && (threadIdx.x & 31) == 0) g_hp_timing[threadIdx.x >> 5][k] += (unsigned long long)(val)
 #else
 #define HPT_NOW(v)
 #define HPT_ADD(k, val)
@@ -267,7 +270,7 @@ __device__ __forceinline__ void sweep(const Sweep &w, const double *__restrict__
                 const int need = T + 1 - RING + 2;
                 if (threadIdx.x == 0 && need > 0 && seen_succ < (unsigned)need) {
                     long long spins = 0;  // (a protocol error must not hang the GPU: fail the launch)
-                    while ((seen_succ = ld_acquire(lk.flag_succ)) < (unsigned)need)
+                    while ((seen_succ = ~ld_acquire(lk.flag_succ)) < (unsigned)need)
                         if (++spins > (1ll << 28)) __trap();
                 }
             }
@@ -278,7 +281,7 @@ __device__ __forceinline__ void sweep(const Sweep &w, const double *__restrict__
             // progress for the predecessor's slot reuse (our slot resets are
             // ordered before it: CTA barrier, then a release by thread 0)
             if (GL && lk.halo_in && threadIdx.x == 0 && T >= 0 && (T % PUBLISH == PUBLISH - 1 || T == w.S - 1))
-                st_release(lk.flag_self, (unsigned)T + 1);
+                st_release(lk.flag_self, ~((unsigned)T + 1));
         } else {
             cluster_arrive();
             cluster_wait();
@@ -323,13 +326,15 @@ __global__ void __launch_bounds__(HpTraits<UPW>::MAXT, 1)
     for (int e = threadIdx.x; e < 2 * w.rows * 32; e += blockDim.x) hp_buf[e] = 0.0;
     Link lk = {nullptr, nullptr, nullptr, nullptr};
     if (GL) {
-        // glbuf: [batch][2 halves][nc boundaries][RING][G][32] rings (filled
-        // with the empty sentinel by the host), then the [batch][2][nc]
-        // progress words (zeroed)
+        // glbuf: [batch][2 halves][nc boundaries][RING][G][32] rings, then two sets (forward sweep,
+        // backward sweep) of [batch][2][nc] progress words; the host fills all of it with 0xff
         const size_t ring = (size_t)RING * w.G * 32;
         const i64 hs = sys * 2 + half;  // this system half
         double *rings = glbuf + (size_t)hs * nc * ring;
-        unsigned *flags = (unsigned *)(glbuf + (size_t)gridDim.x / nc * nc * ring) + hs * nc;
+        // progress words are stored complemented (all-ones = no step done), one set per sweep, so a
+        // single 0xff fill before the forward sweep prepares the rings (empty sentinel) and both sets;
+        // every ring slot is consumed and reset by its reader, so the backward sweep finds them empty
+        unsigned *flags = (unsigned *)(glbuf + (size_t)gridDim.x / nc * nc * ring) + (FWD ? 0 : gridDim.x) + hs * nc;
         const int pred = FWD ? crank - 1 : crank + 1, succ = FWD ? crank + 1 : crank - 1;
         // boundary b lies between CTAs b and b + 1
         if (pred >= 0 && pred < nc) lk.halo_in = rings + (size_t)(FWD ? pred : crank) * ring;
@@ -442,9 +447,9 @@ extern "C" int ntd_ilu0_hp_apply_ex(const double *coef, int64_t split, const dou
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess && !gl && nc > 8)
             e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e == cudaSuccess && gl) e = cudaMemsetAsync(glbuf, 0xff, sizeof(double) * ring_doubles, st);
-        if (e == cudaSuccess && gl)
-            e = cudaMemsetAsync(glbuf + ring_doubles, 0, sizeof(unsigned) * 2 * batch * nc, st);
+        if (e == cudaSuccess && gl && pass == 0)
+            e = cudaMemsetAsync(glbuf, 0xff, sizeof(double) * ring_doubles + sizeof(unsigned) * 2 * (2 * batch * nc),
+                                st);
         if (e != cudaSuccess) {
             ntd::set_error("ilu0 hp apply attributes", e);
             return NTD_ELAUNCH;
