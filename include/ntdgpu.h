@@ -301,7 +301,8 @@ int ntd_ilu0_hp_apply(const double *coef, int64_t split, const double *r,
 /* ntd_ilu0_hp_apply with the link mode chosen by the caller: links = 1 a
  * thread-block cluster (<= 16 CTAs per half: boundary rows by DSMEM stores,
  * a cluster barrier per step), 2 global-memory rings with sentinel values
- * (cooperative launch, 2 * batch * ctas_per_half <= 148; what a lone system
+ * (a cluster launch up to 16 CTAs per half, a cooperative launch with
+ * 2 * batch * ctas_per_half <= 148 above; what a lone system
  * uses), 0 = 2 above 16 CTAs per half, else 1.  Bitwise the same result. */
 int ntd_ilu0_hp_apply_ex(const double *coef, int64_t split, const double *r,
                          double *z, double *acc, double *work, int64_t nx,

@@ -394,7 +394,7 @@ extern "C" int ntd_ilu0_hp_apply_ex(const double *coef, int64_t split, const dou
     if (nc < 1 || nc > 74 || W < 1 || W > 24 || links < 0 || links > 2) return NTD_EINVAL;
     if (links == 1 && nc > 16) return NTD_EINVAL;
     const bool gl = nc > 1 && (links == 2 || (links == 0 && nc > 16));
-    if (gl && 2 * batch * nc > 148) return NTD_EINVAL;
+    if (gl && nc > 16 && 2 * batch * nc > 148) return NTD_EINVAL;
     const i64 nxy = nx * ny, G = (ny + 31) / 32, T = nx + 31;
     if (split % nxy != 0) return NTD_ENOTSUP;
     const i64 ks = split / nxy, nk = ks > nz - ks ? ks : nz - ks;
@@ -445,7 +445,11 @@ extern "C" int ntd_ilu0_hp_apply_ex(const double *coef, int64_t split, const dou
     for (int pass = 0; pass < 2; pass++) {
         Kern k = pass == 0 ? kf : kb;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess && !gl && nc > 8)
+        // global links need every CTA of a half resident at once: up to 16 CTAs a thread-block cluster
+        // guarantees that (a plain cluster launch costs less than a cooperative one), above that a
+        // cooperative launch
+        const bool coop = gl && nc > 16;
+        if (e == cudaSuccess && !coop && nc > 8)
             e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e == cudaSuccess && gl && pass == 0)
             e = cudaMemsetAsync(glbuf, 0xff, sizeof(double) * ring_doubles + sizeof(unsigned) * 2 * (2 * batch * nc),
@@ -460,7 +464,7 @@ extern "C" int ntd_ilu0_hp_apply_ex(const double *coef, int64_t split, const dou
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
-        if (gl) {
+        if (coop) {
             attr[0].id = cudaLaunchAttributeCooperative;
             attr[0].val.cooperative = 1;
         } else {
