@@ -177,16 +177,21 @@ def ilu0_hp_config(nx, ny, nz, split, systems_on_gpu):
     if units <= 24:
         return 1, max(1, units)
     nc = min(16, budget, nk)
-    if systems_on_gpu == 1:
-        # a lone system: CTAs on separate SMs linked through global-memory
-        # rings (cooperative launch; third element 2 = that link mode) beat a
-        # cluster with its barrier per step, and with the halo requested one
-        # step ahead fewer, fuller CTAs beat many thin ones (every CTA of the
-        # chain adds a step of lag): about 12 units = warps per CTA, at most 74
-        # CTAs per half.  Measured per apply: 64^3 0.22 ms (cluster 0.27),
-        # 96^3 0.42 ms on 16-24 CTAs (0.45 on 48, cluster 0.53), 128^3 0.62 ms
-        # (0.65 on 48), 350^3 2.5 ms on 74 CTAs x 16 warps.
-        ncg = min(74, nk, -(-nk // max(1, 12 // g)))
+    if systems_on_gpu <= 8:
+        # up to 8 systems per GPU: CTAs linked through global-memory rings
+        # (third element 2 = that link mode) beat a cluster with its barrier
+        # per step, and with the halo requested one step ahead fewer, fuller
+        # CTAs beat many thin ones (every CTA of the chain adds a step of lag):
+        # about 12 units = warps per CTA; at most 74 CTAs per half for a lone
+        # system (cooperative launch), 16 otherwise (a cluster launch keeps the
+        # CTAs of a half co-resident).  Measured per apply, one system: 64^3
+        # 0.22 ms (cluster 0.27), 96^3 0.41 ms on 12-24 CTAs (0.45 on 48,
+        # cluster 0.53), 128^3 0.62 ms, 350^3 2.5 ms on 74 CTAs x 16 warps;
+        # whole solves at 2 / 4 / 8 systems: 604 / 1082 / 2058 Munk-iter/s
+        # against 563 / 1004 / 1921 with clusters (at 16 systems 2857 against
+        # 2940, so the cluster mapping below stays there).
+        cap = 74 if systems_on_gpu == 1 else 16
+        ncg = min(cap, nk, -(-nk // max(1, 12 // g)))
         wu = _hp_warps(-(-nk // ncg) * g)
         if ncg > 1 and wu is not None:
             return ncg, wu[0], 2

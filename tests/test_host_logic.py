@@ -30,8 +30,10 @@ def test_hp_mappings_within_kernel_limits(grid):
             upw = -(-umax // w)
             assert 1 <= nc <= nk and umax <= 380 and 1 <= upw <= 8
             assert w <= (24 if upw == 1 else 16)
-            if nc > 16 or links == 2:  # global-memory links: a lone system, one CTA per SM
+            if nc > 16:  # global-memory links, cooperative launch: a lone system, one CTA per SM
                 assert systems == 1 and 2 * systems * nc <= 148
+            elif links == 2:  # global-memory links inside a cluster launch
+                assert systems <= 8
             else:
                 assert links in (0, 1)
     assert D.ilu0_hp_config(96, 96, 96, 96 ** 3 // 2, 64) is None  # the batch keeps the skewed kernel

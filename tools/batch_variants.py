@@ -1,7 +1,7 @@
 """Config-4 batch (64 x 96^3) solve rate under different ILU0 / NTD mapping
 policies (experiments; the product picks them in device.ilu0_hp_config /
 ilu0_ctas / ntd_ctas).  python tools/batch_variants.py policy [systems] [groups]
-policies: auto, skew, hp:nc:w (fixed), hpmin (hp whenever it fits)."""
+policies: auto, skew, hp:nc:w[:links] (fixed), hpmin (hp whenever it fits)."""
 import os
 import sys
 import time
@@ -23,8 +23,8 @@ orig = D.ilu0_hp_config
 if policy == "skew":
     D.ilu0_hp_config = lambda *a, **k: None
 elif policy.startswith("hp:"):
-    _, nc, w = policy.split(":")
-    D.ilu0_hp_config = lambda *a, **k: (int(nc), int(w))
+    cfg_ = tuple(int(v) for v in policy.split(":")[1:])  # nc, w[, links]
+    D.ilu0_hp_config = lambda *a, **k: cfg_
 elif policy == "hpmin":
     D.ilu0_hp_config = lambda nx, ny, nz, split, systems: orig(nx, ny, nz, split, 1)
 nx, ny, nz = problems.CONFIGS[4]["grid"]
