@@ -258,6 +258,10 @@ def test_sm_mappings_bitwise(ntd):
                 D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, 2, z=z, acc=acc, skew=P.skew, work=work, hp=(nc, w))
                 assert torch.equal(z, z_ref), (nx, ny, nz, nc, w)
                 assert torch.equal(acc, z_ref + 0.5), (nx, ny, nz, nc, w)
+                if 1 < nc <= 16:  # the same mapping with global-memory rings inside a cluster launch
+                    z3 = torch.empty_like(v)
+                    D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, 2, z=z3, skew=P.skew, work=work, hp=(nc, w, 2))
+                    assert torch.equal(z3, z_ref), (nx, ny, nz, nc, w, "global links")
                 z2 = torch.empty_like(v)
                 D.ilu0_apply(P.ilu, P.split, v, nx, ny, nz, 2, z=z2, skew=P.skew, work=work, hp=(nc, w))
                 assert torch.equal(z2, z_ref), (nx, ny, nz, nc, w)
