@@ -56,11 +56,6 @@ __host__ __device__ constexpr int depth_smb_of(int K)
 }
 
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
-__device__ __forceinline__ void mbar_arrive(void *bar)
-{
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
 // element of cell c inside its TS record / cell of element r (-1: padding)
 __host__ __device__ __forceinline__ int ts_index(int c, int K) { return (c % K) * 32 + c / K; }
 __host__ __device__ __forceinline__ int ts_cell(int r, int nx, int K)
@@ -223,19 +218,6 @@ __global__ void k_prep_ts(double *__restrict__ solve, i64 lines_total)
 //   lower sweep:  block, in-plane coupling (L2' / U2' by half), C1 (+C2), b' (LOWER3)
 //   twist line:   block, L2', U2', C1 (+C2), b' (LOWER3) / xo (UPPER3)
 //   upper sweep:  block, in-plane coupling (U2' / L2'), xo (UPPER3)
-__device__ __forceinline__ void mbar_wait_producer(void *bar, unsigned parity)
-{
-    unsigned ok = 0;
-    const unsigned a = smem_u32(bar);
-    while (!ok) {
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
-            : "=r"(ok)
-            : "r"(a), "r"(parity), "r"(1000000u)
-            : "memory");
-    }
-}
-
 __device__ __forceinline__ void mbar_wait_a(unsigned bar, unsigned parity);
 __device__ __forceinline__ void mbar_expect_tx_a(unsigned bar, unsigned bytes)
 {
@@ -399,28 +381,6 @@ __device__ __forceinline__ void st_buf(BA a, const double (&v)[K])
 #pragma unroll
     for (int k = 0; k < K; k++) stb(adv(a, k * 256), v[k]);
 }
-// sa16: stage address + lane * 16
-template <int K>
-__device__ __forceinline__ void ld_efb(Ops<K> &o, unsigned sa16)
-{
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-        const double2 v = lds2(sa16 + o_efb(K) * 8 + k * 512);
-        o.eF[k] = v.x;
-        o.eB[k] = v.y;
-    }
-}
-template <int K>
-__device__ __forceinline__ void ld_prep(Ops<K> &o, unsigned sa16)
-{
-#pragma unroll
-    for (int c = 0; c < NPREP / 2; c++) {
-        const double2 v = lds2(sa16 + o_prep(K) * 8 + c * 512);
-        o.pr[2 * c] = v.x;
-        o.pr[2 * c + 1] = v.y;
-    }
-}
-
 template <int A, int B, class F>
 __device__ __forceinline__ void static_for(F &&f)
 {
