@@ -621,25 +621,45 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
         }
     };
     // PIPE (narrow lines): step r solves record r while the operands of record r+1 are loaded behind
-    // its shuffle rounds.  Wide lines (K > 5) do not have the registers for two operand sets: a step
-    // loads its own record first, and only the neighbour-plane / lower-sweep values, which may come
-    // from global memory, are requested one line ahead.
+    // its shuffle rounds, in five equal shares.  Wide lines (K > 5) do not have the registers for two
+    // whole operand sets; their loads follow the registers as the line solve frees them: the rhs part
+    // and cp of record r die with rho, eF / eB with the lane maps, so record r+1's couplings, then its
+    // rhs part, then its eF / eB are loaded behind rounds 0..4, while its scan coefficients (and xo)
+    // are read in its own step behind round 0, after which the stage is released.  Neighbour-plane
+    // values, which come from global memory, are requested two lines ahead (wn).
     constexpr bool PIPE = K <= 5;
     const unsigned cpT = (unsigned)o_l2(K) * 8 + l8;  // the twist record is read with L2' as cp
     Ops<K> cur;
-    Raw<K> wn;  // wide lines: neighbour values of the next lower-type record
+    Raw<K> wn;  // wide lines: couplings of the next lower-type record, neighbour values of the one after
     bool okn = true;
-    bool okw = false;  // wide lines: this step's record was seen complete by the previous step's test
+    auto ld_pr = [&](Ops<K> &o, unsigned s) {
+#pragma unroll
+        for (int j = 0; j < NPREP / 2; j++) {
+            const double2 v = lds2(s + l16 + o_prep(K) * 8 + j * 512);
+            o.pr[2 * j] = v.x;
+            o.pr[2 * j + 1] = v.y;
+        }
+    };
+    auto ld_efb = [&](auto A, auto B, Ops<K> &o, unsigned s) {
+        static_for<decltype(A)::value, decltype(B)::value>([&](auto J) {
+            constexpr int j = decltype(J)::value;
+            const double2 v = lds2(s + l16 + o_efb(K) * 8 + j * 512);
+            o.eF[j] = v.x;
+            o.eB[j] = v.y;
+        });
+    };
+    const std::integral_constant<int, 0> I0{};
+    const std::integral_constant<int, (K + 1) / 2> IH{};
+    const std::integral_constant<int, K> IK{};
     // ---------------- prologue: the plane's first record (a lower line, or the twist line when cnt == 0)
-    if constexpr (PIPE) {
+    {
         Raw<K> w;
         mbar_wait_a(full(rec), par(rec));
         load_L(ALL, WITH_N, cur, w, sa(rec), yn, y2p, cpL);
-        mbar_arrive_if(empty(rec), lane == 0 && cnt > 0);  // the twist record releases itself
+        if constexpr (PIPE) mbar_arrive_if(empty(rec), lane == 0 && cnt > 0);  // the twist record releases itself
         okn = mbar_test_a(full(rec + 1), par(rec + 1));
         fin_L(cur, w);
-    } else {
-        nbr_L(wn, yn, y2p);
+        if constexpr (!PIPE) nbr_L(wn, cnt > 0 ? adv(yn, dqB) : yn, cnt > 0 ? y2p + dq * LR : y2p);
     }
     // ---------------- level-2 lower sweep (ntd_solve.py:147-171)
     double xprev[K];
@@ -650,23 +670,37 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
         Ops<K> nxt;
         Raw<K> w;
         const bool last = i == cnt - 1;  // the next record is the twist line (an L-type record as well)
-        if constexpr (!PIPE) {
-            if (!okw) mbar_wait_a(full(rec), par(rec));  // (tested during the previous step)
-            load_L(ALL, NO_N, cur, wn, sa(rec), yn, y2p, cpL);
-            mbar_arrive_if(empty(rec), lane == 0);
-            fin_L(cur, wn);
-        }
         // (checked here, at a block boundary: a branch inside the line solve splits its straight-line
         // code and costs ~65 cycles per step)
-        if (PIPE && !okn) mbar_wait_a(full(rec + 1), par(rec + 1));
+        if (!okn) mbar_wait_a(full(rec + 1), par(rec + 1));
+        // wide lines: neighbour values two lines ahead (the twist line is the last lower-type record)
+        const BA yn2 = last ? yn : adv(yn, 2 * dqB);
+        const double *y2q2 = last ? y2p : y2p + 2 * dq * LR;
+        const unsigned sn = sa(rec + 1), cpn = last ? cpT : cpL;
         double rho[K], x[K];
 #pragma unroll
         for (int k = 0; k < K; k++) rho[k] = fma(-cur.cp[k], xprev[k], cur.pt[k]);  // line 0: xprev = 0
         solve_line<K, false>(cur, lane, rho, x, [&](auto J) {
             constexpr int j = decltype(J)::value;
             if constexpr (!PIPE) {
-                if constexpr (j == 0) nbr_L(wn, adv(yn, dqB), y2p + dq * LR);
-                if constexpr (j == NHOOK) okw = mbar_test_a(full(rec + 1), par(rec + 1));
+                if constexpr (j == 0) {
+                    ld_pr(cur, sa(rec));
+                    mbar_arrive_if(empty(rec), lane == 0);
+                    ld_row(wn.c1, sn + c1o);
+                } else if constexpr (j == 1) {
+                    if constexpr (lower3) ld_row(wn.bx, sn + rx_of(K) * 8 + l8);
+                    if constexpr (TWO) ld_row(wn.c2, sn + o_u3(K) * 8 + l8);
+                } else if constexpr (j == 2) {
+                    fin_L(nxt, wn);
+                    nbr_L(wn, yn2, y2q2);
+                    ld_row(nxt.cp, sn + cpn);
+                } else if constexpr (j == 3) {
+                    ld_efb(I0, IH, nxt, sn);
+                } else if constexpr (j == 4) {
+                    ld_efb(IH, IK, nxt, sn);
+                } else {
+                    okn = mbar_test_a(full(rec + 2), par(rec + 2));
+                }
             } else if constexpr (j < NHOOK) {
                 load_L(J, WITH_N, nxt, w, sa(rec + 1), adv(yn, dqB), y2p + dq * LR, last ? cpT : cpL);
             } else {
@@ -677,10 +711,8 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
         st_buf(xl, x);
 #pragma unroll
         for (int k = 0; k < K; k++) xprev[k] = x[k];
-        if constexpr (PIPE) {
-            fin_L(nxt, w);
-            cur = nxt;
-        }
+        if constexpr (PIPE) fin_L(nxt, w);
+        cur = nxt;
         xl = adv(xl, dqB);
         yn = adv(yn, dqB);
         y2p += dq * LR;
@@ -700,15 +732,11 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
     double ycur[K], xocur[K];
     {
         double u2c[K], xo[K];
-        if constexpr (!PIPE) {
-            if (!okw) mbar_wait_a(full(rec), par(rec));
-            load_L(ALL, NO_N, cur, wn, sa(rec), yn, y2p, cpT);
-            fin_L(cur, wn);
-        }
+        if constexpr (!PIPE) ld_pr(cur, sa(rec));
         ld_row(u2c, sa(rec) + o_u2(K) * 8 + l8);
         if (!lower3) ld_row(xo, sa(rec) + rx_of(K) * 8 + l8);
         mbar_arrive_if(empty(rec), lane == 0);
-        if (PIPE && cnt > 0 && !okn) mbar_wait_a(full(rec + 1), par(rec + 1));
+        if (cnt > 0 && !okn) mbar_wait_a(full(rec + 1), par(rec + 1));
         double rho[K];
 #pragma unroll
         for (int k = 0; k < K; k++) {
@@ -722,8 +750,11 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
             constexpr int j = decltype(J)::value;
             if (cnt > 0) {
                 if constexpr (!PIPE) {
-                    if constexpr (j == 0) ld_buf(ycur, adv(xl, -dqB));
-                    if constexpr (j == NHOOK) okw = mbar_test_a(full(rec + 1), par(rec + 1));
+                    if constexpr (j == 0) ld_row(nxt.cp, sa(rec + 1) + cpU);
+                    if constexpr (j == 1) ld_buf(ycur, adv(xl, -dqB));
+                    if constexpr (j == 3) ld_efb(I0, IH, nxt, sa(rec + 1));
+                    if constexpr (j == 4) ld_efb(IH, IK, nxt, sa(rec + 1));
+                    if constexpr (j == NHOOK) okn = mbar_test_a(full(rec + 2), par(rec + 2));
                 } else if constexpr (j < NHOOK) {
                     load_U(J, WITH_N, nxt, ycur, xocur, sa(rec + 1), adv(xl, -dqB));
                 } else {
@@ -744,20 +775,14 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
     }
     // ---------------- level-2 upper sweep (ntd_solve.py:178-185)
     //   value_q = y_q - T_q^{-1}(cp' value_prev);  LOWER3: x_q = value_q;  UPPER3: x_q = xo_q - value_q
-    if constexpr (PIPE) cur = nxt;
+    cur = nxt;
     BA xu = adv(xl, -dqB);
     double *xg = xpl + (i64)(t2 - dq) * LR;
 #pragma unroll 1
     for (int i = 0; i < cnt; i++, rec++) {
         const bool more = i + 1 < cnt;
         double ynx[K], xonx[K];
-        if constexpr (!PIPE) {
-            double dummy[K];
-            if (!okw) mbar_wait_a(full(rec), par(rec));
-            load_U(ALL, NO_N, cur, dummy, xocur, sa(rec), xu);
-            mbar_arrive_if(empty(rec), lane == 0);
-        }
-        if (PIPE && more && !okn) mbar_wait_a(full(rec + 1), par(rec + 1));
+        if (more && !okn) mbar_wait_a(full(rec + 1), par(rec + 1));
         double rho[K];
 #pragma unroll
         for (int k = 0; k < K; k++) rho[k] = cur.cp[k] * xn[k];
@@ -767,8 +792,20 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
         solve_line<K, true>(cur, lane, rho, xn, [&](auto J) {
             constexpr int j = decltype(J)::value;
             if constexpr (!PIPE) {
-                if constexpr (j == 0) ld_buf(ynx, adv(xu, -dqB));
-                if constexpr (j == NHOOK) okw = more && mbar_test_a(full(rec + 1), par(rec + 1));
+                if constexpr (j == 0) {
+                    ld_pr(cur, sa(rec));
+                    if constexpr (!lower3) ld_row(xocur, sa(rec) + rx_of(K) * 8 + l8);
+                    mbar_arrive_if(empty(rec), lane == 0);
+                    ld_row(nxt.cp, sa(rec + 1) + cpU);
+                } else if constexpr (j == 1) {
+                    ld_buf(ynx, adv(xu, -dqB));
+                } else if constexpr (j == 3) {
+                    ld_efb(I0, IH, nxt, sa(rec + 1));
+                } else if constexpr (j == 4) {
+                    ld_efb(IH, IK, nxt, sa(rec + 1));
+                } else if constexpr (j == NHOOK) {
+                    okn = mbar_test_a(full(rec + 2), par(rec + 2));
+                }
             } else if constexpr (j < NHOOK) {
                 load_U(J, WITH_N, nxt, ynx, xonx, sa(rec + 1), adv(xu, -dqB));
             } else {
@@ -784,8 +821,8 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
         if constexpr (SMB) st_buf(xu, nv);
 #pragma unroll
         for (int k = 0; k < K; k++) ycur[k] = ynx[k];
+        cur = nxt;
         if constexpr (PIPE) {
-            cur = nxt;
 #pragma unroll
             for (int k = 0; k < K; k++) xocur[k] = xonx[k];
         }
