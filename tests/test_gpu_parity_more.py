@@ -57,7 +57,10 @@ def lognormal_grid(nx, ny, nz, seed):
 # shared-memory plane buffer: 20x40, 40x70 take the ring kernel with global neighbour lines)
 K_GRIDS = [(20, 9, 7), (40, 11, 6), (96, 10, 5), (120, 7, 6), (150, 9, 5), (180, 6, 5), (250, 7, 4),
            (350, 5, 4), (400, 5, 3), (500, 4, 3), (95, 4, 3), (97, 3, 3), (33, 2, 2), (161, 3, 2), (65, 1, 4),
-           (31, 5, 1), (20, 40, 3), (40, 70, 2), (200, 200, 2)]
+           (31, 5, 1), (20, 40, 3), (40, 70, 2), (200, 200, 2),
+           # wide lines (K > 5) on planes of 1, 2 and 3 lines and on a single plane: the pipelined loads'
+           # first / last steps (prologue, twist line alone, look-ahead past the sweep)
+           (170, 1, 3), (170, 2, 3), (230, 2, 1), (340, 1, 1), (340, 3, 5), (352, 4, 2)]
 
 
 @pytest.mark.parametrize("grid", K_GRIDS, ids=[f"nx{g[0]}" for g in K_GRIDS])
