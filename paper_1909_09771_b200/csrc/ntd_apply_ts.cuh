@@ -537,8 +537,8 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
     //   upper-type record: cp, y, [xo], eF|eB pairs, scan coefficient pairs
     constexpr int NL_L = K * (4 + (lower3 ? 1 : 0) + (TWO ? 2 : 0)) + NPREP / 2;
     constexpr int NL_U = K * (3 + (lower3 ? 0 : 1)) + NPREP / 2;
-    // (WN = false: without the neighbour-plane / lower-sweep values, which the wide-line mode requests
-    // one line ahead through nbr_L / nbr_U)
+    // (narrow lines; wide lines use the lists only for a plane's first record and place their loads
+    // by register lifetime, below)
     auto item_L = [&](auto I, auto WN, Ops<K> &o, Raw<K> &w, unsigned s, BA ya, const double *y2q, unsigned cpo) {
         constexpr int i = decltype(I)::value;
         constexpr bool wn = decltype(WN)::value;
@@ -593,7 +593,6 @@ __device__ void solve_plane(const TsArrays &S, const PlaneDesc &P, const Seq &Q,
         }
     };
     const std::integral_constant<bool, true> WITH_N{};
-    const std::integral_constant<bool, false> NO_N{};
     auto load_L = [&](auto J, auto WN, Ops<K> &o, Raw<K> &w, unsigned s, BA ya, const double *y2q, unsigned cpo) {
         constexpr int j = decltype(J)::value;
         constexpr int a = j < 0 ? 0 : j * NL_L / NHOOK, b = j < 0 ? NL_L : (j + 1) * NL_L / NHOOK;
