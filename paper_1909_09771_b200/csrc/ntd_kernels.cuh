@@ -491,6 +491,19 @@ __global__ void __launch_bounds__(128) k_ntd_apply(const double *__restrict__ pr
 // walked sequentially), every operation exactly rounded in the reference's
 // order.  The resulting factor is bitwise equal to the reference's.
 constexpr int REF_LANES = 4;
+#ifdef FACTOR_TIMING
+#include <cstdio>
+__device__ unsigned long long g_ft[16];
+#define FT0 const long long ft0_ = clock64();
+#define FTA(i) if (threadIdx.x == 0) g_ft[i] += (unsigned long long)(clock64() - ft0_);
+#define FTM(i) if (threadIdx.x == 0) { const long long now_ = clock64(); g_ft[i] += (unsigned long long)(now_ - ftm_); ftm_ = now_; }
+#define FTM0 long long ftm_ = clock64();
+#else
+#define FT0
+#define FTA(i)
+#define FTM(i)
+#define FTM0
+#endif
 
 // One chain of a line (both chains of a line run concurrently, one per
 // half-warp h).  Chain position e = 0..m-1 is cell lo + e*step.
@@ -506,21 +519,50 @@ __device__ __forceinline__ void chain_ref_compose(const double *__restrict__ x, 
     // sl: lane within the half-warp; lanes 0..REF_LANES-1 compose one chunk each
     if (m < 2 * REF_LANES || sl >= REF_LANES) return;
     const int chunk = m / REF_LANES, base = sl * chunk;
-    int p = lo + base * step;
-    double a = SCALED ? mul_rn(-off[p], dr[p]) : mul_rn(-dr[p], off[p]);
-    double aa = a, cc = SCALED ? mul_rn(rhs[p], dr[p]) : x[p];
-    aw[base] = aa;
-    cw[base] = cc;
-    // (the prefix maps are separate shared-memory arrays: with the no-alias promise the operand loads
-    // of the next cells are issued ahead of this cell's dependent multiply-adds)
-#pragma unroll 4
-    for (int t = 1; t < chunk; t++) {
-        p += step;
-        a = SCALED ? mul_rn(-off[p], dr[p]) : mul_rn(-dr[p], off[p]);
-        aa = mul_rn(a, aa);
-        cc = add_rn(mul_rn(a, cc), SCALED ? mul_rn(rhs[p], dr[p]) : x[p]);
-        aw[base + t] = aa;
-        cw[base + t] = cc;
+    // Cells are walked four at a time; the operands of the next four are requested before the
+    // current four's dependent multiply-adds (the compiler does not move the loads above the
+    // prefix-map stores by itself once this is inlined), clamped to the chunk.
+    auto cell = [&](int t) { return lo + (base + (t < chunk ? t : chunk - 1)) * step; };
+    double o[4], d[4], r[4];
+    auto fetch = [&](int t0, double (&oo)[4], double (&dd)[4], double (&rr)[4]) {
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int p = cell(t0 + j);
+            oo[j] = off[p];
+            dd[j] = dr[p];
+            rr[j] = SCALED ? rhs[p] : x[p];
+        }
+    };
+    double aa, cc;
+    {
+        const int p = lo + base * step;
+        const double a = SCALED ? mul_rn(-off[p], dr[p]) : mul_rn(-dr[p], off[p]);
+        aa = a;
+        cc = SCALED ? mul_rn(rhs[p], dr[p]) : x[p];
+        aw[base] = aa;
+        cw[base] = cc;
+    }
+    fetch(1, o, d, r);
+#pragma unroll 1
+    for (int t0 = 1; t0 < chunk; t0 += 4) {
+        double on[4], dn[4], rn[4];
+        fetch(t0 + 4, on, dn, rn);
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            if (t0 + j < chunk) {
+                const double a = SCALED ? mul_rn(-o[j], d[j]) : mul_rn(-d[j], o[j]);
+                aa = mul_rn(a, aa);
+                cc = add_rn(mul_rn(a, cc), SCALED ? mul_rn(r[j], d[j]) : r[j]);
+                aw[base + t0 + j] = aa;
+                cw[base + t0 + j] = cc;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            o[j] = on[j];
+            d[j] = dn[j];
+            r[j] = rn[j];
+        }
     }
 }
 
@@ -556,7 +598,25 @@ __device__ __forceinline__ void chain_ref_finish(double *x, const double *dr, co
         car[REF_LANES] = carry;
     }
     __syncwarp();
-    for (int e = sl; e < REF_LANES * chunk; e += 16) x[lo + e * step] = add_rn(mul_rn(aw[e], car[e / chunk]), cw[e]);
+    // (chunk by chunk: the carry of a chunk is one value, no division per cell)
+#pragma unroll
+    for (int l = 0; l < REF_LANES; l++) {
+        const double cl = car[l];
+        const int e1 = (l + 1) * chunk;
+        // (four cells of this lane at a time, loads first)
+        for (int e = l * chunk + sl; e < e1; e += 64) {
+            double av[4], cv[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int ej = e + 16 * j < e1 ? e + 16 * j : e;
+                av[j] = aw[ej];
+                cv[j] = cw[ej];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+                if (e + 16 * j < e1) x[lo + (e + 16 * j) * step] = add_rn(mul_rn(av[j], cl), cv[j]);
+        }
+    }
     if (sl == 0) {  // remainder, sequential from the last carry
         double xp = car[REF_LANES];
         int p = lo + REF_LANES * chunk * step;
@@ -569,118 +629,191 @@ __device__ __forceinline__ void chain_ref_finish(double *x, const double *dr, co
     __syncwarp();
 }
 
-// _line_solve (ntd_solve.py:134-137) of one line of n cells by one warp:
-// x = T^-1 b with T's factor (mr, l1, u1).  All arrays line-local (index 0 =
-// first cell); x and b may live in global memory.  lsm: >= 2n doubles of smem
-// (prefix maps), car: 2 x (REF_LANES + 1) doubles of smem.
-static __device__ void line_solve_ref(double *x, const double *b, const double *mr, const double *l1, const double *u1,
-                               int n, double *lsm, double *car)
+// _line_solve (ntd_solve.py:134-137) of one line of n <= 32K cells by one warp:
+// x = T^-1 b with T's factor (mr, l1, u1; line-local global arrays).
+//
+// Everything a line touches is requested up front -- the factor, and whatever
+// the caller's right-hand side is made of (ldf: loads of a cell into a RawLine;
+// evf: RawLine -> rhs value) -- so a line costs ONE memory round trip;
+// the chains then walk shared memory, and wf(cell, x, RawLine) stores the
+// result.  (Before, the operands were read from global memory inside the
+// composition's sequential chunk walks and the callers' elementwise steps
+// around the solve were plain loops over the line whose loads could not pass
+// the previous iteration's store: ~11 serialised round trips per loop at
+// nx = 350.)  Same operations in the same order: bitwise the same result.
+// On return s_x(lsm, n) holds x and, with KEEP, s_b(lsm, n) the rhs; s_l /
+// s_u / s_mr still hold the line's factor.
+// lsm: 7n doubles of smem (prefix maps 2n, then mr, l1, u1, x, b); car: 2 x
+// (REF_LANES + 1) doubles of smem.
+struct RawLine {  // (references to one cell's slots of five register arrays; unused ones fold away)
+    double &a, &b, &c, &d, &e;
+};
+__device__ __forceinline__ double *s_mr_of(double *lsm, int n) { return lsm + 2 * n; }
+__device__ __forceinline__ double *s_l_of(double *lsm, int n) { return lsm + 3 * n; }
+__device__ __forceinline__ double *s_u_of(double *lsm, int n) { return lsm + 4 * n; }
+__device__ __forceinline__ double *s_x_of(double *lsm, int n) { return lsm + 5 * n; }
+__device__ __forceinline__ double *s_b_of(double *lsm, int n) { return lsm + 6 * n; }
+constexpr int LSM_PER_WARP = 7;  // x nx doubles
+
+template <int K, bool KEEP, class LF, class EF, class WF>
+static __device__ __forceinline__ void line_solve_ref(LF &&ldf, EF &&evf, WF &&wf, const double *mr, const double *l1,
+                                                      const double *u1, int n, double *lsm, double *car)
 {
     const int lane = threadIdx.x & 31, h = lane >> 4, sl = lane & 15;
     const int t = (n - 1) / 2;
+    FT0
+    double *s_mr = s_mr_of(lsm, n), *s_l = s_l_of(lsm, n), *s_u = s_u_of(lsm, n), *s_x = s_x_of(lsm, n);
+    double ra[K], rb[K], rc[K], rd[K], re[K];
+    FTM0
+    {
+        double v[3][K];
+        // (unconditional loads at a clamped cell: guarded loads end up in per-cell branches next to
+        // their stores, one memory round trip per cell instead of one per line)
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            const int c = min(lane + 32 * k, n - 1);
+            v[0][k] = mr[c];
+            v[1][k] = l1[c];
+            v[2][k] = u1[c];
+            ldf(c, RawLine{ra[k], rb[k], rc[k], rd[k], re[k]});
+        }
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            const int c = lane + 32 * k;
+            if (c < n) {
+                s_mr[c] = v[0][k];
+                s_l[c] = v[1][k];
+                s_u[c] = v[2][k];
+                const double r = evf(RawLine{ra[k], rb[k], rc[k], rd[k], re[k]});
+                s_x[c] = r;
+                if (KEEP) s_b_of(lsm, n)[c] = r;
+            }
+        }
+    }
+    __syncwarp();
+    FTM(9)
     // half 0: ascending chain over cells 0..t-1; half 1: descending n-1..t+1
     const int m = h == 0 ? t : n - 1 - t;
     const int lo = h == 0 ? 0 : n - 1, step = h == 0 ? 1 : -1;
     double *aw = lsm + (h == 0 ? 0 : 2 * t), *cw = aw + m;
     double *ch = car + h * (REF_LANES + 1);
-    // _line_lower (ntd_solve.py:107-121)
-    chain_ref_compose<true>(x, mr, h == 0 ? l1 : u1, b, lo, step, m, aw, cw, sl);
+    // _line_lower (ntd_solve.py:107-121); the rhs is consumed in place (x_e overwrites rhs_e)
+    chain_ref_compose<true>(nullptr, s_mr, h == 0 ? s_l : s_u, s_x, lo, step, m, aw, cw, sl);
     __syncwarp();
-    chain_ref_finish<true>(x, mr, h == 0 ? l1 : u1, b, lo, step, m, 0.0, aw, cw, ch, sl);
+    FTM(10)
+    chain_ref_finish<true>(s_x, s_mr, h == 0 ? s_l : s_u, s_x, lo, step, m, 0.0, aw, cw, ch, sl);
+    FTM(11)
     if (lane == 0) {
-        double acc = b[t];
-        if (t > 0) acc = sub_rn(acc, mul_rn(l1[t], x[t - 1]));
-        if (t < n - 1) acc = sub_rn(acc, mul_rn(u1[t], x[t + 1]));
-        x[t] = mul_rn(acc, mr[t]);
+        double acc = s_x[t];
+        if (t > 0) acc = sub_rn(acc, mul_rn(s_l[t], s_x[t - 1]));
+        if (t < n - 1) acc = sub_rn(acc, mul_rn(s_u[t], s_x[t + 1]));
+        s_x[t] = mul_rn(acc, s_mr[t]);
     }
     __syncwarp();
     // _line_upper (ntd_solve.py:124-131): outward from the twist
-    const double xt = x[t];
+    const double xt = s_x[t];
     const int lo2 = h == 0 ? t - 1 : t + 1, step2 = -step;
-    chain_ref_compose<false>(x, mr, h == 0 ? u1 : l1, nullptr, lo2, step2, m, aw, cw, sl);
+    FTM(12)
+    chain_ref_compose<false>(s_x, s_mr, h == 0 ? s_u : s_l, nullptr, lo2, step2, m, aw, cw, sl);
     __syncwarp();
-    chain_ref_finish<false>(x, mr, h == 0 ? u1 : l1, nullptr, lo2, step2, m, xt, aw, cw, ch, sl);
+    FTM(13)
+    chain_ref_finish<false>(s_x, s_mr, h == 0 ? s_u : s_l, nullptr, lo2, step2, m, xt, aw, cw, ch, sl);
+    FTM(14)
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const int c = lane + 32 * k;
+        if (c < n) wf(c, s_x[c], RawLine{ra[k], rb[k], rc[k], rd[k], re[k]});
+    }
+    __syncwarp();
+    FTM(15)
+    FTA(2)
 }
 
 // _plane_solve (ntd_solve.py:140-185) of factored plane (F at offset pb) in
 // the reference's order, by a warp pair (w2 = 0: lines 0..t2, w2 = 1: lines
 // t2+1..ny-1; the two level-2 halves only meet at the twist line).
-// rhs: plane-local right-hand side (read only); X: solution; B, XS, BS:
-// plane-local scratch (B receives the consumed copy of rhs).
-static __device__ void plane_solve_ref(const FactorPtrs &F, i64 pb, const double *rhs, double *X, double *B, double *XS,
-                                double *BS, int nx, int ny, int w2, int bar_id, double *lsm, double *car)
+// rhs: plane-local right-hand side (read only); X: solution.  The reference's
+// scratch copies (b, xs, bs) live in registers / shared memory per line: each
+// line's right-hand side is formed from rhs, the coupling and the neighbour
+// line as the line is staged, and the upper sweep's x -= xs is the solve's
+// write-back.
+template <int K>
+static __device__ void plane_solve_ref(const FactorPtrs &F, i64 pb, const double *rhs, double *X, int nx, int ny,
+                                       int w2, int bar_id, double *lsm, double *car)
 {
-    const int lane = threadIdx.x & 31;
     const int t2 = (ny - 1) / 2;
     const double *mr = F.mr + pb, *l1 = F.l1 + pb, *u1 = F.u1 + pb, *l2 = F.l2 + pb, *u2 = F.u2 + pb;
-    const i64 q0 = w2 == 0 ? 0 : (i64)(t2 + 1) * nx, q1 = w2 == 0 ? (i64)(t2 + 1) * nx : (i64)ny * nx;
-    for (i64 k = q0 + lane; k < q1; k += 32) B[k] = rhs[k];
-    __syncwarp();
-    auto lsolve = [&](double *xx, const double *bb, i64 off) {
-        line_solve_ref(xx + off, bb + off, mr + off, l1 + off, u1 + off, nx, lsm, car);
+    // lower-sweep line at offset s: rhs - cpl * X[nb] (first line of the sweep: rhs)
+    auto lower = [&](i64 s, const double *cpl, i64 nb, bool first) {
+        line_solve_ref<K, false>(
+            [&](int c, const RawLine &r) {
+                r.a = rhs[s + c];
+                if (!first) {
+                    r.b = cpl[s + c];
+                    r.c = X[s + c + nb];
+                }
+            },
+            [&](const RawLine &r) { return first ? r.a : sub_rn(r.a, mul_rn(r.b, r.c)); },
+            [&](int c, double v, const RawLine &) { X[s + c] = v; }, mr + s, l1 + s, u1 + s, nx, lsm, car);
+    };
+    // upper-sweep line: xs = T^-1 (cpl * X[nb]); x -= xs
+    auto upper = [&](i64 s, const double *cpl, i64 nb) {
+        line_solve_ref<K, false>(
+            [&](int c, const RawLine &r) {
+                r.a = cpl[s + c];
+                r.b = X[s + c + nb];
+                r.c = X[s + c];
+            },
+            [&](const RawLine &r) { return mul_rn(r.a, r.b); },
+            [&](int c, double v, const RawLine &r) { X[s + c] = sub_rn(r.c, v); }, mr + s, l1 + s, u1 + s, nx, lsm,
+            car);
     };
     // level-2 lower sweep, ends inward (ntd_solve.py:147-171)
     if (w2 == 0) {
-        for (int q = 0; q < t2; q++) {
-            const i64 s = (i64)q * nx;
-            if (q > 0) {
-                for (int c = lane; c < nx; c += 32) B[s + c] = sub_rn(B[s + c], mul_rn(l2[s + c], X[s + c - nx]));
-                __syncwarp();
-            }
-            lsolve(X, B, s);
-        }
+        for (int q = 0; q < t2; q++) lower((i64)q * nx, l2, -nx, q == 0);
     } else {
-        for (int q = ny - 1; q > t2; q--) {
-            const i64 s = (i64)q * nx;
-            if (q < ny - 1) {
-                for (int c = lane; c < nx; c += 32) B[s + c] = sub_rn(B[s + c], mul_rn(u2[s + c], X[s + c + nx]));
-                __syncwarp();
-            }
-            lsolve(X, B, s);
-        }
+        for (int q = ny - 1; q > t2; q--) lower((i64)q * nx, u2, nx, q == ny - 1);
     }
     __threadfence_block();
     named_bar(bar_id, 64);
     // twist line (ntd_solve.py:172-177)
     if (w2 == 0) {
         const i64 s = (i64)t2 * nx;
-        for (int c = lane; c < nx; c += 32) {
-            double v = B[s + c];
-            if (t2 > 0) v = sub_rn(v, mul_rn(l2[s + c], X[s + c - nx]));
-            if (t2 < ny - 1) v = sub_rn(v, mul_rn(u2[s + c], X[s + c + nx]));
-            B[s + c] = v;
-        }
-        __syncwarp();
-        lsolve(X, B, s);
+        const bool hm = t2 > 0, hp = t2 < ny - 1;
+        line_solve_ref<K, false>(
+            [&](int c, const RawLine &r) {
+                r.a = rhs[s + c];
+                if (hm) {
+                    r.b = l2[s + c];
+                    r.c = X[s + c - nx];
+                }
+                if (hp) {
+                    r.d = u2[s + c];
+                    r.e = X[s + c + nx];
+                }
+            },
+            [&](const RawLine &r) {
+                double v = r.a;
+                if (hm) v = sub_rn(v, mul_rn(r.b, r.c));
+                if (hp) v = sub_rn(v, mul_rn(r.d, r.e));
+                return v;
+            },
+            [&](int c, double v, const RawLine &) { X[s + c] = v; }, mr + s, l1 + s, u1 + s, nx, lsm, car);
     }
     __threadfence_block();
     named_bar(bar_id, 64);
     // level-2 upper sweep, twist outward (ntd_solve.py:178-185)
     if (w2 == 0) {
-        for (int q = t2 - 1; q >= 0; q--) {
-            const i64 s = (i64)q * nx;
-            for (int c = lane; c < nx; c += 32) BS[s + c] = mul_rn(u2[s + c], X[s + c + nx]);
-            __syncwarp();
-            lsolve(XS, BS, s);
-            for (int c = lane; c < nx; c += 32) X[s + c] = sub_rn(X[s + c], XS[s + c]);
-            __syncwarp();
-        }
+        for (int q = t2 - 1; q >= 0; q--) upper((i64)q * nx, u2, nx);
     } else {
-        for (int q = t2 + 1; q < ny; q++) {
-            const i64 s = (i64)q * nx;
-            for (int c = lane; c < nx; c += 32) BS[s + c] = mul_rn(l2[s + c], X[s + c - nx]);
-            __syncwarp();
-            lsolve(XS, BS, s);
-            for (int c = lane; c < nx; c += 32) X[s + c] = sub_rn(X[s + c], XS[s + c]);
-            __syncwarp();
-        }
+        for (int q = t2 + 1; q < ny; q++) upper((i64)q * nx, l2, -nx);
     }
     __threadfence_block();
     named_bar(bar_id, 64);
 }
 
 // Per-pair global scratch (plane-local, nxy each).
-enum { S_PC0 = 0, S_PC1 = 5, S_W = 10, S_YL, S_BETA, S_QD, S_TDW, S_XW, S_BW, S_PER_PAIR };
+enum { S_PC0 = 0, S_PC1 = 5, S_W = 10, S_BETA, S_QD, S_TDW, S_PER_PAIR };
 
 struct PairScratch {
     double *base;
@@ -713,6 +846,7 @@ static __device__ int line_factor_warp(const double *__restrict__ td, const doub
 {
     const int lane = threadIdx.x & 31;
     const int t = (nx - 1) / 2;
+    FT0
     for (int c = lane; c < nx; c += 32) {
         sd[c] = td[c];
         double p = 0.0;
@@ -731,8 +865,15 @@ static __device__ int line_factor_warp(const double *__restrict__ td, const doub
         const int cnt = asc ? t : nx - 1 - t, stp = asc ? 1 : -1;
         int i = asc ? 0 : nx - 1;
         double m = 0.0;
+        // (the next cell's operands are read before this cell's dependent multiply, subtract and
+        // reciprocal, so their shared-memory latency is off the recurrence; the line has a twist cell
+        // past each walk, so the look-ahead stays inside the line)
+        double dn = sd[i], cn = sc[i];
         for (int it = 0; it < cnt; it++, i += stp) {
-            const double piv = sub_rn(sd[i], mul_rn(sc[i], m));
+            const double d = dn, cc = cn;
+            dn = sd[i + stp];
+            cn = sc[i + stp];
+            const double piv = sub_rn(d, mul_rn(cc, m));
             if (bad < 0 && (piv == 0.0 || !isfinite(piv))) bad = i;
             m = __drcp_rn(piv);  // == 1.0 / piv (both correctly rounded)
             sm[i] = m;
@@ -758,49 +899,74 @@ static __device__ int line_factor_warp(const double *__restrict__ td, const doub
     if (badt >= 0) return badt;
     for (int c = lane; c < nx; c += 32) mr[c] = sm[c];
     __syncwarp();
+    FTA(7)
     return -1;
 }
 
 // _correct_line (ntd_factor.py:113-144): line q corrected through factored
 // line m.  P* are the plane's corrected bands (plane-local), L1G/U1G/MRG the
-// plane's factor outputs, TDW/XW/BW scratch.  Returns -1 or bad plane-local row.
+// plane's factor outputs.  w = T_m^-1 u, beta and the neighbours' beta / u
+// stay in shared memory (line_solve_ref leaves x, the rhs and line m's l1 / u1
+// there).  Returns -1 or bad plane-local row.
 template <int K>
 __device__ i64 correct_line_warp(int q, int m, const double *P_l2, const double *P_u2, double *TDW, double *L1G,
-                                 double *U1G, const double *MRG, double *XW, double *BW, int nx, double *lsm,
-                                 double *car)
+                                 double *U1G, const double *MRG, int nx, double *lsm, double *car)
 {
     const int lane = threadIdx.x & 31;
     const i64 sq = (i64)q * nx, sm = (i64)m * nx;
+    FT0
     const double *src = m < q ? P_u2 : P_l2;
-    for (int c = lane; c < nx; c += 32) BW[sm + c] = src[sm + c];
-    __syncwarp();
-    line_solve_ref(XW + sm, BW + sm, MRG + sm, L1G + sm, U1G + sm, nx, lsm, car);
-    __syncwarp();
+    line_solve_ref<K, true>(
+        [&](int c, const RawLine &r) { r.a = src[sm + c]; },
+        [&](const RawLine &r) { return r.a; }, [&](int, double, const RawLine &) {}, MRG + sm, L1G + sm, U1G + sm, nx,
+        lsm, car);
+    double *s_w = s_x_of(lsm, nx), *s_uu = s_b_of(lsm, nx);
+    const double *s_l1m = s_l_of(lsm, nx), *s_u1m = s_u_of(lsm, nx);
+    // what the update reads from global memory, requested before the divisions below
+    const double *rsp = m < q ? P_l2 : P_u2;
+    double rs[K], tdm[K], tdq[K], l1q[K], u1q[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const int c = min(lane + 32 * k, nx - 1);
+        rs[k] = rsp[sq + c];
+        tdm[k] = TDW[sm + c];
+        tdq[k] = TDW[sq + c];
+        l1q[k] = L1G[sq + c];
+        u1q[k] = U1G[sq + c];
+    }
     // beta = w/u where u != 0 (first non-finite -> error)
     int badk = 0x7fffffff;
-    for (int c = lane; c < nx; c += 32) {
-        double u = BW[sm + c];
-        double bet = u != 0.0 ? XW[sm + c] / u : 0.0;
-        if (!isfinite(bet) && c < badk) badk = c;
-        XW[sm + c] = bet;
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const int c = lane + 32 * k;
+        if (c < nx) {
+            const double u = s_uu[c];
+            const double bet = u != 0.0 ? s_w[c] / u : 0.0;
+            if (!isfinite(bet) && c < badk) badk = c;
+            s_w[c] = bet;
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) badk = min(badk, __shfl_xor_sync(FULL_MASK, badk, o));
     __syncwarp();
     if (badk != 0x7fffffff) return sm + badk;
-    for (int c = lane; c < nx; c += 32) {
-        double rs = m < q ? P_l2[sq + c] : P_u2[sq + c];
-        double bet = XW[sm + c];
-        double inner = sub_rn(mul_rn(2.0, bet), mul_rn(mul_rn(bet, TDW[sm + c]), bet));
-        TDW[sq + c] = sub_rn(TDW[sq + c], mul_rn(mul_rn(rs, inner), BW[sm + c]));
-        if (c >= 1)
-            L1G[sq + c] = add_rn(L1G[sq + c], mul_rn(mul_rn(mul_rn(mul_rn(rs, bet), L1G[sm + c]), XW[sm + c - 1]),
-                                                     BW[sm + c - 1]));
-        if (c + 1 < nx)
-            U1G[sq + c] = add_rn(U1G[sq + c], mul_rn(mul_rn(mul_rn(mul_rn(rs, bet), U1G[sm + c]), XW[sm + c + 1]),
-                                                     BW[sm + c + 1]));
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const int c = lane + 32 * k;
+        if (c < nx) {
+            const double bet = s_w[c];
+            const double inner = sub_rn(mul_rn(2.0, bet), mul_rn(mul_rn(bet, tdm[k]), bet));
+            TDW[sq + c] = sub_rn(tdq[k], mul_rn(mul_rn(rs[k], inner), s_uu[c]));
+            if (c >= 1)
+                L1G[sq + c] = add_rn(l1q[k], mul_rn(mul_rn(mul_rn(mul_rn(rs[k], bet), s_l1m[c]), s_w[c - 1]),
+                                                    s_uu[c - 1]));
+            if (c + 1 < nx)
+                U1G[sq + c] = add_rn(u1q[k], mul_rn(mul_rn(mul_rn(mul_rn(rs[k], bet), s_u1m[c]), s_w[c + 1]),
+                                                    s_uu[c + 1]));
+        }
     }
     __syncwarp();
+    FTA(8)
     return -1;
 }
 
@@ -821,7 +987,7 @@ __device__ void factor_plane_pair(const FactorCtx &c, i64 pb, const double *P[5]
     const int lane = threadIdx.x & 31;
     const int nx = c.nx, ny = c.ny, t2 = (ny - 1) / 2;
     double *L1G = c.pre + pb, *U1G = c.pre + c.n + pb, *MRG = c.pre + 6 * c.n + pb;
-    double *TDW = S.at(S_TDW), *XW = S.at(S_XW), *BW = S.at(S_BW);
+    double *TDW = S.at(S_TDW);
     double *sd = lsm, *sc = lsm + nx, *sm = lsm + 2 * nx;
     auto init_line = [&](int q) {
         i64 sq = (i64)q * nx;
@@ -840,8 +1006,7 @@ __device__ void factor_plane_pair(const FactorCtx &c, i64 pb, const double *P[5]
         int q = w2 == 0 ? i : ny - 1 - i;
         init_line(q);
         if (i > 0) {
-            i64 st = correct_line_warp<K>(q, w2 == 0 ? q - 1 : q + 1, P[3], P[4], TDW, L1G, U1G, MRG, XW, BW, nx,
-                                          lsm, car);
+            i64 st = correct_line_warp<K>(q, w2 == 0 ? q - 1 : q + 1, P[3], P[4], TDW, L1G, U1G, MRG, nx, lsm, car);
             if (st >= 0) {
                 mcode = 2;
                 mrow = st;
@@ -876,11 +1041,11 @@ __device__ void factor_plane_pair(const FactorCtx &c, i64 pb, const double *P[5]
         i64 st = -1;
         int code = 0;
         if (t2 > 0) {
-            st = correct_line_warp<K>(q, q - 1, P[3], P[4], TDW, L1G, U1G, MRG, XW, BW, nx, lsm, car);
+            st = correct_line_warp<K>(q, q - 1, P[3], P[4], TDW, L1G, U1G, MRG, nx, lsm, car);
             if (st >= 0) code = 2;
         }
         if (!code && t2 < ny - 1) {
-            st = correct_line_warp<K>(q, q + 1, P[3], P[4], TDW, L1G, U1G, MRG, XW, BW, nx, lsm, car);
+            st = correct_line_warp<K>(q, q + 1, P[3], P[4], TDW, L1G, U1G, MRG, nx, lsm, car);
             if (st >= 0) code = 2;
         }
         if (!code) {
@@ -911,9 +1076,13 @@ __device__ void correct_from_pair(const FactorCtx &c, int p, int m, double *P[5]
     const double *useg = (m < p ? c.a + 6 * n : c.a) + (i64)m * nxy;  // u3 | l3 = copies of A's +-nxy
     const double *rowscale = (m < p ? c.a : c.a + 6 * n) + (i64)p * nxy;
     double *W = S.at(S_W), *BETA = S.at(S_BETA), *QD = S.at(S_QD);
-    // _apply_factored_plane (ntd_factor.py:336-348): w = nested solve of plane
-    // m on a copy of u (BETA / QD serve as the solve's scratch planes)
-    plane_solve_ref(F, (i64)m * nxy, useg, W, S.at(S_YL), BETA, QD, c.nx, c.ny, w2, bar_id, lsm, car);
+    // _apply_factored_plane (ntd_factor.py:336-348): w = nested solve of plane m on u
+    {
+        FT0
+        plane_solve_ref<K>(F, (i64)m * nxy, useg, W, c.nx, c.ny, w2, bar_id, lsm, car);
+        FTA(1)
+    }
+    FT0
     // beta (_beta_from :242-249), qw (_plane_band_action :266-274), qd shift (:393-399)
     int fb = 0, fq = 0;
     // The plane loops below are elementwise over distinct scratch planes, walked by the pair's 64
@@ -925,7 +1094,7 @@ __device__ void correct_from_pair(const FactorCtx &c, int p, int m, double *P[5]
                      *__restrict__ q3 = Q[3], *__restrict__ q4 = Q[4];
         const double *__restrict__ us = useg, *__restrict__ Wr = W;
         double *__restrict__ Bo = BETA, *__restrict__ Qo = QD;
-#pragma unroll 2
+#pragma unroll 4
         for (i64 k = tid; k < nxy; k += 64) {
             double u = us[k], w = Wr[k];
             double bet = u != 0.0 ? w / u : 0.0;
@@ -945,6 +1114,7 @@ __device__ void correct_from_pair(const FactorCtx &c, int p, int m, double *P[5]
     if (fb) flag[0] = 1;
     if (fq) flag[1] = 1;
     named_bar(bar_id, 64);
+    FTA(3)
     if (flag[0] || flag[1]) {
         if (tid == 0) set_err(ecode, eplane, erow, flag[0] ? 2 : 3, p, -1);
         named_bar(bar_id, 64);
@@ -952,13 +1122,14 @@ __device__ void correct_from_pair(const FactorCtx &c, int p, int m, double *P[5]
     }
     // _plane_correction (ntd_factor.py:222-239)
     {
+        FT0
         double *__restrict__ p0 = P[0], *__restrict__ p1 = P[1], *__restrict__ p2 = P[2], *__restrict__ p3 = P[3],
                             *__restrict__ p4 = P[4];
         const double *__restrict__ q1 = Q[1], *__restrict__ q2 = Q[2], *__restrict__ q3 = Q[3],
                      *__restrict__ q4 = Q[4];
         const double *__restrict__ us = useg, *__restrict__ rsc = rowscale, *__restrict__ Br = BETA,
                      *__restrict__ Qr = QD;
-#pragma unroll 2
+#pragma unroll 4
         for (i64 k = tid; k < nxy; k += 64) {
             double rs = rsc[k], bet = Br[k];
             double inner = sub_rn(mul_rn(2.0, bet), mul_rn(mul_rn(bet, Qr[k]), bet));
@@ -969,8 +1140,9 @@ __device__ void correct_from_pair(const FactorCtx &c, int p, int m, double *P[5]
             if (k >= nx) p3[k] = add_rn(p3[k], mul_rn(mul_rn(mul_rn(rb, q3[k]), Br[k - nx]), us[k - nx]));
             if (k + nx < nxy) p4[k] = add_rn(p4[k], mul_rn(mul_rn(mul_rn(rb, q4[k]), Br[k + nx]), us[k + nx]));
         }
+        named_bar(bar_id, 64);
+        FTA(4)
     }
-    named_bar(bar_id, 64);
 }
 
 // plane_bands_of (ntd_factor.py:372-376): d, -1, +1, -nx, +nx of plane p
@@ -981,6 +1153,7 @@ static __device__ void load_plane_bands(const FactorCtx &c, int p, double *P[5],
     double *__restrict__ p0 = P[0], *__restrict__ p1 = P[1], *__restrict__ p2 = P[2], *__restrict__ p3 = P[3],
                         *__restrict__ p4 = P[4];
     const double *__restrict__ a = c.a + pb;
+    FT0
 #pragma unroll 4
     for (i64 k = tid; k < c.nxy; k += 64) {
         p0[k] = a[3 * n + k];
@@ -990,6 +1163,7 @@ static __device__ void load_plane_bands(const FactorCtx &c, int p, double *P[5],
         p4[k] = a[5 * n + k];
     }
     named_bar(bar_id, 64);
+    FTA(0)
 }
 
 // factor_one (ntd_factor.py:406-419)
@@ -1000,6 +1174,7 @@ __device__ void factor_one_pair(const FactorCtx &c, int p, double *P[5], const P
 {
     const int tid = threadIdx.x & 63;
     const i64 pb = (i64)p * c.nxy, n = c.n;
+    FT0
     {
         const double *__restrict__ p3 = P[3], *__restrict__ p4 = P[4];
         double *__restrict__ o2 = c.pre + 2 * n + pb, *__restrict__ o3 = c.pre + 3 * n + pb;
@@ -1010,15 +1185,20 @@ __device__ void factor_one_pair(const FactorCtx &c, int p, double *P[5], const P
         }
     }
     named_bar(bar_id, 64);
+    FTA(5)
     const double *Pc[5] = {P[0], P[1], P[2], P[3], P[4]};
-    factor_plane_pair<K>(c, pb, Pc, S, w2, bar_id, ecode, eplane, erow, p, lsm, wbad, car);
+    {
+        FT0
+        factor_plane_pair<K>(c, pb, Pc, S, w2, bar_id, ecode, eplane, erow, p, lsm, wbad, car);
+        FTA(6)
+    }
 }
 
 template <int K>
 __global__ void __launch_bounds__(128) k_ntd_factor(const double *__restrict__ a, double *pre, double *work,
                                                     int64_t *status, int nx, int ny, int nz)
 {
-    extern __shared__ double lsm_all[];  // 4 warps x 3 x nx
+    extern __shared__ double lsm_all[];  // 4 warps x LSM_PER_WARP x nx (line_solve_ref)
     __shared__ double ex[2][2 * 2 * (32 * K + 1)];
     __shared__ int ecode_s[2];
     __shared__ i64 eplane_s[2], erow_s[2];
@@ -1037,7 +1217,7 @@ __global__ void __launch_bounds__(128) k_ntd_factor(const double *__restrict__ a
     c.ny = ny;
     c.nz = nz;
     const int warp = __shfl_sync(FULL_MASK, (int)(threadIdx.x >> 5), 0), pair = warp >> 1, w2 = warp & 1, bar = 1 + pair;
-    double *lsm = lsm_all + warp * 3 * nx;
+    double *lsm = lsm_all + warp * LSM_PER_WARP * nx;
     double *car = car_s[warp];
     if (threadIdx.x < 2) {
         ecode_s[threadIdx.x] = 0;
@@ -1132,6 +1312,17 @@ __global__ void __launch_bounds__(128) k_ntd_factor(const double *__restrict__ a
         status[sys * 3 + 0] = h >= 0 ? ecode_s[h] : 0;
         status[sys * 3 + 1] = h >= 0 ? eplane_s[h] : -1;
         status[sys * 3 + 2] = h >= 0 ? erow_s[h] : -1;
+#ifdef FACTOR_TIMING
+        if (sys == 0)
+            printf("factor timing (warp 0, Mcycles): load_bands %llu  plane_solve %llu  [line_solve %llu]  beta/qd %llu  "
+                   "plane_corr %llu  copy %llu  factor_plane %llu  [line_factor %llu  correct_line %llu]\n",
+                   g_ft[0] >> 20, g_ft[1] >> 20, g_ft[2] >> 20, g_ft[3] >> 20, g_ft[4] >> 20, g_ft[5] >> 20,
+                   g_ft[6] >> 20, g_ft[7] >> 20, g_ft[8] >> 20);
+        if (sys == 0)
+            printf("  line_solve parts: stage %llu  compose1 %llu  finish1 %llu  twist %llu  compose2 %llu  finish2 %llu  "
+                   "writeback %llu\n", g_ft[9] >> 20, g_ft[10] >> 20, g_ft[11] >> 20, g_ft[12] >> 20, g_ft[13] >> 20,
+                   g_ft[14] >> 20, g_ft[15] >> 20);
+#endif
     }
 }
 
@@ -1156,7 +1347,7 @@ int launch_factor_k(const double *a, double *pre, double *work, int64_t *status,
     int launch_factor_k<K>(const double *a, double *pre, double *work, int64_t *status, int nx, int ny, int nz,    \
                            i64 batch, cudaStream_t st)                                                             \
     {                                                                                                              \
-        size_t smem = sizeof(double) * 4 * 3 * (size_t)nx;                                                        \
+        size_t smem = sizeof(double) * 4 * LSM_PER_WARP * (size_t)nx;                                             \
         cudaError_t e = cudaFuncSetAttribute(k_ntd_factor<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                                              (int)(smem > 48 * 1024 ? smem : 48 * 1024));                          \
         if (e != cudaSuccess) {                                                                                    \

@@ -7,7 +7,11 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1909_09771_b200 import problems  # noqa: E402
+from paper_1909_09771_b200 import _lib  # noqa: E402
 from paper_1909_09771_b200 import device as D  # noqa: E402
+
+if os.environ.get("VARIANT_LIB"):
+    _lib.LIB_PATH = os.environ["VARIANT_LIB"]
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 nx, ny, nz = problems.CONFIGS[cfg]["grid"]
