@@ -491,6 +491,7 @@ __global__ void __launch_bounds__(128) k_ntd_apply(const double *__restrict__ pr
 // walked sequentially), every operation exactly rounded in the reference's
 // order.  The resulting factor is bitwise equal to the reference's.
 constexpr int REF_LANES = 4;
+static_assert(REF_LANES == 4, "chain_ref_finish picks among four chunk carries");
 #ifdef FACTOR_TIMING
 #include <cstdio>
 __device__ unsigned long long g_ft[16];
@@ -521,40 +522,51 @@ __device__ __forceinline__ void chain_ref_compose(const double *__restrict__ x, 
     const int chunk = m / REF_LANES, base = sl * chunk;
     // Cells are walked four at a time; the operands of the next four are requested before the
     // current four's dependent multiply-adds (the compiler does not move the loads above the
-    // prefix-map stores by itself once this is inlined), clamped to the chunk.
-    auto cell = [&](int t) { return lo + (base + (t < chunk ? t : chunk - 1)) * step; };
-    double o[4], d[4], r[4];
-    auto fetch = [&](int t0, double (&oo)[4], double (&dd)[4], double (&rr)[4]) {
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-            const int p = cell(t0 + j);
-            oo[j] = off[p];
-            dd[j] = dr[p];
-            rr[j] = SCALED ? rhs[p] : x[p];
-        }
-    };
+    // prefix-map stores by itself once this is inlined).  Running pointers: po/pd/pr at the batch's
+    // first cell, pa/pc at its prefix-map slots; a batch past the chunk's end re-reads the last cell.
+    const double *po = off + (lo + base * step), *pd = dr + (lo + base * step);
+    const double *pr = (SCALED ? rhs : x) + (lo + base * step);
+    double *pa = aw + base, *pc = cw + base;
     double aa, cc;
     {
-        const int p = lo + base * step;
-        const double a = SCALED ? mul_rn(-off[p], dr[p]) : mul_rn(-dr[p], off[p]);
+        const double a = SCALED ? mul_rn(-po[0], pd[0]) : mul_rn(-pd[0], po[0]);
         aa = a;
-        cc = SCALED ? mul_rn(rhs[p], dr[p]) : x[p];
-        aw[base] = aa;
-        cw[base] = cc;
+        cc = SCALED ? mul_rn(pr[0], pd[0]) : pr[0];
+        pa[0] = aa;
+        pc[0] = cc;
     }
-    fetch(1, o, d, r);
-#pragma unroll 1
-    for (int t0 = 1; t0 < chunk; t0 += 4) {
-        double on[4], dn[4], rn[4];
-        fetch(t0 + 4, on, dn, rn);
+    double o[4], d[4], r[4];
+    auto fetch = [&](int left, const double *qo, const double *qd, const double *qr, double (&oo)[4], double (&dd)[4],
+                     double (&rr)[4]) {  // left: cells of the chunk from qo on (>= 1)
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-            if (t0 + j < chunk) {
+            const int e = (j < left ? j : left - 1) * step;
+            oo[j] = qo[e];
+            dd[j] = qd[e];
+            rr[j] = qr[e];
+        }
+    };
+    int left = chunk - 1;  // cells not yet composed
+    po += step;
+    pd += step;
+    pr += step;
+    pa += 1;
+    pc += 1;
+    if (left > 0) fetch(left, po, pd, pr, o, d, r);
+#pragma unroll 1
+    for (; left > 0; left -= 4) {
+        double on[4], dn[4], rn[4];
+        const int nleft = left > 4 ? left - 4 : 1;
+        const int adv4 = left > 4 ? 4 * step : 0;
+        fetch(nleft, po + adv4, pd + adv4, pr + adv4, on, dn, rn);
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            if (j < left) {
                 const double a = SCALED ? mul_rn(-o[j], d[j]) : mul_rn(-d[j], o[j]);
                 aa = mul_rn(a, aa);
                 cc = add_rn(mul_rn(a, cc), SCALED ? mul_rn(r[j], d[j]) : r[j]);
-                aw[base + t0 + j] = aa;
-                cw[base + t0 + j] = cc;
+                pa[j] = aa;
+                pc[j] = cc;
             }
         }
 #pragma unroll
@@ -563,6 +575,11 @@ __device__ __forceinline__ void chain_ref_compose(const double *__restrict__ x, 
             d[j] = dn[j];
             r[j] = rn[j];
         }
+        po += 4 * step;
+        pd += 4 * step;
+        pr += 4 * step;
+        pa += 4;
+        pc += 4;
     }
 }
 
@@ -598,23 +615,30 @@ __device__ __forceinline__ void chain_ref_finish(double *x, const double *dr, co
         car[REF_LANES] = carry;
     }
     __syncwarp();
-    // (chunk by chunk: the carry of a chunk is one value, no division per cell)
-#pragma unroll
-    for (int l = 0; l < REF_LANES; l++) {
-        const double cl = car[l];
-        const int e1 = (l + 1) * chunk;
-        // (four cells of this lane at a time, loads first)
-        for (int e = l * chunk + sl; e < e1; e += 64) {
+    {
+        // cells e = sl, sl + 16, ... of the composed part, four at a time, loads first; the carry of a
+        // cell's chunk is picked by comparisons (no division per cell)
+        const double c0 = car[0], c1 = car[1], c2 = car[2], c3 = car[3];
+        const int total = REF_LANES * chunk;
+        const double *pa = aw + sl, *pc = cw + sl;
+        double *px = x + (lo + sl * step);
+#pragma unroll 1
+        for (int e = sl; e < total; e += 64, pa += 64, pc += 64, px += 64 * step) {
             double av[4], cv[4];
 #pragma unroll
             for (int j = 0; j < 4; j++) {
-                const int ej = e + 16 * j < e1 ? e + 16 * j : e;
-                av[j] = aw[ej];
-                cv[j] = cw[ej];
+                const int o16 = e + 16 * j < total ? 16 * j : 0;
+                av[j] = pa[o16];
+                cv[j] = pc[o16];
             }
 #pragma unroll
-            for (int j = 0; j < 4; j++)
-                if (e + 16 * j < e1) x[lo + (e + 16 * j) * step] = add_rn(mul_rn(av[j], cl), cv[j]);
+            for (int j = 0; j < 4; j++) {
+                const int ej = e + 16 * j;
+                if (ej < total) {
+                    const double cl = ej < chunk ? c0 : ej < 2 * chunk ? c1 : ej < 3 * chunk ? c2 : c3;
+                    px[16 * j * step] = add_rn(mul_rn(av[j], cl), cv[j]);
+                }
+            }
         }
     }
     if (sl == 0) {  // remainder, sequential from the last carry
